@@ -1,0 +1,224 @@
+/*
+ * bode.h -- C ABI of libbode.so, the B200 (sm_100a) batched adaptive ODE
+ * solver behind the batchode / torchode-style Python facade.
+ *
+ * Plain C: pointers, sizes and PODs only (no torch or CUDA types in the
+ * signatures; streams travel as void*).  Every entry point replaces one
+ * function of the reference's solve path (reference = /root/reference,
+ * package ``batchode``, paths relative to pkg/src/batchode/):
+ *
+ *   bode_solve / bode_solve_host  <- solve()            solver.py:352-369
+ *                                    BatchSolver.__init__/run/solution
+ *                                                       solver.py:148-206,324-349
+ *                                    (whole loop: step_once solver.py:208-282,
+ *                                     _emit solver.py:284-322)
+ *   bode_rk_step                  <- Stepper.step / rk_step  stepper.py:54-110,142-152
+ *   bode_interpolate              <- Stepper.interpolate / interpolate
+ *                                                       stepper.py:112-139,155-165
+ *   bode_error_norm               <- error_norm         controller.py:120-142
+ *   bode_adapt_step               <- adapt_step         controller.py:200-238
+ *   bode_initial_step             <- initial_step       controller.py:145-197
+ *
+ * Error behaviour mirrors the reference: invalid arguments (the cases where
+ * batchode raises ValueError) return BODE_EINVAL with a message in
+ * bode_last_error(); numerical failure is never an error code, it is a
+ * per-instance status (SolveStatus, solver.py:45-50).
+ *
+ * Memory: the caller owns every buffer, including the workspace
+ * (bode_workspace_size); the library allocates nothing persistent.  All
+ * device entry points are stream-ordered and asynchronous; bode_solve_host
+ * is the synchronous host-buffer convenience used for end-to-end timing.
+ */
+#ifndef BODE_H_
+#define BODE_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define BODE_ABI_VERSION 1
+
+/* return codes */
+#define BODE_OK 0
+#define BODE_EINVAL 1       /* invalid argument (reference: ValueError) */
+#define BODE_ECUDA 2        /* CUDA runtime / launch failure */
+#define BODE_EUNSUPPORTED 3 /* valid request this build does not implement */
+
+/* per-instance status codes == batchode.SolveStatus (solver.py:45-50) */
+#define BODE_RUNNING 0
+#define BODE_SUCCESS 1
+#define BODE_MAX_STEPS_EXCEEDED 2
+#define BODE_STEP_UNDERFLOW 3
+#define BODE_INFINITE_DYNAMICS 4
+
+/* methods (tableau.py:102 dopri5, :152 tsit5; heun per SURVEY.md 8(b)) */
+#define BODE_METHOD_DOPRI5 0
+#define BODE_METHOD_TSIT5 1
+#define BODE_METHOD_HEUN 2
+
+/* registered dynamics (the reference takes any NumPy callable f(t, y),
+ * stepper.py:19-20; a device solver needs them compiled in).  Parameter
+ * slots p0..p7 per dynamics; slot k is per-instance when bit k of
+ * inst_mask is set (read from inst_params, row-major n x popcount(mask)),
+ * else shared_params[k].
+ *   VDP        d=2  p0=mu                         (problems.py:41-50)
+ *   LORENZ     d=3  p0=sigma p1=rho p2=beta
+ *   ZERO       any  f=0
+ *   CONST      any  p0=c                          f=c
+ *   LINEAR     any  p0=lam                        f=lam*y
+ *   LINEAR_COS any  p0=lam p1=amp p2=omega        f=lam*y + amp*cos(omega*t)
+ *   LINEAR_SIN any  p0=lam p1=amp p2=omega        f=lam*y + amp*sin(omega*t)
+ *   RELAX_COS  any  p0=lam p1=omega               f=lam*(y - cos(omega*t))
+ *   SQUARE     any  p0=thr                        f= y>thr ? inf : y*y
+ *   LOGISTIC   any                                f=y*(1-y)   (problems.py:178-179)
+ *   SIN_PLUS_T any                                f=sin(y)+t
+ *   HARMONIC   d=2                                f=(y1,-y0)  (problems.py:169-170)
+ *   DAMPED     d=2                                f=(y1,-y0-0.1*y1*|y1|)
+ *   MLP        any  weights in bode_mlp_weights   f=W2 tanh(W1 y + b1) + b2 (fp32) */
+#define BODE_DYN_VDP 1
+#define BODE_DYN_LORENZ 2
+#define BODE_DYN_ZERO 3
+#define BODE_DYN_CONST 4
+#define BODE_DYN_LINEAR 5
+#define BODE_DYN_LINEAR_COS 6
+#define BODE_DYN_LINEAR_SIN 7
+#define BODE_DYN_RELAX_COS 8
+#define BODE_DYN_SQUARE 9
+#define BODE_DYN_LOGISTIC 10
+#define BODE_DYN_SIN_PLUS_T 11
+#define BODE_DYN_HARMONIC 12
+#define BODE_DYN_DAMPED 13
+#define BODE_DYN_MLP 20
+
+/* arithmetic mode: EXACT = unfused IEEE ops in the reference's operation
+ * order; FAST = FMA contraction allowed. */
+#define BODE_MODE_EXACT 0
+#define BODE_MODE_FAST 1
+
+/* dt0 modes (solver.py:176-183) */
+#define BODE_DT0_HEURISTIC 0 /* initial_step(), controller.py:145-197 */
+#define BODE_DT0_SCALAR 1
+#define BODE_DT0_ARRAY 2
+
+typedef struct bode_dynamics {
+  int32_t kind;               /* BODE_DYN_* */
+  uint32_t inst_mask;         /* bit k: slot k is per-instance */
+  const double* inst_params;  /* (n, popcount(inst_mask)) or NULL */
+  double shared_params[8];
+  /* MLP only (BODE_DYN_MLP): fp32 row-major, device pointers */
+  const float* W1; /* (H, d) */
+  const float* b1; /* (H,)   */
+  const float* W2; /* (d, H) */
+  const float* b2; /* (d,)   */
+  int64_t hidden;  /* H */
+} bode_dynamics;
+
+typedef struct bode_controller {
+  /* PidCoefficients (controller.py:57-83); exponents -beta/k are formed
+   * on the host exactly as the reference does (controller.py:221-226). */
+  double beta1, beta2, beta3;
+  double safety, factor_min, factor_max;
+  int32_t update_history_on_reject;
+  int32_t _pad;
+} bode_controller;
+
+typedef struct bode_solve_args {
+  int32_t abi_version; /* = BODE_ABI_VERSION */
+  int32_t method;      /* BODE_METHOD_* */
+  int32_t mode;        /* BODE_MODE_* */
+  int32_t dt0_mode;    /* BODE_DT0_* */
+  int64_t n, d;
+  bode_dynamics dyn;
+  bode_controller ctrl;
+  /* problem (IvpBatch, solver.py:53-101); device pointers for bode_solve,
+   * host pointers for bode_solve_host */
+  const double* y0;      /* (n, d) */
+  const double* t_start; /* (n,) */
+  const double* t_end;   /* (n,) */
+  /* t_eval: CSR (values + (n+1) offsets) or, with offsets NULL, one shared
+   * sorted array of t_eval_len points used by every instance */
+  const double* t_eval;
+  const int64_t* t_eval_offsets;
+  int64_t t_eval_len;
+  /* tolerances (Tolerances, controller.py:39-54): array (n,) or scalar */
+  const double* atol_v;
+  const double* rtol_v;
+  double atol, rtol;
+  int64_t max_steps;   /* solver.py:42,155 */
+  double dt0;          /* BODE_DT0_SCALAR */
+  const double* dt0_v; /* BODE_DT0_ARRAY, (n,) */
+  /* processing order (cost-sorted LPT queue); NULL = natural order */
+  const int64_t* order;
+  /* outputs.  ys follows the t_eval layout: CSR rows (offsets) or dense
+   * (n, t_eval_len, d); only the first n_emitted[i] rows of an instance are
+   * written (unreached points are absent, solver.py:126-131). */
+  double* ys;
+  int64_t* n_emitted;   /* (n,) */
+  int64_t* n_steps;     /* (n,) */
+  int64_t* n_accepted;  /* (n,) */
+  double* final_dt;     /* (n,) */
+  int32_t* status;      /* (n,) */
+  int64_t* n_f_evals;   /* (1,) batch-global count (solver.py:184,224,239) */
+  /* optional record_trace (solver.py:196-199,257-261): (n, trace_cap) */
+  double* trace_t;
+  double* trace_dt;
+  uint8_t* trace_accept;
+  int64_t trace_cap;
+  /* scratch from bode_workspace_size(); device memory */
+  void* workspace;
+  size_t workspace_bytes;
+  void* stream; /* cudaStream_t */
+  /* launch shape overrides (0 = auto) */
+  int32_t threads_per_block;
+  int32_t blocks;
+} bode_solve_args;
+
+int bode_abi_version(void);
+const char* bode_last_error(void);
+size_t bode_workspace_size(const bode_solve_args* args);
+
+/* Full batched solve on device buffers, asynchronous on args->stream. */
+int bode_solve(const bode_solve_args* args);
+
+/* Same, but every pointer in args is a HOST pointer: copies inputs to the
+ * device, solves, copies outputs back and synchronises (end-to-end path). */
+int bode_solve_host(const bode_solve_args* args);
+
+/* One embedded RK trial step on the full batch (Stepper.step):
+ * k0 = f0 for FSAL methods, else f(t, y).  k: (stages, n, d). */
+int bode_rk_step(int32_t method, int32_t mode, const bode_dynamics* dyn, int64_t n,
+                 int64_t d, const double* t, const double* dt, const double* y,
+                 const double* f0, double* y_next, double* err, double* k,
+                 void* stream);
+
+/* Dense output y(t + theta*dt) from a step's stage derivatives; theta in
+ * [0,1] is checked on the host path by the facade (stepper.py:126-127). */
+int bode_interpolate(int32_t method, int32_t mode, int64_t n, int64_t d,
+                     const double* k, const double* y0, const double* dt,
+                     const double* theta, double* out, void* stream);
+
+/* Mixed-tolerance RMS norm, NumPy pairwise summation order. */
+int bode_error_norm(int64_t n, int64_t d, const double* err, const double* y0,
+                    const double* y1, const double* atol_v, const double* rtol_v,
+                    double atol, double rtol, double* norm, void* stream);
+
+/* adapt_step: updates (norm_prev, norm_prev2, dt) in place. */
+int bode_adapt_step(int64_t n, const double* norm, int32_t error_order,
+                    const bode_controller* ctrl, double* norm_prev,
+                    double* norm_prev2, double* dt, uint8_t* accept,
+                    double* dt_next, void* stream);
+
+/* initial_step: dt (NaN where f0 is non-finite) and f0. */
+int bode_initial_step(const bode_dynamics* dyn, int64_t n, int64_t d,
+                      const double* t0, const double* y0, int32_t order,
+                      const double* atol_v, const double* rtol_v, double atol,
+                      double rtol, const double* direction, double* dt,
+                      double* f0, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BODE_H_ */
