@@ -1,0 +1,395 @@
+"""Benchmark: accepted instance-steps/s of the batched independent ODE solve.
+
+Headline workload (BASELINE.json metric, configs[1]):
+Van der Pol, 2^20 instances per GPU, mu ~ U[1,10], t_end ~ U[5,20],
+y0 = (2, 0), t_eval = {t_end_i}, dopri5, PI42 (0.6, -0.2, 0), atol = rtol =
+1e-6, fp64, exact (reference-order, unfused) arithmetic.  A "step" is one
+complete solve of that batch: the persistent kernel runs every instance to
+termination.  value = sum_i n_accepted_i / device time (max over ranks,
+weak scaling: every rank solves its own 2^20-instance shard).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2|c1|c3|c5]
+    python bench.py --impl reference ...   # CPU reference arm (oracle port)
+"""
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+PI42 = dict(betas=(0.6, -0.2, 0.0), safety=0.9, factor_min=0.2, factor_max=10.0, hist=True)
+ICTRL = dict(betas=(1.0, 0.0, 0.0), safety=0.9, factor_min=0.2, factor_max=10.0, hist=True)
+
+# algorithmic flops: per attempted step 82d+20+6*F_f (FSAL,
+# s=7), per emitted point 15d+51; pow counted separately (2 per step with PI42)
+F_F = {"vdp": 5, "lorenz": 8}
+
+
+def flops_per_step(dyn, d):
+    return 82 * d + 20 + 6 * F_F[dyn]
+
+
+def flops_per_point(d):
+    return 15 * d + 51
+
+
+# ----------------------------------------------------------------- configs --
+def make_config(name, rank, n_override=None):
+    """Seeded synthetic inputs; rank r of a weak-scaling run draws shard r."""
+    if name == "c2":
+        n = n_override or 2 ** 20
+        rng = np.random.default_rng(1000 + rank) if rank else np.random.default_rng(0)
+        mu = rng.uniform(1.0, 10.0, n)
+        t_end = rng.uniform(5.0, 20.0, n)
+        return dict(workload="vdp_1M_dopri5_pi42_fp64", dyn="vdp", n=n, d=2,
+                    y0=np.tile([2.0, 0.0], (n, 1)), t_start=np.zeros(n), t_end=t_end,
+                    te2d=t_end[:, None].copy(), mu=mu, method="dopri5", ctrl=PI42,
+                    tol=1e-6, max_steps=10_000, cost=mu * t_end)
+    if name == "c1":
+        n = n_override or 256
+        rng = np.random.default_rng(0)
+        mu = rng.uniform(1.0, 10.0, n)
+        return dict(workload="vdp_256_dopri5_I_50pts_fp64", dyn="vdp", n=n, d=2,
+                    y0=np.tile([2.0, 0.0], (n, 1)), t_start=np.zeros(n), t_end=np.full(n, 10.0),
+                    te1d=np.linspace(0.0, 10.0, 50), mu=mu, method="dopri5", ctrl=ICTRL,
+                    tol=1e-6, max_steps=100_000, cost=None)
+    if name == "c5":
+        n = n_override or 2 ** 20
+        rng = np.random.default_rng(0 if rank == 0 else 1000 + rank)
+        mu = np.exp(rng.uniform(0.0, np.log(1000.0), n))
+        return dict(workload="vdp_1M_stiff_logmu_dopri5_pi42_fp64", dyn="vdp", n=n, d=2,
+                    y0=np.tile([2.0, 0.0], (n, 1)), t_start=np.zeros(n), t_end=np.full(n, 10.0),
+                    mu=mu, method="dopri5", ctrl=PI42, tol=1e-6, max_steps=100_000,
+                    cost=mu)
+    if name == "c3":
+        n = n_override or 2 ** 18
+        rng = np.random.default_rng(0 if rank == 0 else 1000 + rank)
+        y0 = 1.0 + 0.1 * rng.normal(size=(n, 3))
+        return dict(workload="lorenz_256K_tsit5_1e-8_1000pts_fp64", dyn="lorenz", n=n, d=3,
+                    y0=y0, t_start=np.zeros(n), t_end=np.full(n, 10.0),
+                    te1d=np.linspace(0.0, 10.0, 1000), mu=None, method="tsit5", ctrl=ICTRL,
+                    tol=1e-8, max_steps=100_000, cost=None)
+    raise ValueError(name)
+
+
+def n_points(cfg):
+    if "te2d" in cfg:
+        return cfg["te2d"].size
+    if "te1d" in cfg:
+        return cfg["n"] * cfg["te1d"].size
+    return 0
+
+
+# ------------------------------------------------------------ CPU legs ----
+def cpu_run(cfg, sample, nthreads):
+    """Oracle (C restatement of the reference, test infrastructure) on the
+    first `sample` instances; returns (accepted, seconds)."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle as O
+
+    k = min(sample, cfg["n"])
+    if "te2d" in cfg:
+        te = [cfg["te2d"][i] for i in range(k)]
+    else:
+        te = cfg.get("te1d")
+    dyn = (dict(name="vdp", inst=cfg["mu"][:k, None]) if cfg["dyn"] == "vdp"
+           else dict(name="lorenz", inst=None, shared=(10.0, 28.0, 8.0 / 3.0)))
+    t0 = time.perf_counter()
+    r = O.solve(cfg["y0"][:k], cfg["t_start"][:k], cfg["t_end"][:k], te, dyn,
+                method=cfg["method"], atol=cfg["tol"], rtol=cfg["tol"], ctrl=cfg["ctrl"],
+                max_steps=cfg["max_steps"], nthreads=nthreads)
+    dt = time.perf_counter() - t0
+    return int(r["n_accepted"].sum()), dt, k
+
+
+def cpu_sample_size(cfg):
+    return {"c2": 262_144, "c5": 16_384, "c3": 4_096, "c1": 256}[cfg["_name"]]
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the reference algorithm on host cores (oracle port,
+    all threads), rank 0 only."""
+    if rank != 0:
+        return
+    cfg = make_config(args.config, 0)
+    cfg["_name"] = args.config
+    nthreads = os.cpu_count() or 1
+    sample = cpu_sample_size(cfg)
+    for _ in range(args.warmup):
+        cpu_run(cfg, sample, nthreads)
+    acc, secs = 0, 0.0
+    for _ in range(args.steps):
+        a, s, k = cpu_run(cfg, sample, nthreads)
+        acc += a
+        secs += s
+    value = acc / secs
+    line = dict(metric="accepted instance-steps/sec", value=value,
+                unit="instance-steps/s", n_gpus=args.gpus, steps=args.steps,
+                warmup=args.warmup, ms_per_step=1e3 * secs / args.steps, higher_is_better=True,
+                scaling="weak", vs_baseline=None, dtype="f64", data="synthetic",
+                impl="reference",
+                config=dict(workload=cfg["workload"], sample_instances=sample,
+                            parallelism="host threads"),
+                cpu_baseline=dict(value=value, unit="instance-steps/s", cores=nthreads,
+                                  kind="port",
+                                  sample=f"first {sample} instances of the seeded "
+                                         f"{cfg['workload']} batch per step (C oracle = "
+                                         "restatement of batchode, pthreads)"),
+                e2e=dict(value=value, unit="instance-steps/s", h2d_bytes_per_step=0,
+                         d2h_bytes_per_step=0))
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------ GPU leg -----
+class ClockSampler:
+    def __init__(self, path):
+        self.path = path
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.fh = open(self.path, "w")
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "--query-gpu=index,clocks.sm,clocks.max.sm,power.draw,"
+                 "clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+                 "clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=self.fh, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            self.proc.wait()
+            self.fh.close()
+
+    def summary(self, gpu_index):
+        try:
+            rows = [r.split(",") for r in open(self.path).read().strip().splitlines()]
+        except Exception:
+            return None
+        rows = [[c.strip() for c in r] for r in rows if len(r) >= 9 and r[0].strip() == str(gpu_index)]
+        if not rows:
+            return None
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = max(float(r[2]) for r in rows if r[2].replace(".", "").isdigit())
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in rows for k in range(4) if "Active" in r[5 + k]})
+        return dict(sm_mhz=float(np.median(sm)) if sm else None, sm_max_mhz=mx,
+                    reasons=reasons, samples=len(rows))
+
+
+def fp64_peak(torch, lib, dev):
+    """Measured DFMA throughput (bode_probe_fp64), TFLOP/s."""
+    out = torch.zeros(1, dtype=torch.float64, device=dev)
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    blocks, iters = sms * 8, 20000
+    st = torch.cuda.current_stream(dev)
+    best = 0.0
+    for _ in range(4):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        lib.bode_probe_fp64(iters, blocks, out.data_ptr(), st.cuda_stream)
+        e1.record(st)
+        e1.synchronize()
+        secs = e0.elapsed_time(e1) / 1e3
+        best = max(best, 2.0 * 8 * 256 * blocks * iters / secs / 1e12)
+    return best
+
+
+def run_bode(args, rank, world, local_rank):
+    import torch
+
+    import paper_2210_12375_b200 as bode
+    from paper_2210_12375_b200 import _abi
+
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+    lib = _abi.load()
+    cfg = make_config(args.config, rank)
+    cfg["_name"] = args.config
+    n, d = cfg["n"], cfg["d"]
+    f64 = dict(dtype=torch.float64, device=dev)
+    y0 = torch.tensor(cfg["y0"], **f64)
+    ts = torch.tensor(cfg["t_start"], **f64)
+    tn = torch.tensor(cfg["t_end"], **f64)
+    dyn = (bode.vdp_dynamics(bode.VdpParams(torch.tensor(cfg["mu"], **f64)))
+           if cfg["dyn"] == "vdp" else bode.lorenz_dynamics())
+    ctrl = bode.PidCoefficients(*cfg["ctrl"]["betas"])
+    te_kw = {}
+    if "te2d" in cfg:
+        te_kw["t_eval"] = torch.tensor(cfg["te2d"], **f64)
+    elif "te1d" in cfg:
+        te_kw["t_eval"] = torch.tensor(cfg["te1d"], **f64)
+    cost = torch.tensor(cfg["cost"], **f64) if (cfg["cost"] is not None and args.lpt) else None
+    flush = torch.empty(256 * 2 ** 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
+    st = torch.cuda.current_stream(dev)
+
+    def one_step():
+        return bode.solve_device(y0, ts, tn, dyn, method=cfg["method"], atol=cfg["tol"],
+                                 rtol=cfg["tol"], controller=ctrl, max_steps=cfg["max_steps"],
+                                 mode=args.mode, cost_hint=cost, **te_kw)
+
+    for _ in range(args.warmup):
+        out = one_step()
+    torch.cuda.synchronize(dev)
+    if dist:
+        dist.barrier()
+    times, accepted, attempted = [], 0, 0
+    kern_ms = 0.0
+    clock_path = os.path.join(ROOT, "gpurun_out" if os.path.isdir(os.path.join(ROOT, "gpurun_out"))
+                              else ".", f"clocks_rank{rank}.csv")
+    with ClockSampler(clock_path) as clk:
+        for _ in range(args.steps):
+            flush.zero_()
+            torch.cuda.synchronize(dev)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(st)
+            out = one_step()
+            e1.record(st)
+            e1.synchronize()
+            times.append(e0.elapsed_time(e1))
+            accepted += int(out["n_accepted"].sum())
+            attempted += int(out["n_steps"].sum())
+        time.sleep(0.25)
+    torch.cuda.synchronize(dev)
+    total_ms = float(np.sum(times))
+    # max over ranks of device time; sum of accepted over ranks
+    if dist:
+        tt = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        total_ms = float(tt.item())
+        aa = torch.tensor([accepted, attempted], dtype=torch.float64, device=dev)
+        dist.all_reduce(aa)
+        accepted, attempted = int(aa[0].item()), int(aa[1].item())
+    value = accepted / (total_ms / 1e3)
+
+    # ---- roofline: the persistent kernel alone (events on its stream)
+    peak_fp64 = fp64_peak(torch, lib, dev)
+    pts = n_points(cfg)
+    flops_launch = (flops_per_step(cfg["dyn"], d) * (attempted / args.steps / max(world, 1))
+                    + flops_per_point(d) * pts)
+    # one extra timed solve, split: the solve is memset + persistent + finalize
+    flush.zero_()
+    torch.cuda.synchronize(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(st)
+    one_step()
+    e1.record(st)
+    e1.synchronize()
+    kern_ms = e0.elapsed_time(e1)
+    achieved = flops_launch / (kern_ms / 1e3) / 1e12
+
+    # ---- end to end through the reference-facing solve() with host buffers
+    e2e = None
+    if not args.no_e2e:
+        prob = bode.IvpBatch(cfg["y0"], cfg["t_start"], cfg["t_end"],
+                             cfg.get("te2d", cfg.get("te1d", [np.empty(0)] * n)))
+        dyn_h = (bode.vdp_dynamics(bode.VdpParams(cfg["mu"])) if cfg["dyn"] == "vdp"
+                 else bode.lorenz_dynamics())
+        tab = {"dopri5": bode.dopri5, "tsit5": bode.tsit5}[cfg["method"]]()
+        kw = dict(tableau=tab, tol=bode.Tolerances(cfg["tol"], cfg["tol"]), controller=ctrl,
+                  max_steps=cfg["max_steps"], mode=args.mode,
+                  cost_hint=cfg["cost"] if args.lpt else None)
+        bode.solve(prob, dyn_h, **kw)
+        if dist:
+            dist.barrier()
+        e2e_t, e2e_acc = [], 0
+        for _ in range(max(1, min(args.steps, 5))):
+            flush.zero_()
+            torch.cuda.synchronize(dev)
+            t0 = time.perf_counter()
+            sol = bode.solve(prob, dyn_h, **kw)
+            e2e_t.append(time.perf_counter() - t0)
+            e2e_acc += int(sol.stats.n_accepted.sum())
+        tot = float(np.sum(e2e_t))
+        if dist:
+            tt = torch.tensor([tot, e2e_acc], dtype=torch.float64, device=dev)
+            dist.all_reduce(tt[:1], op=dist.ReduceOp.MAX)
+            acc_t = torch.tensor([float(e2e_acc)], dtype=torch.float64, device=dev)
+            dist.all_reduce(acc_t)
+            tot, e2e_acc = float(tt[0].item()), int(acc_t.item())
+        h2d = (prob.y0.nbytes + prob.t_start.nbytes + prob.t_end.nbytes + prob.te_values.nbytes
+               + (0 if prob.te_shared else prob.te_offsets.nbytes)
+               + (cfg["mu"].nbytes if cfg["mu"] is not None else 0)
+               + (8 * n if args.lpt and cfg["cost"] is not None else 0))
+        d2h = 8 * pts * d + n * (8 + 8 + 8 + 8 + 4) + 8
+        e2e = dict(value=e2e_acc / tot, unit="instance-steps/s", h2d_bytes_per_step=int(h2d),
+                   d2h_bytes_per_step=int(d2h), ms_per_step=1e3 * tot / len(e2e_t),
+                   path="paper_2210_12375_b200.solve -> bode_solve_host (pageable numpy)")
+
+    # ---- CPU baseline (rank 0, N=1 only)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        nthreads = os.cpu_count() or 1
+        sample = cpu_sample_size(cfg)
+        a, s, k = cpu_run(cfg, sample, nthreads)
+        cpu = dict(value=a / s, unit="instance-steps/s", cores=nthreads, kind="port",
+                   sample=f"first {k} instances of the seeded batch, one solve "
+                          f"({s:.2f} s wall, C oracle restating batchode, pthreads)")
+
+    clocks = clk.summary(local_rank)
+    if rank == 0:
+        line = dict(
+            metric="accepted instance-steps/sec", value=value, unit="instance-steps/s",
+            n_gpus=world, steps=args.steps, warmup=args.warmup,
+            ms_per_step=total_ms / args.steps, higher_is_better=True, scaling="weak",
+            vs_baseline=None, dtype="f64", data="synthetic",
+            config=dict(workload=cfg["workload"], instances_per_gpu=n,
+                        global_instances=n * world, method=cfg["method"],
+                        controller="PI42" if cfg["ctrl"] is PI42 else "I",
+                        tol=cfg["tol"], mode=args.mode, lpt_order=bool(args.lpt),
+                        parallelism=f"shard{world}", l2="flushed (256 MiB write) between steps",
+                        accepted_per_step=accepted / args.steps,
+                        attempted_per_step=attempted / args.steps),
+            roofline=dict(bound="fp64", achieved=achieved, peak=peak_fp64, unit="TFLOP/s",
+                          frac=achieved / peak_fp64, traffic=None,
+                          kernel="bode_persistent_kernel",
+                          note="algorithmic flops (SURVEY §8(a): 82d+20+6F_f per attempted "
+                               "step, 15d+51 per point; pow not counted) / solve time; peak = "
+                               "DFMA throughput measured in-run by bode_probe_fp64 (2 flops/DFMA)",
+                          kernel_ms=kern_ms),
+            cpu_baseline=cpu, e2e=e2e, gpu_launches=2 * args.steps, clocks=clocks)
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=10)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", default="bode", choices=["bode", "reference"])
+    p.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c5"])
+    p.add_argument("--mode", default="exact", choices=["exact", "fast"])
+    p.add_argument("--lpt", type=int, default=1, help="cost-sorted (LPT) instance queue")
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-cpu", action="store_true")
+    args = p.parse_args()
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local_rank = int(os.environ.get("LOCAL_RANK", 0))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+    else:
+        run_bode(args, rank, world, local_rank)
+
+
+if __name__ == "__main__":
+    main()

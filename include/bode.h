@@ -177,6 +177,8 @@ typedef struct bode_solve_args {
 } bode_solve_args;
 
 int bode_abi_version(void);
+/* sizeof(bode_solve_args) as compiled, for binding layout checks */
+size_t bode_sizeof_args(void);
 const char* bode_last_error(void);
 size_t bode_workspace_size(const bode_solve_args* args);
 
@@ -217,6 +219,11 @@ int bode_initial_step(const bode_dynamics* dyn, int64_t n, int64_t d,
                       const double* atol_v, const double* rtol_v, double atol,
                       double rtol, const double* direction, double* dt,
                       double* f0, void* stream);
+
+/* Measurement utility (not on the solve path): launches blocks x 256
+ * threads each running 8 independent chains of `iters` DFMAs, so a timed
+ * launch gives the FP64 roofline denominator (2 flops per DFMA). */
+int bode_probe_fp64(int64_t iters, int32_t blocks, double* out, void* stream);
 
 #ifdef __cplusplus
 }

@@ -1,0 +1,29 @@
+"""bode: B200-native batched independent ODE solving (arXiv 2210.12375).
+
+Drop-in for the reference's solve path (``batchode``; torchode-style names
+in :mod:`.torchode`).  Host code is Python; the solve runs in hand-written
+sm_100a kernels behind the C ABI in ``include/bode.h`` (``libbode.so``).
+"""
+
+from .controller import (NORM_FLOOR, PID_PRESETS, PidCoefficients, Tolerances,
+                         integral_controller, pid_controller)
+from .dynamics import (AnalyticProblem, DeviceDynamics, VdpParams, analytic_problems,
+                       constant_dynamics, damped_dynamics, forced_linear_dynamics,
+                       harmonic_dynamics, linear_dynamics, logistic_dynamics,
+                       lorenz_dynamics, mlp_dynamics, relaxation_dynamics,
+                       sin_plus_t_dynamics, square_dynamics, vdp_dynamics, zero_dynamics)
+from .solver import (DEFAULT_MAX_STEPS, IvpBatch, Solution, SolveStats, SolveStatus, solve,
+                     solve_device)
+from .tableau import ButcherTableau, dopri5, heun, tsit5
+
+__version__ = "0.1.0"
+
+__all__ = [
+    "NORM_FLOOR", "PID_PRESETS", "PidCoefficients", "Tolerances", "integral_controller",
+    "pid_controller", "AnalyticProblem", "DeviceDynamics", "VdpParams", "analytic_problems",
+    "constant_dynamics", "damped_dynamics", "forced_linear_dynamics", "harmonic_dynamics",
+    "linear_dynamics", "logistic_dynamics", "lorenz_dynamics", "mlp_dynamics",
+    "relaxation_dynamics", "sin_plus_t_dynamics", "square_dynamics", "vdp_dynamics",
+    "zero_dynamics", "DEFAULT_MAX_STEPS", "IvpBatch", "Solution", "SolveStats", "SolveStatus",
+    "solve", "solve_device", "ButcherTableau", "dopri5", "heun", "tsit5",
+]

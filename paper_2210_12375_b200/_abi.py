@@ -1,0 +1,114 @@
+"""ctypes binding of ``libbode.so`` (the C ABI declared in include/bode.h).
+
+The library is built in-tree by ``__graft_entry__.build()`` (or
+``make -C paper_2210_12375_b200/csrc``) into ``paper_2210_12375_b200/_build``.
+There is deliberately no fallback: if the CUDA library is missing, every
+solve raises ``BodeLibraryError``.
+"""
+
+import ctypes as C
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "_build", "libbode.so")
+
+ABI_VERSION = 1
+OK, EINVAL, ECUDA, EUNSUPPORTED = 0, 1, 2, 3
+METHOD = {"dopri5": 0, "tsit5": 1, "heun": 2}
+MODE = {"exact": 0, "fast": 1}
+DT0_HEURISTIC, DT0_SCALAR, DT0_ARRAY = 0, 1, 2
+DYN = {"vdp": 1, "lorenz": 2, "zero": 3, "const": 4, "linear": 5, "linear_cos": 6,
+       "linear_sin": 7, "relax_cos": 8, "square": 9, "logistic": 10, "sin_plus_t": 11,
+       "harmonic": 12, "damped": 13, "mlp": 20}
+
+
+class BodeLibraryError(RuntimeError):
+    """libbode.so is missing or failed (CUDA error)."""
+
+
+class Dynamics_(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("inst_mask", C.c_uint32),
+                ("inst_params", C.c_void_p), ("shared_params", C.c_double * 8),
+                ("W1", C.c_void_p), ("b1", C.c_void_p), ("W2", C.c_void_p),
+                ("b2", C.c_void_p), ("hidden", C.c_int64)]
+
+
+class Controller_(C.Structure):
+    _fields_ = [("beta1", C.c_double), ("beta2", C.c_double), ("beta3", C.c_double),
+                ("safety", C.c_double), ("factor_min", C.c_double),
+                ("factor_max", C.c_double), ("update_history_on_reject", C.c_int32),
+                ("_pad", C.c_int32)]
+
+
+class SolveArgs(C.Structure):
+    _fields_ = [("abi_version", C.c_int32), ("method", C.c_int32), ("mode", C.c_int32),
+                ("dt0_mode", C.c_int32), ("n", C.c_int64), ("d", C.c_int64),
+                ("dyn", Dynamics_), ("ctrl", Controller_),
+                ("y0", C.c_void_p), ("t_start", C.c_void_p), ("t_end", C.c_void_p),
+                ("t_eval", C.c_void_p), ("t_eval_offsets", C.c_void_p),
+                ("t_eval_len", C.c_int64), ("atol_v", C.c_void_p), ("rtol_v", C.c_void_p),
+                ("atol", C.c_double), ("rtol", C.c_double), ("max_steps", C.c_int64),
+                ("dt0", C.c_double), ("dt0_v", C.c_void_p), ("order", C.c_void_p),
+                ("ys", C.c_void_p), ("n_emitted", C.c_void_p), ("n_steps", C.c_void_p),
+                ("n_accepted", C.c_void_p), ("final_dt", C.c_void_p),
+                ("status", C.c_void_p), ("n_f_evals", C.c_void_p),
+                ("trace_t", C.c_void_p), ("trace_dt", C.c_void_p),
+                ("trace_accept", C.c_void_p), ("trace_cap", C.c_int64),
+                ("workspace", C.c_void_p), ("workspace_bytes", C.c_size_t),
+                ("stream", C.c_void_p), ("threads_per_block", C.c_int32),
+                ("blocks", C.c_int32)]
+
+
+# every symbol include/bode.h declares, with its ctypes signature
+_P, _I32, _I64, _D, _SZ = C.c_void_p, C.c_int32, C.c_int64, C.c_double, C.c_size_t
+SIGNATURES = {
+    "bode_abi_version": ([], C.c_int),
+    "bode_sizeof_args": ([], _SZ),
+    "bode_last_error": ([], C.c_char_p),
+    "bode_workspace_size": ([C.POINTER(SolveArgs)], _SZ),
+    "bode_solve": ([C.POINTER(SolveArgs)], C.c_int),
+    "bode_solve_host": ([C.POINTER(SolveArgs)], C.c_int),
+    "bode_rk_step": ([_I32, _I32, _P, _I64, _I64, _P, _P, _P, _P, _P, _P, _P, _P], C.c_int),
+    "bode_interpolate": ([_I32, _I32, _I64, _I64, _P, _P, _P, _P, _P, _P], C.c_int),
+    "bode_error_norm": ([_I64, _I64, _P, _P, _P, _P, _P, _D, _D, _P, _P], C.c_int),
+    "bode_adapt_step": ([_I64, _P, _I32, _P, _P, _P, _P, _P, _P, _P], C.c_int),
+    "bode_initial_step": ([_P, _I64, _I64, _P, _P, _I32, _P, _P, _D, _D, _P, _P, _P, _P],
+                          C.c_int),
+    "bode_probe_fp64": ([_I64, _I32, _P, _P], C.c_int),
+}
+
+_lib = None
+
+
+def load():
+    """Load libbode.so once; raises BodeLibraryError if it is not built."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise BodeLibraryError(
+            f"{LIB_PATH} not found: build the CUDA extension first "
+            "(python -c 'import __graft_entry__ as g; g.build()'); there is no CPU fallback")
+    lib = C.CDLL(LIB_PATH)
+    for name, (args, res) in SIGNATURES.items():
+        fn = getattr(lib, name)
+        fn.argtypes = args
+        fn.restype = res
+    if lib.bode_abi_version() != ABI_VERSION:
+        raise BodeLibraryError("libbode.so ABI version mismatch")
+    if lib.bode_sizeof_args() != C.sizeof(SolveArgs):
+        raise BodeLibraryError("bode_solve_args layout mismatch between header and binding")
+    _lib = lib
+    return lib
+
+
+def check(rc):
+    """Map a C return code onto the reference's exception types."""
+    if rc == OK:
+        return
+    msg = load().bode_last_error().decode()
+    if rc == EINVAL:
+        raise ValueError(msg)
+    if rc == EUNSUPPORTED:
+        raise NotImplementedError(msg)
+    raise BodeLibraryError(msg)

@@ -1,0 +1,437 @@
+// bode_device.cuh -- device-side numerics shared by the persistent solver
+// and the unit-op kernels.  Every function restates one reference function
+// (paths relative to /root/reference/pkg/src/batchode/) in the reference's
+// NumPy operation order; Ops selects exact (separately rounded IEEE ops,
+// SURVEY.md Appendix A) or fast (FMA-contracted) arithmetic.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "../../include/bode.h"
+#include "tableau_coeffs.h"
+
+namespace bode {
+
+// ----------------------------------------------------------------- ops --
+struct ExactOps {
+  static constexpr bool kFast = false;
+  static __device__ __forceinline__ double mul(double a, double b) { return __dmul_rn(a, b); }
+  static __device__ __forceinline__ double add(double a, double b) { return __dadd_rn(a, b); }
+  static __device__ __forceinline__ double sub(double a, double b) { return __dsub_rn(a, b); }
+  // (a*b)+c with two roundings, as NumPy evaluates it
+  static __device__ __forceinline__ double mad(double a, double b, double c) {
+    return __dadd_rn(__dmul_rn(a, b), c);
+  }
+};
+
+struct FastOps {
+  static constexpr bool kFast = true;
+  static __device__ __forceinline__ double mul(double a, double b) { return a * b; }
+  static __device__ __forceinline__ double add(double a, double b) { return a + b; }
+  static __device__ __forceinline__ double sub(double a, double b) { return a - b; }
+  static __device__ __forceinline__ double mad(double a, double b, double c) { return fma(a, b, c); }
+};
+
+__device__ __forceinline__ double ddiv(double a, double b) { return __ddiv_rn(a, b); }
+__device__ __forceinline__ double dsqrt(double a) { return __dsqrt_rn(a); }
+
+// np.maximum / np.minimum: NaN-propagating (unlike fmax/fmin)
+__device__ __forceinline__ double np_max(double a, double b) {
+  return (a != a) ? a : ((b != b) ? b : (a >= b ? a : b));
+}
+__device__ __forceinline__ double np_min(double a, double b) {
+  return (a != a) ? a : ((b != b) ? b : (a <= b ? a : b));
+}
+
+// array ** python-float the way NumPy evaluates it (fast_scalar_power
+// short-cuts for 0, +-1, 2, 0.5; controller.py:221-226, :193)
+__device__ __forceinline__ double np_scalar_pow(double x, double e) {
+  if (e == 0.0) return 1.0;
+  if (e == 1.0) return x;
+  if (e == -1.0) return ddiv(1.0, x);
+  if (e == 2.0) return __dmul_rn(x, x);
+  if (e == 0.5) return dsqrt(x);
+  return pow(x, e);
+}
+
+// NumPy pairwise_sum (umath loops_utils.h.src) seeded with 0.0, which is the
+// reduction order of np.mean(..., axis=1) on a C-contiguous row.
+template <int N, class O>
+__device__ __forceinline__ double pairwise_sum(const double* a) {
+  if constexpr (N < 8) {
+    double r = 0.0;
+#pragma unroll
+    for (int i = 0; i < N; i++) r = O::add(r, a[i]);
+    return r;
+  } else if constexpr (N <= 128) {
+    double r[8];
+#pragma unroll
+    for (int j = 0; j < 8; j++) r[j] = a[j];
+#pragma unroll
+    for (int i = 8; i < N - (N % 8); i += 8) {
+#pragma unroll
+      for (int j = 0; j < 8; j++) r[j] = O::add(r[j], a[i + j]);
+    }
+    double res = O::add(O::add(O::add(r[0], r[1]), O::add(r[2], r[3])),
+                        O::add(O::add(r[4], r[5]), O::add(r[6], r[7])));
+#pragma unroll
+    for (int i = N - (N % 8); i < N; i++) res = O::add(res, a[i]);
+    return res;
+  } else {
+    constexpr int n2 = (N / 2) - ((N / 2) % 8);
+    return O::add(pairwise_sum<n2, O>(a), pairwise_sum<N - n2, O>(a + n2));
+  }
+}
+
+// runtime-length variant (MLP widths, unit ops)
+template <class O>
+__device__ double pairwise_sum_rt(const double* a, int64_t n) {
+  if (n < 8) {
+    double r = 0.0;
+    for (int64_t i = 0; i < n; i++) r = O::add(r, a[i]);
+    return r;
+  }
+  if (n <= 128) {
+    double r[8];
+    int64_t i;
+    for (int j = 0; j < 8; j++) r[j] = a[j];
+    for (i = 8; i < n - (n % 8); i += 8)
+      for (int j = 0; j < 8; j++) r[j] = O::add(r[j], a[i + j]);
+    double res = O::add(O::add(O::add(r[0], r[1]), O::add(r[2], r[3])),
+                        O::add(O::add(r[4], r[5]), O::add(r[6], r[7])));
+    for (; i < n; i++) res = O::add(res, a[i]);
+    return res;
+  }
+  int64_t h = n / 2;
+  h -= h % 8;
+  return O::add(pairwise_sum_rt<O>(a, h), pairwise_sum_rt<O>(a + h, n - h));
+}
+
+// ------------------------------------------------------------ tableaus --
+template <int M> struct Tab;
+template <> struct Tab<BODE_METHOD_DOPRI5> {
+  static constexpr int S = BODE_DOPRI5_STAGES, ORDER = BODE_DOPRI5_ORDER,
+                       ERR_ORDER = BODE_DOPRI5_ERROR_ORDER, NI = BODE_DOPRI5_NINTERP;
+  static constexpr bool FSAL = BODE_DOPRI5_FSAL;
+  static __device__ __forceinline__ constexpr double a(int i, int j) { return bode_dopri5_a(i, j); }
+  static __device__ __forceinline__ constexpr double b(int i) { return bode_dopri5_b(i); }
+  static __device__ __forceinline__ constexpr double e(int i) { return bode_dopri5_berr(i); }
+  static __device__ __forceinline__ constexpr double c(int i) { return bode_dopri5_c(i); }
+  static __device__ __forceinline__ constexpr double w(int i, int j) { return bode_dopri5_interp(i, j); }
+};
+template <> struct Tab<BODE_METHOD_TSIT5> {
+  static constexpr int S = BODE_TSIT5_STAGES, ORDER = BODE_TSIT5_ORDER,
+                       ERR_ORDER = BODE_TSIT5_ERROR_ORDER, NI = BODE_TSIT5_NINTERP;
+  static constexpr bool FSAL = BODE_TSIT5_FSAL;
+  static __device__ __forceinline__ constexpr double a(int i, int j) { return bode_tsit5_a(i, j); }
+  static __device__ __forceinline__ constexpr double b(int i) { return bode_tsit5_b(i); }
+  static __device__ __forceinline__ constexpr double e(int i) { return bode_tsit5_berr(i); }
+  static __device__ __forceinline__ constexpr double c(int i) { return bode_tsit5_c(i); }
+  static __device__ __forceinline__ constexpr double w(int i, int j) { return bode_tsit5_interp(i, j); }
+};
+template <> struct Tab<BODE_METHOD_HEUN> {
+  static constexpr int S = BODE_HEUN_STAGES, ORDER = BODE_HEUN_ORDER,
+                       ERR_ORDER = BODE_HEUN_ERROR_ORDER, NI = BODE_HEUN_NINTERP;
+  static constexpr bool FSAL = BODE_HEUN_FSAL;
+  static __device__ __forceinline__ constexpr double a(int i, int j) { return bode_heun_a(i, j); }
+  static __device__ __forceinline__ constexpr double b(int i) { return bode_heun_b(i); }
+  static __device__ __forceinline__ constexpr double e(int i) { return bode_heun_berr(i); }
+  static __device__ __forceinline__ constexpr double c(int i) { return bode_heun_c(i); }
+  static __device__ __forceinline__ constexpr double w(int i, int j) { return bode_heun_interp(i, j); }
+};
+
+// ------------------------------------------------------------ dynamics --
+// Registered device functors replacing the reference's NumPy callables
+// (stepper.py:19-20).  Each evaluates f(t, y) for ONE instance in the
+// operation order of the NumPy expression it replaces.
+struct DynParams {
+  int32_t kind;
+  uint32_t inst_mask;
+  int32_t n_inst;
+  const double* inst;
+  double shared[8];
+};
+
+__device__ __forceinline__ void load_params(const DynParams& P, int64_t i, double* p, int np) {
+  int r = 0;
+  for (int k = 0; k < np; k++) {
+    if ((P.inst_mask >> k) & 1u) {
+      p[k] = P.inst[i * P.n_inst + r];
+      r++;
+    } else {
+      p[k] = P.shared[k];
+    }
+  }
+}
+
+template <class O>
+struct VdP {  // problems.py:45-48: (v, mu*(1-x*x)*v - x)
+  static constexpr int D = 2;
+  double mu;
+  __device__ __forceinline__ void load(const DynParams& P, int64_t i) { load_params(P, i, &mu, 1); }
+  __device__ __forceinline__ void operator()(double, const double* y, double* f) const {
+    const double x = y[0], v = y[1];
+    f[0] = v;
+    f[1] = O::sub(O::mul(O::mul(mu, O::sub(1.0, O::mul(x, x))), v), x);
+  }
+};
+
+template <class O>
+struct Lorenz {  // (s*(y-x), x*(r-z)-y, x*y - b*z)
+  static constexpr int D = 3;
+  double s, r, b;
+  __device__ __forceinline__ void load(const DynParams& P, int64_t i) {
+    double p[3];
+    load_params(P, i, p, 3);
+    s = p[0];
+    r = p[1];
+    b = p[2];
+  }
+  __device__ __forceinline__ void operator()(double, const double* y, double* f) const {
+    const double x = y[0], yy = y[1], z = y[2];
+    f[0] = O::mul(s, O::sub(yy, x));
+    f[1] = O::sub(O::mul(x, O::sub(r, z)), yy);
+    if constexpr (O::kFast) {
+      f[2] = fma(x, yy, -(b * z));
+    } else {
+      f[2] = O::sub(O::mul(x, yy), O::mul(b, z));
+    }
+  }
+};
+
+template <class O>
+struct Harmonic {  // problems.py:169-170
+  static constexpr int D = 2;
+  __device__ __forceinline__ void load(const DynParams&, int64_t) {}
+  __device__ __forceinline__ void operator()(double, const double* y, double* f) const {
+    f[0] = y[1];
+    f[1] = -y[0];
+  }
+};
+
+template <class O>
+struct Damped {  // (y1, -y0 - 0.1*y1*|y1|)
+  static constexpr int D = 2;
+  __device__ __forceinline__ void load(const DynParams&, int64_t) {}
+  __device__ __forceinline__ void operator()(double, const double* y, double* f) const {
+    f[0] = y[1];
+    f[1] = O::sub(-y[0], O::mul(O::mul(0.1, y[1]), fabs(y[1])));
+  }
+};
+
+// Component-wise family; the sub-kind is uniform across a launch.
+template <class O, int DD>
+struct Elementwise {
+  static constexpr int D = DD;
+  int32_t kind;
+  double p[3];
+  __device__ __forceinline__ void load(const DynParams& P, int64_t i) {
+    kind = P.kind;
+    load_params(P, i, p, 3);
+  }
+  __device__ __forceinline__ void operator()(double t, const double* y, double* f) const {
+    switch (kind) {
+      case BODE_DYN_ZERO:
+#pragma unroll
+        for (int j = 0; j < D; j++) f[j] = 0.0;
+        break;
+      case BODE_DYN_CONST:
+#pragma unroll
+        for (int j = 0; j < D; j++) f[j] = p[0];
+        break;
+      case BODE_DYN_LINEAR:
+#pragma unroll
+        for (int j = 0; j < D; j++) f[j] = O::mul(p[0], y[j]);
+        break;
+      case BODE_DYN_LINEAR_COS: {
+        const double g = O::mul(p[1], cos(O::mul(p[2], t)));
+#pragma unroll
+        for (int j = 0; j < D; j++) f[j] = O::mad(p[0], y[j], g);
+        break;
+      }
+      case BODE_DYN_LINEAR_SIN: {
+        const double g = O::mul(p[1], sin(O::mul(p[2], t)));
+#pragma unroll
+        for (int j = 0; j < D; j++) f[j] = O::mad(p[0], y[j], g);
+        break;
+      }
+      case BODE_DYN_RELAX_COS: {
+        const double g = cos(O::mul(p[1], t));
+#pragma unroll
+        for (int j = 0; j < D; j++) f[j] = O::mul(p[0], O::sub(y[j], g));
+        break;
+      }
+      case BODE_DYN_SQUARE:
+#pragma unroll
+        for (int j = 0; j < D; j++) f[j] = (y[j] > p[0]) ? __longlong_as_double(0x7ff0000000000000LL)
+                                                         : O::mul(y[j], y[j]);
+        break;
+      case BODE_DYN_LOGISTIC:
+#pragma unroll
+        for (int j = 0; j < D; j++) f[j] = O::mul(y[j], O::sub(1.0, y[j]));
+        break;
+      case BODE_DYN_SIN_PLUS_T:
+#pragma unroll
+        for (int j = 0; j < D; j++) f[j] = O::add(sin(y[j]), t);
+        break;
+      default:
+#pragma unroll
+        for (int j = 0; j < D; j++) f[j] = __longlong_as_double(0x7ff8000000000000LL);
+    }
+  }
+};
+
+// ---------------------------------------------------------- controller --
+struct CtrlParams {
+  double e1, e2, e3;  // (-beta_i)/k formed on the host (controller.py:221-226)
+  double safety, fmin, fmax;
+  int32_t hist;
+};
+
+// error_norm, controller.py:120-142 (one instance)
+template <int D, class O>
+__device__ __forceinline__ double error_norm(const double* e, const double* y0, const double* y1,
+                                             double atol, double rtol) {
+  double sq[D];
+#pragma unroll
+  for (int j = 0; j < D; j++) {
+    const double scale = O::mad(rtol, np_max(fabs(y0[j]), fabs(y1[j])), atol);
+    const double r = ddiv(e[j], scale);
+    sq[j] = O::mul(r, r);
+  }
+  const double s = pairwise_sum<D, O>(sq);
+  double mean;
+  if constexpr ((D & (D - 1)) == 0) {
+    mean = __dmul_rn(s, 1.0 / D);  // exact: division by a power of two
+  } else {
+    mean = ddiv(s, (double)D);
+  }
+  const double norm = dsqrt(mean);
+  return isfinite(norm) ? norm : __longlong_as_double(0x7ff0000000000000LL);
+}
+
+// adapt_step, controller.py:200-238 (one instance).  dt is dt_used on entry,
+// dt_next on exit; returns accept.
+__device__ __forceinline__ bool adapt(const CtrlParams& C, double norm, double& n1, double& n2,
+                                      double& dt) {
+  const bool accept = norm <= 1.0;
+  const double a = np_max(norm, 1e-10);
+  const double b = np_max(n1, 1e-10);
+  const double g = np_max(n2, 1e-10);
+  double factor = __dmul_rn(C.safety, np_scalar_pow(a, C.e1));
+  if (C.e2 != 0.0) factor = __dmul_rn(factor, np_scalar_pow(b, C.e2));
+  if (C.e3 != 0.0) factor = __dmul_rn(factor, np_scalar_pow(g, C.e3));
+  if (!isfinite(factor)) factor = C.fmin;
+  factor = np_min(np_max(factor, C.fmin), C.fmax);
+  dt = __dmul_rn(dt, factor);
+  if (C.hist || accept) {
+    n2 = n1;
+    n1 = a;
+  }
+  return accept;
+}
+
+// initial_step, controller.py:145-197 (one instance).  Returns dt (NaN when
+// f0 is non-finite) and writes f0.
+template <class F, class O>
+__device__ __forceinline__ double initial_step(const F& f, double t0, const double* y0, int order,
+                                               double atol, double rtol, double direction,
+                                               double* f0) {
+  constexpr int D = F::D;
+  f(t0, y0, f0);
+  bool bad = false;
+  double scale[D], sq[D];
+#pragma unroll
+  for (int j = 0; j < D; j++) {
+    bad |= !isfinite(f0[j]);
+    scale[j] = O::mad(rtol, fabs(y0[j]), atol);
+  }
+#pragma unroll
+  for (int j = 0; j < D; j++) {
+    const double q = ddiv(y0[j], scale[j]);
+    sq[j] = O::mul(q, q);
+  }
+  const double d0 = dsqrt(ddiv(pairwise_sum<D, O>(sq), (double)D));
+#pragma unroll
+  for (int j = 0; j < D; j++) {
+    const double q = ddiv(f0[j], scale[j]);
+    sq[j] = O::mul(q, q);
+  }
+  const double d1 = dsqrt(ddiv(pairwise_sum<D, O>(sq), (double)D));
+  const bool degenerate = (d0 < 1e-5) || (d1 < 1e-5) || !isfinite(d1);
+  const double h0 = degenerate ? 1e-6 : ddiv(__dmul_rn(0.01, d0), d1);
+  const double hd = __dmul_rn(h0, direction);
+  double y1[D], f1[D];
+#pragma unroll
+  for (int j = 0; j < D; j++) y1[j] = O::mad(hd, f0[j], y0[j]);
+  f(__dadd_rn(t0, hd), y1, f1);
+#pragma unroll
+  for (int j = 0; j < D; j++) {
+    const double q = ddiv(O::sub(f1[j], f0[j]), scale[j]);
+    sq[j] = O::mul(q, q);
+  }
+  const double d2 = ddiv(dsqrt(ddiv(pairwise_sum<D, O>(sq), (double)D)), h0);
+  const double dmax = np_max(d1, d2);
+  const bool small = (dmax <= 1e-15) || !isfinite(dmax);
+  const double h1 = small ? np_max(1e-6, __dmul_rn(h0, 1e-3))
+                          : np_scalar_pow(ddiv(0.01, dmax), ddiv(1.0, (double)(order + 1)));
+  const double dt = __dmul_rn(np_min(__dmul_rn(100.0, h0), h1), direction);
+  return bad ? __longlong_as_double(0x7ff8000000000000LL) : dt;
+}
+
+// Stepper.step, stepper.py:54-110 (one instance).  k[0] must hold f0 for
+// FSAL tableaus; on return k[0..S-1] are the stage derivatives.
+template <class T, class F, class O>
+__device__ __forceinline__ void rk_step(const F& f, double t, double h, const double* y,
+                                        double (*k)[F::D], double* y_next, double* err) {
+  constexpr int D = F::D, S = T::S;
+  if constexpr (!T::FSAL) f(t, y, k[0]);
+#pragma unroll
+  for (int i = 1; i < S; i++) {
+    double ys[D];
+#pragma unroll
+    for (int c = 0; c < D; c++) {
+      double s = O::mul(T::a(i, 0), k[0][c]);
+#pragma unroll
+      for (int j = 1; j < i; j++) s = O::mad(T::a(i, j), k[j][c], s);
+      ys[c] = O::mad(h, s, y[c]);
+    }
+    f(O::mad(T::c(i), h, t), ys, k[i]);
+  }
+#pragma unroll
+  for (int c = 0; c < D; c++) {
+    double s = O::mul(T::b(0), k[0][c]);
+    double e = O::mul(T::e(0), k[0][c]);
+#pragma unroll
+    for (int i = 1; i < S; i++) {
+      s = O::mad(T::b(i), k[i][c], s);
+      e = O::mad(T::e(i), k[i][c], e);
+    }
+    y_next[c] = O::mad(h, s, y[c]);
+    err[c] = O::mul(h, e);
+  }
+}
+
+// Stepper.interpolate, stepper.py:112-139: Horner weights, then y0 + dt*sum.
+template <class T, int D, class O>
+__device__ __forceinline__ void interpolate(const double (*k)[D], const double* y0, double h,
+                                            double theta, double* out) {
+  constexpr int S = T::S, M = T::NI;
+  double w[S];
+#pragma unroll
+  for (int i = 0; i < S; i++) {
+    double v = T::w(i, M - 1);
+#pragma unroll
+    for (int j = M - 2; j >= 0; j--) v = O::mad(v, theta, T::w(i, j));
+    w[i] = O::mul(v, theta);
+  }
+#pragma unroll
+  for (int c = 0; c < D; c++) {
+    double s = O::mul(w[0], k[0][c]);
+#pragma unroll
+    for (int i = 1; i < S; i++) s = O::mad(w[i], k[i][c], s);
+    out[c] = O::mad(h, s, y0[c]);
+  }
+}
+
+}  // namespace bode

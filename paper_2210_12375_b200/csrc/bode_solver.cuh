@@ -1,0 +1,288 @@
+// bode_solver.cuh -- the persistent batched integrator (kernel K2).
+//
+// One lane (thread) owns one instance at a time and runs the reference's
+// whole per-instance state machine to termination: FSAL stages, RK axpys,
+// RMS error norm, PID update, accept/reject, t_end truncation, statuses,
+// statistics and Horner dense output straight to ys.  This is the
+// batch-independent restatement of the reference's lockstep loop
+// (solver.py:148-322).  There is no per-step launch
+// and no host sync: when a lane's instance terminates the warp pulls the
+// next instance from a global queue (warp-aggregated atomicAdd), so lanes
+// never idle on an "all done?" flag and step-count divergence costs only the
+// tail.  The queue may be cost-sorted (longest first) by the caller.
+//
+// The batch-global n_f_evals (solver.py:184,224,239) is rebuilt exactly:
+// every lane records "instance rejected at iteration j and still running"
+// in a per-block shared-memory bitmap of iterations, blocks OR it into a
+// global bitmap, and bode_finalize counts 1 + (S-1)*max n_steps + refreshes.
+#pragma once
+#include "bode_device.cuh"
+
+namespace bode {
+
+struct SolveParams {
+  int64_t n;
+  DynParams dyn;
+  CtrlParams ctrl;
+  const double* y0;
+  const double* t_start;
+  const double* t_end;
+  const double* t_eval;
+  const int64_t* t_eval_offsets;
+  int64_t t_eval_len;
+  const double* atol_v;
+  const double* rtol_v;
+  double atol, rtol;
+  int64_t max_steps;
+  int32_t dt0_mode;
+  double dt0;
+  const double* dt0_v;
+  const int64_t* order;
+  double* ys;
+  int64_t* n_emitted;
+  int64_t* n_steps;
+  int64_t* n_accepted;
+  double* final_dt;
+  int32_t* status;
+  double* trace_t;
+  double* trace_dt;
+  uint8_t* trace_accept;
+  int64_t trace_cap;
+  // workspace
+  unsigned long long* queue;   // next instance position
+  unsigned long long* max_n;   // max n_steps over the batch
+  uint32_t* refresh;           // global bitmap over iterations
+  int32_t smem_words;          // >0: per-block shared bitmap of this many words
+};
+
+struct Workspace {
+  static constexpr size_t kHeader = 64;
+  static size_t bitmap_words(int64_t max_steps) { return (size_t)((max_steps + 2 + 31) / 32); }
+  static size_t bytes(int64_t max_steps) { return kHeader + 4 * bitmap_words(max_steps); }
+};
+
+template <int M, class F, class O>
+struct Lane {
+  using T = Tab<M>;
+  static constexpr int D = F::D, S = T::S;
+  F f;
+  double y[D];
+  double k[S][D];  // k[0] is the FSAL cache f0
+  double t, dt, t_end, atol, rtol, n1, n2;
+  int64_t idx, nsteps, nacc, cursor, m;
+  const double* te;
+  double* ys;
+  int32_t status;
+
+  // BatchSolver.__init__ for one row (solver.py:148-206)
+  __device__ __forceinline__ void init(const SolveParams& P, int64_t i) {
+    idx = i;
+    f.load(P.dyn, i);
+    t = P.t_start[i];
+    t_end = P.t_end[i];
+    atol = P.atol_v ? P.atol_v[i] : P.atol;
+    rtol = P.rtol_v ? P.rtol_v[i] : P.rtol;
+#pragma unroll
+    for (int c = 0; c < D; c++) y[c] = P.y0[i * D + c];
+    if (P.t_eval_offsets) {
+      const int64_t off = P.t_eval_offsets[i];
+      te = P.t_eval + off;
+      m = P.t_eval_offsets[i + 1] - off;
+      ys = P.ys ? P.ys + off * D : nullptr;
+    } else {
+      te = P.t_eval;
+      m = P.t_eval_len;
+      ys = P.ys ? P.ys + i * P.t_eval_len * D : nullptr;
+    }
+    const double direction = (t_end - t) > 0.0 ? 1.0 : -1.0;
+    if (P.dt0_mode == BODE_DT0_HEURISTIC) {
+      dt = initial_step<F, O>(f, t, y, T::ORDER, atol, rtol, direction, k[0]);
+    } else {
+      dt = P.dt0_mode == BODE_DT0_SCALAR ? P.dt0 : P.dt0_v[i];
+      f(t, y, k[0]);
+      bool fin = true;
+#pragma unroll
+      for (int c = 0; c < D; c++) fin &= isfinite(k[0][c]);
+      if (!fin) dt = __longlong_as_double(0x7ff8000000000000LL);
+    }
+    status = BODE_RUNNING;
+    if (!isfinite(dt)) {
+      status = BODE_INFINITE_DYNAMICS;
+      dt = 0.0;
+    }
+    cursor = 0;
+    while (cursor < m && te[cursor] == t) {  // points at t_start: copies of y0
+      if (ys) {
+#pragma unroll
+        for (int c = 0; c < D; c++) ys[cursor * D + c] = y[c];
+      }
+      cursor++;
+    }
+    n1 = 1.0;
+    n2 = 1.0;
+    nsteps = 0;
+    nacc = 0;
+  }
+
+  // one iteration of step_once for this row (solver.py:208-282); returns
+  // true when the row just rejected and is still running (FSAL refresh at
+  // the next iteration, solver.py:220-226)
+  __device__ __forceinline__ bool step(const SolveParams& P) {
+    const int64_t j = nsteps;
+    const double remaining = O::sub(t_end, t);
+    const bool trunc = fabs(dt) >= fabs(remaining);
+    const double h = trunc ? remaining : dt;
+    double yn[D], err[D];
+    rk_step<T, F, O>(f, t, h, y, k, yn, err);
+    const double norm = error_norm<D, O>(err, y, yn, atol, rtol);
+    double dtn = h;
+    const bool accept = adapt(P.ctrl, norm, n1, n2, dtn);
+    nsteps = j + 1;
+    if (P.trace_cap > 0 && j < P.trace_cap) {
+      const int64_t o = idx * P.trace_cap + j;
+      if (P.trace_t) P.trace_t[o] = t;
+      if (P.trace_dt) P.trace_dt[o] = h;
+      if (P.trace_accept) P.trace_accept[o] = accept;
+    }
+    if (accept) {
+      nacc++;
+      const double t_old = t;
+      if (cursor < m && h != 0.0) emit(t_old, h);
+#pragma unroll
+      for (int c = 0; c < D; c++) y[c] = yn[c];
+      t = trunc ? t_end : O::add(t_old, h);
+      if constexpr (T::FSAL) {
+#pragma unroll
+        for (int c = 0; c < D; c++) k[0][c] = k[S - 1][c];
+      }
+      if (trunc) status = BODE_SUCCESS;
+    }
+    dt = dtn;
+    if (status == BODE_RUNNING && O::add(t, dt) == t) status = BODE_STEP_UNDERFLOW;
+    if (status == BODE_RUNNING && nsteps >= P.max_steps) status = BODE_MAX_STEPS_EXCEEDED;
+    return !accept && status == BODE_RUNNING;
+  }
+
+  // _emit, solver.py:284-322: every point with theta in (.., 1] is
+  // interpolated from the pre-commit state (y is still y_old here)
+  __device__ __forceinline__ void emit(double t_old, double h) {
+    while (cursor < m) {
+      double theta = ddiv(O::sub(te[cursor], t_old), h);
+      if (!(theta <= 1.0)) break;
+      theta = np_max(theta, 0.0);
+      double out[D];
+      interpolate<T, D, O>(k, y, h, theta, out);
+      if (ys) {
+#pragma unroll
+        for (int c = 0; c < D; c++) ys[cursor * D + c] = out[c];
+      }
+      cursor++;
+    }
+  }
+
+  __device__ __forceinline__ void finish(const SolveParams& P) const {
+    P.n_emitted[idx] = cursor;
+    P.n_steps[idx] = nsteps;
+    P.n_accepted[idx] = nacc;
+    P.final_dt[idx] = dt;
+    P.status[idx] = status;
+  }
+};
+
+template <int M, class F, class O>
+__global__ void __launch_bounds__(128) bode_persistent_kernel(const SolveParams P) {
+  extern __shared__ uint32_t s_refresh[];
+  const int lane = threadIdx.x & 31;
+  for (int w = threadIdx.x; w < P.smem_words; w += blockDim.x) s_refresh[w] = 0u;
+  __syncthreads();
+
+  Lane<M, F, O> L;
+  bool have = false, done = false;
+  unsigned long long my_max = 0;
+  const unsigned lt_mask = (1u << lane) - 1u;
+
+  while (true) {
+    const unsigned need = __ballot_sync(0xffffffffu, !have && !done);
+    if (need) {
+      const int leader = __ffs(need) - 1;
+      unsigned long long base = 0;
+      if (lane == leader) base = atomicAdd(P.queue, (unsigned long long)__popc(need));
+      base = __shfl_sync(0xffffffffu, base, leader);
+      if (!have && !done) {
+        const unsigned long long pos = base + __popc(need & lt_mask);
+        if (pos >= (unsigned long long)P.n) {
+          done = true;
+        } else {
+          const int64_t i = P.order ? P.order[pos] : (int64_t)pos;
+          L.init(P, i);
+          if (L.status == BODE_RUNNING) {
+            have = true;
+          } else {
+            L.finish(P);
+          }
+        }
+      }
+    }
+    if (!__any_sync(0xffffffffu, have)) {
+      if (__all_sync(0xffffffffu, done)) break;
+      continue;
+    }
+    if (have) {
+      const int64_t j = L.nsteps;
+      if (L.step(P)) {
+        const uint64_t bit = (uint64_t)j + 1;
+        const uint32_t w = (uint32_t)(bit >> 5), msk = 1u << (bit & 31);
+        if (P.smem_words > 0) {
+          if (!(s_refresh[w] & msk)) atomicOr(&s_refresh[w], msk);
+        } else {
+          if (!(__ldcg(&P.refresh[w]) & msk)) atomicOr(&P.refresh[w], msk);
+        }
+      }
+      if (L.status != BODE_RUNNING) {
+        if ((unsigned long long)L.nsteps > my_max) my_max = (unsigned long long)L.nsteps;
+        L.finish(P);
+        have = false;
+      }
+    }
+  }
+  // max n_steps: warp reduce then one atomic per warp
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const unsigned long long v = __shfl_xor_sync(0xffffffffu, my_max, o);
+    my_max = v > my_max ? v : my_max;
+  }
+  if (lane == 0 && my_max) atomicMax(P.max_n, my_max);
+  __syncthreads();
+  for (int w = threadIdx.x; w < P.smem_words; w += blockDim.x)
+    if (s_refresh[w]) atomicOr(&P.refresh[w], s_refresh[w]);
+}
+
+// n_f_evals = 1 + (S-1)*max_n + #refresh iterations in [1, max_n)  (FSAL)
+//           = 1 + S*max_n                                        (non-FSAL)
+__global__ void bode_finalize_kernel(const unsigned long long* max_n, const uint32_t* refresh,
+                                     int stages, int fsal, int64_t* n_f_evals);
+
+template <int M, class F, class O>
+cudaError_t launch_persistent(const SolveParams& P, int threads, int blocks, cudaStream_t st) {
+  auto kern = bode_persistent_kernel<M, F, O>;
+  const size_t smem = (size_t)P.smem_words * 4;
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  if (threads <= 0) threads = 128;
+  if (blocks <= 0) {
+    int dev = 0, sms = 0, per_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem);
+    if (per_sm < 1) per_sm = 1;
+    const int64_t need = (P.n + threads - 1) / threads;
+    blocks = (int)((int64_t)sms * per_sm < need ? (int64_t)sms * per_sm : need);
+    if (blocks < 1) blocks = 1;
+  }
+  kern<<<blocks, threads, smem, st>>>(P);
+  return cudaGetLastError();
+}
+
+}  // namespace bode

@@ -1,0 +1,411 @@
+"""Batched independent ODE solve: the reference-facing entry points.
+
+Mirrors ``batchode.solver`` (reference ``pkg/src/batchode/solver.py``):
+``SolveStatus`` (:45-50), ``IvpBatch`` (:53-101, same validation and
+ValueErrors), ``SolveStats`` (:104-119), ``Solution`` (:122-138) and
+``solve`` (:352-369, same signature and defaults).  The loop itself
+(``BatchSolver`` :141-349) is the persistent sm_100a kernel behind
+``bode_solve`` -- one C-ABI call per solve, no per-step launches.
+
+Two call styles:
+  * ``solve(problem, f, ...)``: NumPy in, NumPy out, exactly like the
+    reference.  It goes through ``bode_solve_host`` (host buffers, copies
+    inside the call) -- the end-to-end path.
+  * ``solve_device(...)``: torch CUDA tensors in/out, asynchronous on the
+    current stream, no host sync -- the device-resident path.
+"""
+
+import enum
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _abi
+from .controller import PidCoefficients, Tolerances, integral_controller
+from .dynamics import DeviceDynamics, as_device_dynamics, build_struct
+from .tableau import method_of
+
+__all__ = ["DEFAULT_MAX_STEPS", "SolveStatus", "IvpBatch", "SolveStats", "Solution",
+           "solve", "solve_device"]
+
+DEFAULT_MAX_STEPS = 10_000
+
+
+class SolveStatus(enum.IntEnum):
+    RUNNING = 0
+    SUCCESS = 1
+    MAX_STEPS_EXCEEDED = 2
+    STEP_UNDERFLOW = 3
+    INFINITE_DYNAMICS = 4
+
+
+class IvpBatch:
+    """A batch of independent initial value problems (solver.py:53-101).
+
+    ``t_eval`` is, as in the reference, a list of per-instance sorted arrays
+    (ragged, possibly empty).  For large batches it may also be given as a
+    2-D array (n, m) -- every instance m points -- or a 1-D array shared by
+    all instances; these are validated vectorised and passed to the device
+    without building per-instance lists.
+    """
+
+    def __init__(self, y0, t_start, t_end, t_eval):
+        self.y0 = np.atleast_2d(np.asarray(y0, dtype=float))
+        self.t_start = np.asarray(t_start, dtype=float)
+        self.t_end = np.asarray(t_end, dtype=float)
+        n, d = self.y0.shape
+        if n < 1 or d < 1:
+            raise ValueError("need at least one instance and one state component")
+        if self.t_start.shape != (n,) or self.t_end.shape != (n,):
+            raise ValueError("t_start/t_end must have one entry per instance")
+        if np.any(self.t_end == self.t_start):
+            raise ValueError("t_end must differ from t_start for every instance")
+        direction = np.sign(self.t_end - self.t_start)
+        span = np.abs(self.t_end - self.t_start)
+        self._te_list = None
+        if isinstance(t_eval, np.ndarray) and t_eval.ndim == 1 and t_eval.dtype != object:
+            te = np.asarray(t_eval, dtype=float)  # shared by every instance
+            self.te_values, self.te_offsets, self.te_shared = te, None, True
+            if te.size:
+                pos = (te[None, :] - self.t_start[:, None]) * direction[:, None]
+                self._check_dense(pos, span)
+        elif isinstance(t_eval, np.ndarray) and t_eval.ndim == 2:
+            te = np.ascontiguousarray(t_eval, dtype=float)
+            if te.shape[0] != n:
+                raise ValueError("t_eval must have one (possibly empty) array per instance")
+            m = te.shape[1]
+            self.te_values = te.reshape(-1)
+            self.te_offsets = np.arange(n + 1, dtype=np.int64) * m
+            self.te_shared = False
+            if m:
+                pos = (te - self.t_start[:, None]) * direction[:, None]
+                self._check_dense(pos, span)
+        else:
+            if len(t_eval) != n:
+                raise ValueError("t_eval must have one (possibly empty) array per instance")
+            lst = [np.asarray(te, dtype=float) for te in t_eval]
+            for i, te in enumerate(lst):
+                if te.size == 0:
+                    continue
+                pos = (te - self.t_start[i]) * direction[i]
+                if np.any(np.diff(pos) < 0):
+                    raise ValueError(f"t_eval of instance {i} is not sorted in integration direction")
+                if pos[0] < 0 or pos[-1] > span[i]:
+                    raise ValueError(f"t_eval of instance {i} leaves the integration interval")
+            self._te_list = lst
+            lens = np.fromiter((te.size for te in lst), dtype=np.int64, count=n)
+            self.te_offsets = np.zeros(n + 1, dtype=np.int64)
+            np.cumsum(lens, out=self.te_offsets[1:])
+            self.te_values = (np.concatenate(lst) if self.te_offsets[-1] else np.zeros(0))
+            self.te_shared = False
+
+    @staticmethod
+    def _check_dense(pos, span):
+        bad = np.any(np.diff(pos, axis=1) < 0, axis=1)
+        if np.any(bad):
+            i = int(np.flatnonzero(bad)[0])
+            raise ValueError(f"t_eval of instance {i} is not sorted in integration direction")
+        bad = (pos[:, 0] < 0) | (pos[:, -1] > span)
+        if np.any(bad):
+            i = int(np.flatnonzero(bad)[0])
+            raise ValueError(f"t_eval of instance {i} leaves the integration interval")
+
+    @property
+    def t_eval(self) -> list:
+        if self._te_list is None:
+            n = self.batch_size
+            if self.te_shared:
+                self._te_list = [self.te_values] * n
+            else:
+                o = self.te_offsets
+                self._te_list = [self.te_values[o[i]:o[i + 1]] for i in range(n)]
+        return self._te_list
+
+    @property
+    def batch_size(self) -> int:
+        return self.y0.shape[0]
+
+    @property
+    def n_features(self) -> int:
+        return self.y0.shape[1]
+
+    @property
+    def direction(self) -> np.ndarray:
+        return np.sign(self.t_end - self.t_start)
+
+    def eval_counts(self) -> np.ndarray:
+        n = self.batch_size
+        if self.te_shared:
+            return np.full(n, self.te_values.size, dtype=np.int64)
+        return np.diff(self.te_offsets)
+
+
+@dataclass
+class SolveStats:
+    """Per-instance statistics (solver.py:104-119); n_f_evals is batch-global."""
+
+    n_steps: np.ndarray
+    n_accepted: np.ndarray
+    n_f_evals: np.ndarray
+    final_dt: np.ndarray
+    extra: dict = field(default_factory=dict)
+
+
+class Solution:
+    """Outputs at the requested times plus statistics and statuses
+    (solver.py:122-138).  ``ys[i]`` holds only the points instance i
+    reached; the ragged list is materialised lazily from the flat buffer."""
+
+    def __init__(self, ys_flat, offsets, shared_len, n_emitted, stats, status, d):
+        self.ys_flat = ys_flat
+        self.offsets = offsets
+        self.shared_len = shared_len
+        self.n_emitted = n_emitted
+        self.stats = stats
+        self.status = status
+        self.d = d
+        self._ys = None
+
+    @property
+    def ys(self) -> list:
+        if self._ys is None:
+            n, d = self.status.shape[0], self.d
+            if self.offsets is None:
+                m = self.shared_len
+                dense = self.ys_flat.reshape(n, m, d) if m else np.zeros((n, 0, d))
+                self._ys = [dense[i, :self.n_emitted[i]] for i in range(n)]
+            else:
+                o = self.offsets
+                flat = self.ys_flat.reshape(-1, d)
+                self._ys = [flat[o[i]:o[i] + self.n_emitted[i]] for i in range(n)]
+        return self._ys
+
+    @property
+    def ok(self) -> bool:
+        return bool(np.all(self.status == SolveStatus.SUCCESS))
+
+
+def _controller_struct(controller: PidCoefficients):
+    c = _abi.Controller_()
+    c.beta1, c.beta2, c.beta3 = controller.beta1, controller.beta2, controller.beta3
+    c.safety, c.factor_min, c.factor_max = controller.safety, controller.factor_min, controller.factor_max
+    c.update_history_on_reject = int(bool(controller.update_history_on_reject))
+    return c
+
+
+def _tol_arrays(tol: Tolerances, n: int):
+    out = []
+    for v in (tol.atol, tol.rtol):
+        if np.ndim(v) == 0:
+            out.append((None, float(v)))
+        else:
+            a = np.ascontiguousarray(np.asarray(v, dtype=np.float64).reshape(-1))
+            if a.shape[0] != n:
+                raise ValueError("per-instance tolerances need one entry per instance")
+            out.append((a, 0.0))
+    return out
+
+
+def solve(problem: IvpBatch, f, tableau=None, tol: Tolerances | None = None,
+          controller: PidCoefficients | None = None, max_steps: int = DEFAULT_MAX_STEPS,
+          dt0=None, record_trace: bool = False, *, mode: str = "exact", order=None,
+          cost_hint=None) -> Solution:
+    """Integrate every instance independently with adaptive steps on the GPU
+    (reference ``solve``, solver.py:352-369), host arrays in and out."""
+    if max_steps < 1:
+        raise ValueError("max_steps must be at least 1")
+    lib = _abi.load()
+    dyn = as_device_dynamics(f)
+    method = method_of(tableau)
+    tol = tol if tol is not None else Tolerances()
+    controller = controller if controller is not None else integral_controller()
+    n, d = problem.batch_size, problem.n_features
+    dyn.check_width(d)
+    keep = []
+    a = _abi.SolveArgs()
+    a.abi_version = _abi.ABI_VERSION
+    a.method = _abi.METHOD[method]
+    a.mode = _abi.MODE[mode]
+    a.n, a.d = n, d
+    a.dyn = build_struct(dyn, n, keep)
+    a.ctrl = _controller_struct(controller)
+    y0 = np.ascontiguousarray(problem.y0)
+    ts = np.ascontiguousarray(problem.t_start)
+    tn = np.ascontiguousarray(problem.t_end)
+    te = np.ascontiguousarray(problem.te_values)
+    keep += [y0, ts, tn, te]
+    a.y0, a.t_start, a.t_end = y0.ctypes.data, ts.ctypes.data, tn.ctypes.data
+    a.t_eval = te.ctypes.data if te.size else None
+    if problem.te_shared:
+        a.t_eval_len = te.size
+        n_rows = n * te.size
+        offs = None
+    else:
+        offs = np.ascontiguousarray(problem.te_offsets)
+        keep.append(offs)
+        a.t_eval_offsets = offs.ctypes.data
+        n_rows = int(offs[-1])
+    (av, a.atol), (rv, a.rtol) = _tol_arrays(tol, n)
+    keep += [av, rv]
+    a.atol_v = av.ctypes.data if av is not None else None
+    a.rtol_v = rv.ctypes.data if rv is not None else None
+    a.max_steps = int(max_steps)
+    if dt0 is None:
+        a.dt0_mode = _abi.DT0_HEURISTIC
+    elif np.ndim(dt0) == 0:
+        a.dt0_mode, a.dt0 = _abi.DT0_SCALAR, float(dt0)
+    else:
+        dv = np.ascontiguousarray(np.broadcast_to(np.asarray(dt0, dtype=np.float64), (n,)))
+        keep.append(dv)
+        a.dt0_mode, a.dt0_v = _abi.DT0_ARRAY, dv.ctypes.data
+    if order is None and cost_hint is not None:
+        order = np.argsort(-np.asarray(cost_hint, dtype=np.float64), kind="stable")
+    if order is not None:
+        order = np.ascontiguousarray(np.asarray(order, dtype=np.int64))
+        keep.append(order)
+        a.order = order.ctypes.data
+    ys = np.empty((max(n_rows, 1), d))
+    n_emitted = np.empty(n, np.int64)
+    n_steps = np.empty(n, np.int64)
+    n_accepted = np.empty(n, np.int64)
+    final_dt = np.empty(n)
+    status = np.empty(n, np.int32)
+    nfe = np.zeros(1, np.int64)
+    a.ys = ys.ctypes.data if n_rows else None
+    a.n_emitted, a.n_steps, a.n_accepted = n_emitted.ctypes.data, n_steps.ctypes.data, n_accepted.ctypes.data
+    a.final_dt, a.status, a.n_f_evals = final_dt.ctypes.data, status.ctypes.data, nfe.ctypes.data
+    if record_trace:
+        cap = int(max_steps)
+        tt, tdt, tacc = np.zeros((n, cap)), np.zeros((n, cap)), np.zeros((n, cap), np.uint8)
+        a.trace_t, a.trace_dt, a.trace_accept, a.trace_cap = (tt.ctypes.data, tdt.ctypes.data,
+                                                              tacc.ctypes.data, cap)
+    _abi.check(lib.bode_solve_host(_abi.C.byref(a)))
+    extra = {}
+    if record_trace:
+        extra["trace_t"] = [tt[i, :n_steps[i]].copy() for i in range(n)]
+        extra["trace_dt"] = [tdt[i, :n_steps[i]].copy() for i in range(n)]
+        extra["trace_accept"] = [tacc[i, :n_steps[i]].astype(bool) for i in range(n)]
+    stats = SolveStats(n_steps=n_steps, n_accepted=n_accepted,
+                       n_f_evals=np.full(n, nfe[0], dtype=np.int64), final_dt=final_dt,
+                       extra=extra)
+    return Solution(ys[:n_rows], offs, te.size if problem.te_shared else 0, n_emitted, stats,
+                    status.astype(np.int64), d)
+
+
+def solve_device(y0, t_start, t_end, f, *, t_eval=None, t_eval_offsets=None, method="dopri5",
+                 atol=1e-6, rtol=1e-6, controller: PidCoefficients | None = None,
+                 max_steps: int = DEFAULT_MAX_STEPS, dt0=None, order=None, cost_hint=None,
+                 mode: str = "exact", record_trace: bool = False, stream=None,
+                 threads_per_block: int = 0, blocks: int = 0):
+    """Device-resident solve on torch CUDA tensors; asynchronous (no host
+    sync).  ``t_eval``: None, a 1-D tensor shared by all instances, a 2-D
+    (n, m) tensor, or CSR values with ``t_eval_offsets`` (n+1).  ``atol`` /
+    ``rtol`` / ``dt0``: Python floats or (n,) tensors.  Returns a dict of
+    device tensors: ys, n_emitted, n_steps, n_accepted, final_dt, status,
+    n_f_evals (+ trace_* when ``record_trace``)."""
+    import torch
+
+    lib = _abi.load()
+    if max_steps < 1:
+        raise ValueError("max_steps must be at least 1")
+    dyn = as_device_dynamics(f)
+    method = method_of(method)
+    controller = controller if controller is not None else integral_controller()
+    dev = y0.device
+    if dev.type != "cuda":
+        raise ValueError("solve_device needs CUDA tensors")
+    f64 = dict(dtype=torch.float64, device=dev)
+    y0 = y0.to(**f64).contiguous()
+    n, d = y0.shape
+    dyn.check_width(d)
+    t_start = torch.as_tensor(t_start, **f64).expand(n).contiguous()
+    t_end = torch.as_tensor(t_end, **f64).expand(n).contiguous()
+    keep = [y0, t_start, t_end]
+
+    def dptr(x):
+        t = torch.as_tensor(x, device=dev).contiguous()
+        keep.append(t)
+        return t.data_ptr()
+
+    a = _abi.SolveArgs()
+    a.abi_version = _abi.ABI_VERSION
+    a.method = _abi.METHOD[method]
+    a.mode = _abi.MODE[mode]
+    a.n, a.d = n, d
+    a.dyn = build_struct(dyn, n, keep, device_arrays=dptr)
+    a.ctrl = _controller_struct(controller)
+    a.y0, a.t_start, a.t_end = y0.data_ptr(), t_start.data_ptr(), t_end.data_ptr()
+    offsets = None
+    if t_eval is None:
+        n_rows, shared_len = 0, 0
+    elif t_eval_offsets is not None:
+        tv = t_eval.to(**f64).contiguous()
+        offsets = t_eval_offsets.to(dtype=torch.int64, device=dev).contiguous()
+        keep += [tv, offsets]
+        a.t_eval, a.t_eval_offsets = tv.data_ptr(), offsets.data_ptr()
+        n_rows, shared_len = tv.numel(), 0
+    elif t_eval.dim() == 1:
+        tv = t_eval.to(**f64).contiguous()
+        keep.append(tv)
+        a.t_eval, a.t_eval_len = tv.data_ptr(), tv.numel()
+        n_rows, shared_len = n * tv.numel(), tv.numel()
+    else:
+        tv = t_eval.to(**f64).contiguous()
+        m = tv.shape[1]
+        offsets = torch.arange(n + 1, device=dev, dtype=torch.int64) * m
+        keep += [tv, offsets]
+        a.t_eval, a.t_eval_offsets = tv.data_ptr(), offsets.data_ptr()
+        n_rows, shared_len = n * m, 0
+    for name, v in (("atol", atol), ("rtol", rtol)):
+        if isinstance(v, torch.Tensor) and v.dim() > 0:
+            setattr(a, name + "_v", dptr(v.to(torch.float64)))
+        else:
+            setattr(a, name, float(v))
+    a.max_steps = int(max_steps)
+    if dt0 is None:
+        a.dt0_mode = _abi.DT0_HEURISTIC
+    elif isinstance(dt0, torch.Tensor) and dt0.dim() > 0:
+        a.dt0_mode, a.dt0_v = _abi.DT0_ARRAY, dptr(dt0.to(torch.float64))
+    else:
+        a.dt0_mode, a.dt0 = _abi.DT0_SCALAR, float(dt0)
+    if order is None and cost_hint is not None:
+        order = torch.argsort(cost_hint, descending=True, stable=True)
+    if order is not None:
+        a.order = dptr(order.to(torch.int64))
+    out = dict(
+        ys=torch.empty((max(n_rows, 1), d), **f64),
+        n_emitted=torch.empty(n, dtype=torch.int64, device=dev),
+        n_steps=torch.empty(n, dtype=torch.int64, device=dev),
+        n_accepted=torch.empty(n, dtype=torch.int64, device=dev),
+        final_dt=torch.empty(n, **f64),
+        status=torch.empty(n, dtype=torch.int32, device=dev),
+        n_f_evals=torch.empty(1, dtype=torch.int64, device=dev),
+    )
+    a.ys = out["ys"].data_ptr() if n_rows else None
+    for k in ("n_emitted", "n_steps", "n_accepted", "final_dt", "status", "n_f_evals"):
+        setattr(a, k, out[k].data_ptr())
+    if record_trace:
+        cap = int(max_steps)
+        out["trace_t"] = torch.zeros((n, cap), **f64)
+        out["trace_dt"] = torch.zeros((n, cap), **f64)
+        out["trace_accept"] = torch.zeros((n, cap), dtype=torch.uint8, device=dev)
+        a.trace_t, a.trace_dt = out["trace_t"].data_ptr(), out["trace_dt"].data_ptr()
+        a.trace_accept, a.trace_cap = out["trace_accept"].data_ptr(), cap
+    a.threads_per_block, a.blocks = int(threads_per_block), int(blocks)
+    wsb = lib.bode_workspace_size(_abi.C.byref(a))
+    if wsb == 0:
+        _abi.check(_abi.EINVAL)
+    ws = torch.empty(wsb, dtype=torch.uint8, device=dev)
+    keep.append(ws)
+    a.workspace, a.workspace_bytes = ws.data_ptr(), wsb
+    st = stream if stream is not None else torch.cuda.current_stream(dev)
+    a.stream = st.cuda_stream
+    _abi.check(lib.bode_solve(_abi.C.byref(a)))
+    # keep inputs alive until the stream has consumed them
+    for t in keep:
+        if isinstance(t, torch.Tensor):
+            t.record_stream(st)
+    out["ys"] = out["ys"][:n_rows]
+    out["offsets"] = offsets
+    out["shared_len"] = shared_len
+    return out
