@@ -17,6 +17,7 @@ import json
 import os
 import subprocess
 import sys
+import tempfile
 import time
 
 import numpy as np
@@ -161,7 +162,7 @@ class ClockSampler:
                  "clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
                  "clocks_event_reasons.hw_thermal_slowdown,"
                  "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", "50"],
                 stdout=self.fh, stderr=subprocess.DEVNULL)
         except Exception:
             self.proc = None
@@ -184,7 +185,7 @@ class ClockSampler:
         sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
         mx = max(float(r[2]) for r in rows if r[2].replace(".", "").isdigit())
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[k] for r in rows for k in range(4) if "Active" in r[5 + k]})
+        reasons = sorted({names[k] for r in rows for k in range(4) if r[5 + k] == "Active"})
         return dict(sm_mhz=float(np.median(sm)) if sm else None, sm_max_mhz=mx,
                     reasons=reasons, samples=len(rows))
 
@@ -251,8 +252,7 @@ def run_bode(args, rank, world, local_rank):
         dist.barrier()
     times, accepted, attempted = [], 0, 0
     kern_ms = 0.0
-    clock_path = os.path.join(ROOT, "gpurun_out" if os.path.isdir(os.path.join(ROOT, "gpurun_out"))
-                              else ".", f"clocks_rank{rank}.csv")
+    clock_path = os.path.join(tempfile.gettempdir(), f"bode_clocks_rank{rank}_{os.getpid()}.csv")
     with ClockSampler(clock_path) as clk:
         for _ in range(args.steps):
             flush.zero_()

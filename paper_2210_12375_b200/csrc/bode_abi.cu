@@ -28,6 +28,8 @@ int cuda_fail(cudaError_t e, const char* where) {
     return fail(BODE_EUNSUPPORTED, std::string(where) + ": unsupported dynamics/width combination");
   if (e == cudaErrorInvalidValue)
     return fail(BODE_EINVAL, std::string(where) + ": state width does not match the dynamics");
+  if (e == cudaErrorInvalidConfiguration)
+    return fail(BODE_EINVAL, std::string(where) + ": threads_per_block must be a multiple of 32, <= 128");
   return fail(BODE_ECUDA, std::string(where) + ": " + cudaGetErrorString(e));
 }
 
@@ -94,7 +96,7 @@ int validate(const bode_solve_args* a) {
 }
 
 size_t ws_bytes(const bode_solve_args* a) {
-  size_t b = Workspace::bytes(a->max_steps);
+  size_t b = Workspace::bytes(a->max_steps, a->n, a->d);
   if (a->dyn.kind == BODE_DYN_MLP) b += mlp_workspace_bytes(a);
   return b;
 }
@@ -122,7 +124,8 @@ int bode_solve(const bode_solve_args* a) {
     return fail(BODE_EINVAL, "workspace too small (see bode_workspace_size)");
   cudaStream_t st = (cudaStream_t)a->stream;
   const size_t words = Workspace::bitmap_words(a->max_steps);
-  cudaError_t e = cudaMemsetAsync(a->workspace, 0, Workspace::kHeader + 4 * words, st);
+  cudaError_t e = cudaMemsetAsync(a->workspace, 0,
+                                  Workspace::kHeader + Workspace::bitmap_bytes(a->max_steps), st);
   if (e != cudaSuccess) return cuda_fail(e, "workspace reset");
 
   SolveParams P;
@@ -159,11 +162,12 @@ int bode_solve(const bode_solve_args* a) {
   P.queue = (unsigned long long*)ws;
   P.max_n = (unsigned long long*)(ws + 8);
   P.refresh = (uint32_t*)(ws + Workspace::kHeader);
+  P.f0 = (double*)(ws + Workspace::f0_offset(a->max_steps));
   // per-block shared bitmap when it fits comfortably (<= 32 KB)
   P.smem_words = words * 4 <= 32 * 1024 ? (int32_t)words : 0;
 
   if (a->dyn.kind == BODE_DYN_MLP) {
-    e = mlp_solve(a, P, ws + Workspace::bytes(a->max_steps), st);
+    e = mlp_solve(a, P, ws + Workspace::bytes(a->max_steps, a->n, a->d), st);
     if (e != cudaSuccess) return cuda_fail(e, "mlp solve");
   } else {
     switch (a->method) {

@@ -108,36 +108,36 @@ __device__ double pairwise_sum_rt(const double* a, int64_t n) {
 }
 
 // ------------------------------------------------------------ tableaus --
-template <int M> struct Tab;
-template <> struct Tab<BODE_METHOD_DOPRI5> {
+// Coefficients live in the constant bank so FP64 instructions take them as
+// c[bank][offset] operands (immediates would cost two UMOVs per 64-bit
+// literal).  Layout per method: a[7][7] | b[7] | b_err[7] | c[7] | w[7][4].
+static __constant__ double c_tab[3][98] = {BODE_DOPRI5_FLAT_INIT, BODE_TSIT5_FLAT_INIT,
+                                           BODE_HEUN_FLAT_INIT};
+
+template <int M> struct TabShape;
+template <> struct TabShape<BODE_METHOD_DOPRI5> {
   static constexpr int S = BODE_DOPRI5_STAGES, ORDER = BODE_DOPRI5_ORDER,
                        ERR_ORDER = BODE_DOPRI5_ERROR_ORDER, NI = BODE_DOPRI5_NINTERP;
   static constexpr bool FSAL = BODE_DOPRI5_FSAL;
-  static __device__ __forceinline__ constexpr double a(int i, int j) { return bode_dopri5_a(i, j); }
-  static __device__ __forceinline__ constexpr double b(int i) { return bode_dopri5_b(i); }
-  static __device__ __forceinline__ constexpr double e(int i) { return bode_dopri5_berr(i); }
-  static __device__ __forceinline__ constexpr double c(int i) { return bode_dopri5_c(i); }
-  static __device__ __forceinline__ constexpr double w(int i, int j) { return bode_dopri5_interp(i, j); }
 };
-template <> struct Tab<BODE_METHOD_TSIT5> {
+template <> struct TabShape<BODE_METHOD_TSIT5> {
   static constexpr int S = BODE_TSIT5_STAGES, ORDER = BODE_TSIT5_ORDER,
                        ERR_ORDER = BODE_TSIT5_ERROR_ORDER, NI = BODE_TSIT5_NINTERP;
   static constexpr bool FSAL = BODE_TSIT5_FSAL;
-  static __device__ __forceinline__ constexpr double a(int i, int j) { return bode_tsit5_a(i, j); }
-  static __device__ __forceinline__ constexpr double b(int i) { return bode_tsit5_b(i); }
-  static __device__ __forceinline__ constexpr double e(int i) { return bode_tsit5_berr(i); }
-  static __device__ __forceinline__ constexpr double c(int i) { return bode_tsit5_c(i); }
-  static __device__ __forceinline__ constexpr double w(int i, int j) { return bode_tsit5_interp(i, j); }
 };
-template <> struct Tab<BODE_METHOD_HEUN> {
+template <> struct TabShape<BODE_METHOD_HEUN> {
   static constexpr int S = BODE_HEUN_STAGES, ORDER = BODE_HEUN_ORDER,
                        ERR_ORDER = BODE_HEUN_ERROR_ORDER, NI = BODE_HEUN_NINTERP;
   static constexpr bool FSAL = BODE_HEUN_FSAL;
-  static __device__ __forceinline__ constexpr double a(int i, int j) { return bode_heun_a(i, j); }
-  static __device__ __forceinline__ constexpr double b(int i) { return bode_heun_b(i); }
-  static __device__ __forceinline__ constexpr double e(int i) { return bode_heun_berr(i); }
-  static __device__ __forceinline__ constexpr double c(int i) { return bode_heun_c(i); }
-  static __device__ __forceinline__ constexpr double w(int i, int j) { return bode_heun_interp(i, j); }
+};
+
+template <int M>
+struct Tab : TabShape<M> {
+  static __device__ __forceinline__ double a(int i, int j) { return c_tab[M][i * 7 + j]; }
+  static __device__ __forceinline__ double b(int i) { return c_tab[M][49 + i]; }
+  static __device__ __forceinline__ double e(int i) { return c_tab[M][56 + i]; }
+  static __device__ __forceinline__ double c(int i) { return c_tab[M][63 + i]; }
+  static __device__ __forceinline__ double w(int i, int j) { return c_tab[M][70 + i * 4 + j]; }
 };
 
 // ------------------------------------------------------------ dynamics --

@@ -53,12 +53,17 @@ struct SolveParams {
   unsigned long long* max_n;   // max n_steps over the batch
   uint32_t* refresh;           // global bitmap over iterations
   int32_t smem_words;          // >0: per-block shared bitmap of this many words
+  double* f0;                  // (n, D) FSAL seeds from the init pass
 };
 
 struct Workspace {
   static constexpr size_t kHeader = 64;
   static size_t bitmap_words(int64_t max_steps) { return (size_t)((max_steps + 2 + 31) / 32); }
-  static size_t bytes(int64_t max_steps) { return kHeader + 4 * bitmap_words(max_steps); }
+  static size_t bitmap_bytes(int64_t max_steps) { return (4 * bitmap_words(max_steps) + 255) & ~(size_t)255; }
+  static size_t f0_offset(int64_t max_steps) { return kHeader + bitmap_bytes(max_steps); }
+  static size_t bytes(int64_t max_steps, int64_t n, int64_t d) {
+    return f0_offset(max_steps) + 8 * (size_t)n * (size_t)d;
+  }
 };
 
 template <int M, class F, class O>
@@ -74,8 +79,7 @@ struct Lane {
   double* ys;
   int32_t status;
 
-  // BatchSolver.__init__ for one row (solver.py:148-206)
-  __device__ __forceinline__ void init(const SolveParams& P, int64_t i) {
+  __device__ __forceinline__ void load_problem(const SolveParams& P, int64_t i) {
     idx = i;
     f.load(P.dyn, i);
     t = P.t_start[i];
@@ -94,6 +98,19 @@ struct Lane {
       m = P.t_eval_len;
       ys = P.ys ? P.ys + i * P.t_eval_len * D : nullptr;
     }
+    n1 = 1.0;
+    n2 = 1.0;
+    nsteps = 0;
+    nacc = 0;
+  }
+
+  // BatchSolver.__init__ for one row (solver.py:148-206): f0, dt0 and the
+  // INFINITE_DYNAMICS check, then the points equal to t_start.  Runs in the
+  // init pass (one non-divergent launch over the batch); its results go to
+  // the output buffers (dt -> final_dt, cursor -> n_emitted, status) and the
+  // f0 workspace, from which the persistent kernel resumes the row.
+  __device__ __forceinline__ void initialize(const SolveParams& P, int64_t i) {
+    load_problem(P, i);
     const double direction = (t_end - t) > 0.0 ? 1.0 : -1.0;
     if (P.dt0_mode == BODE_DT0_HEURISTIC) {
       dt = initial_step<F, O>(f, t, y, T::ORDER, atol, rtol, direction, k[0]);
@@ -118,10 +135,25 @@ struct Lane {
       }
       cursor++;
     }
-    n1 = 1.0;
-    n2 = 1.0;
-    nsteps = 0;
-    nacc = 0;
+    if (status == BODE_RUNNING) {
+#pragma unroll
+      for (int c = 0; c < D; c++) P.f0[i * D + c] = k[0][c];
+      P.final_dt[i] = dt;
+      P.n_emitted[i] = cursor;
+      P.status[i] = BODE_RUNNING;
+    } else {
+      finish(P);
+    }
+  }
+
+  // pick up a row prepared by the init pass
+  __device__ __forceinline__ void resume(const SolveParams& P, int64_t i) {
+    load_problem(P, i);
+#pragma unroll
+    for (int c = 0; c < D; c++) k[0][c] = P.f0[i * D + c];
+    dt = P.final_dt[i];
+    cursor = P.n_emitted[i];
+    status = BODE_RUNNING;
   }
 
   // one iteration of step_once for this row (solver.py:208-282); returns
@@ -190,7 +222,7 @@ struct Lane {
 };
 
 template <int M, class F, class O>
-__global__ void __launch_bounds__(128) bode_persistent_kernel(const SolveParams P) {
+__global__ void __launch_bounds__(128, 4) bode_persistent_kernel(const SolveParams P) {
   extern __shared__ uint32_t s_refresh[];
   const int lane = threadIdx.x & 31;
   for (int w = threadIdx.x; w < P.smem_words; w += blockDim.x) s_refresh[w] = 0u;
@@ -214,11 +246,9 @@ __global__ void __launch_bounds__(128) bode_persistent_kernel(const SolveParams 
           done = true;
         } else {
           const int64_t i = P.order ? P.order[pos] : (int64_t)pos;
-          L.init(P, i);
-          if (L.status == BODE_RUNNING) {
+          if (P.status[i] == BODE_RUNNING) {  // else finalised by the init pass
+            L.resume(P, i);
             have = true;
-          } else {
-            L.finish(P);
           }
         }
       }
@@ -257,6 +287,14 @@ __global__ void __launch_bounds__(128) bode_persistent_kernel(const SolveParams 
     if (s_refresh[w]) atomicOr(&P.refresh[w], s_refresh[w]);
 }
 
+template <int M, class F, class O>
+__global__ void __launch_bounds__(128) bode_init_kernel(const SolveParams P) {
+  Lane<M, F, O> L;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < P.n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    L.initialize(P, i);
+}
+
 // n_f_evals = 1 + (S-1)*max_n + #refresh iterations in [1, max_n)  (FSAL)
 //           = 1 + S*max_n                                        (non-FSAL)
 __global__ void bode_finalize_kernel(const unsigned long long* max_n, const uint32_t* refresh,
@@ -271,6 +309,7 @@ cudaError_t launch_persistent(const SolveParams& P, int threads, int blocks, cud
     if (e != cudaSuccess) return e;
   }
   if (threads <= 0) threads = 128;
+  if (threads > 128 || threads % 32) return cudaErrorInvalidConfiguration;
   if (blocks <= 0) {
     int dev = 0, sms = 0, per_sm = 0;
     cudaGetDevice(&dev);
@@ -280,6 +319,10 @@ cudaError_t launch_persistent(const SolveParams& P, int threads, int blocks, cud
     const int64_t need = (P.n + threads - 1) / threads;
     blocks = (int)((int64_t)sms * per_sm < need ? (int64_t)sms * per_sm : need);
     if (blocks < 1) blocks = 1;
+  }
+  {
+    const int64_t ib = (P.n + 127) / 128;
+    bode_init_kernel<M, F, O><<<(unsigned)(ib < 148 * 64 ? ib : 148 * 64), 128, 0, st>>>(P);
   }
   kern<<<blocks, threads, smem, st>>>(P);
   return cudaGetLastError();

@@ -236,7 +236,7 @@ def solve(problem: IvpBatch, f, tableau=None, tol: Tolerances | None = None,
     keep += [y0, ts, tn, te]
     a.y0, a.t_start, a.t_end = y0.ctypes.data, ts.ctypes.data, tn.ctypes.data
     a.t_eval = te.ctypes.data if te.size else None
-    if problem.te_shared:
+    if problem.te_shared or te.size == 0:
         a.t_eval_len = te.size
         n_rows = n * te.size
         offs = None
@@ -288,6 +288,8 @@ def solve(problem: IvpBatch, f, tableau=None, tol: Tolerances | None = None,
     stats = SolveStats(n_steps=n_steps, n_accepted=n_accepted,
                        n_f_evals=np.full(n, nfe[0], dtype=np.int64), final_dt=final_dt,
                        extra=extra)
+    if te.size == 0:
+        offs = None
     return Solution(ys[:n_rows], offs, te.size if problem.te_shared else 0, n_emitted, stats,
                     status.astype(np.int64), d)
 

@@ -1,0 +1,103 @@
+"""Host-side API (no GPU): validation mirrors the reference's ValueErrors,
+the C-ABI library loads and exports every symbol include/bode.h declares,
+and the binding's struct layout matches the compiled one."""
+import ctypes as C
+import os
+import re
+
+import numpy as np
+import pytest
+
+import oracle as O
+import paper_2210_12375_b200 as bode
+from paper_2210_12375_b200 import _abi
+from paper_2210_12375_b200.tableau import method_of
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def header_symbols():
+    src = open(os.path.join(ROOT, "include", "bode.h")).read()
+    return sorted(set(re.findall(r"^\w[\w\s\*]*?\b(bode_\w+)\(", src, re.M)))
+
+
+def test_library_exports_every_header_symbol():
+    lib = _abi.load()
+    syms = header_symbols()
+    assert len(syms) >= 12
+    for s in syms:
+        assert hasattr(lib, s), s
+        assert s in _abi.SIGNATURES, f"binding lacks {s}"
+    assert lib.bode_abi_version() == _abi.ABI_VERSION
+    assert lib.bode_sizeof_args() == C.sizeof(_abi.SolveArgs)
+    assert C.sizeof(O.Args) == C.sizeof(_abi.SolveArgs)
+
+
+def test_workspace_size_and_einval_without_gpu():
+    lib = _abi.load()
+    a = _abi.SolveArgs()
+    a.abi_version = 1
+    assert lib.bode_workspace_size(C.byref(a)) == 0  # n = 0 is invalid
+    assert "instance" in lib.bode_last_error().decode()
+    with pytest.raises(ValueError):
+        _abi.check(lib.bode_solve(C.byref(a)))
+
+
+def test_ivpbatch_validation():  # reference tests/test_solver.py:24-40
+    with pytest.raises(ValueError):
+        bode.IvpBatch(np.ones((1, 1)), np.zeros(1), np.zeros(1), [np.empty(0)])
+    with pytest.raises(ValueError):
+        bode.IvpBatch(np.ones((1, 1)), np.zeros(1), np.ones(1), [np.array([0.5, 0.2])])
+    with pytest.raises(ValueError):
+        bode.IvpBatch(np.ones((1, 1)), np.zeros(1), np.ones(1), [np.array([0.5, 2.0])])
+    with pytest.raises(ValueError):
+        bode.IvpBatch(np.ones((2, 1)), np.zeros(2), np.ones(2), [np.empty(0)])
+    with pytest.raises(ValueError):  # vectorised 2-D form, same rules
+        bode.IvpBatch(np.ones((2, 1)), np.zeros(2), np.ones(2), np.array([[0.1, 0.2], [0.3, 1.5]]))
+    with pytest.raises(ValueError):
+        bode.IvpBatch(np.ones((2, 1)), np.zeros(2), np.ones(2), np.array([0.5, 0.2]))
+    p = bode.IvpBatch(np.ones((2, 1)), np.ones(2), np.zeros(2), np.array([[0.9, 0.1], [1.0, 0.0]]))
+    assert p.t_eval[1].tolist() == [1.0, 0.0]
+
+
+def test_config_validation():  # reference tests/test_controller.py:31-58
+    with pytest.raises(ValueError):
+        bode.Tolerances(atol=-1.0, rtol=1e-6)
+    with pytest.raises(ValueError):
+        bode.Tolerances(atol=0.0, rtol=0.0)
+    with pytest.raises(ValueError):
+        bode.PidCoefficients(safety=0.0)
+    with pytest.raises(ValueError):
+        bode.PidCoefficients(factor_min=1.5)
+    for name in ("PI42", "PI33", "PI34", "H211", "H312"):
+        bode.pid_controller(name)
+    with pytest.raises(ValueError):
+        bode.pid_controller("nope")
+    with pytest.raises(ValueError):
+        bode.VdpParams(-1.0)
+
+
+def test_tableaus_validate_and_custom_rejected():
+    for tab in (bode.dopri5(), bode.tsit5(), bode.heun()):
+        tab.validate()
+        assert method_of(tab) == tab.method
+    t = bode.dopri5()
+    custom = bode.ButcherTableau(stages=t.stages, a=t.a, b=t.b, b_err=t.b_err * 2, c=t.c,
+                                 order=5, error_order=4, interp_coeffs=t.interp_coeffs, fsal=True)
+    with pytest.raises(NotImplementedError):
+        method_of(custom)
+
+
+def test_dynamics_packing_and_callables_rejected():
+    f = bode.forced_linear_dynamics(np.array([1.0, 2.0]), 0.5, 3.0)
+    shared, mask, cols = f.pack(2)
+    assert mask == 0b001 and shared[1] == 0.5 and shared[2] == 3.0
+    assert np.array_equal(cols[0], [1.0, 2.0])
+    with pytest.raises(ValueError):
+        f.pack(3)
+    with pytest.raises(ValueError):
+        bode.vdp_dynamics(bode.VdpParams(2.0)).check_width(3)
+    with pytest.raises(NotImplementedError):
+        bode.solve(bode.IvpBatch(np.ones((1, 1)), [0.0], [1.0], [np.empty(0)]), lambda t, y: y)
+    with pytest.raises(TypeError):
+        bode.vdp_dynamics(bode.VdpParams(2.0))(np.zeros(1), np.ones((1, 2)))
