@@ -174,6 +174,16 @@ typedef struct bode_solve_args {
   /* launch shape overrides (0 = auto) */
   int32_t threads_per_block;
   int32_t blocks;
+  /* optional per-instance cost estimate (n,): when set and `order` is NULL
+   * the library queues instances longest-first (LPT) with an on-device
+   * bucketed counting sort (1/16-octave buckets).  Scheduling only: results
+   * are identical for any order (batch independence). */
+  const double* cost_hint;
+  /* bode_solve_host only: split the batch into this many chunks and overlap
+   * chunk k's solve with chunk k+1's upload and chunk k-1's download
+   * (0 or 1 = no pipelining).  n_f_evals stays batch-global. */
+  int32_t pipeline_chunks;
+  int32_t _pad2;
 } bode_solve_args;
 
 int bode_abi_version(void);

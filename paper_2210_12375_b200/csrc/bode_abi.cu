@@ -2,15 +2,20 @@
 //
 // Translates bode_solve_args into kernel parameters, validates what the
 // reference validates (returning BODE_EINVAL where batchode raises
-// ValueError), and sequences: workspace reset -> persistent solver ->
-// n_f_evals finalisation, all asynchronous on the caller's stream.
+// ValueError), and sequences, asynchronously on the caller's stream:
+//   workspace reset -> [LPT queue order] -> init pass -> persistent solver
+//   -> n_f_evals finalisation.
+// bode_solve_host adds the host<->device copies and, optionally, a chunked
+// pipeline that overlaps chunk k's solve with the neighbouring chunks' copies.
 #include <cstdio>
 #include <cstring>
+#include <mutex>
 #include <string>
 #include <vector>
 
 #include "bode_dispatch.cuh"
 #include "bode_mlp.cuh"
+#include "bode_sched.cuh"
 #include "bode_units.cuh"
 
 using namespace bode;
@@ -92,13 +97,125 @@ int validate(const bode_solve_args* a) {
   if (a->dyn.kind == BODE_DYN_MLP &&
       (!a->dyn.W1 || !a->dyn.b1 || !a->dyn.W2 || !a->dyn.b2 || a->dyn.hidden < 1))
     return fail(BODE_EINVAL, "MLP weights required");
+  if (a->pipeline_chunks < 0) return fail(BODE_EINVAL, "pipeline_chunks must be >= 0");
   return BODE_OK;
 }
 
-size_t ws_bytes(const bode_solve_args* a) {
-  size_t b = Workspace::bytes(a->max_steps, a->n, a->d);
-  if (a->dyn.kind == BODE_DYN_MLP) b += mlp_workspace_bytes(a);
-  return b;
+// Workspace: [header | iteration bitmap | f0 (n_max x d) | LPT scratch | MLP scratch]
+struct Layout {
+  size_t f0, lpt, mlp, total;
+};
+
+Layout layout(const bode_solve_args* a, int64_t n_max) {
+  Layout L;
+  L.f0 = Workspace::f0_offset(a->max_steps);
+  L.lpt = L.f0 + ((8 * (size_t)n_max * (size_t)a->d + 255) & ~(size_t)255);
+  L.mlp = L.lpt + (a->cost_hint && !a->order ? ((lpt_workspace_bytes(n_max) + 255) & ~(size_t)255) : 0);
+  L.total = L.mlp + (a->dyn.kind == BODE_DYN_MLP ? mlp_workspace_bytes(a) : 0);
+  return L;
+}
+
+int64_t chunk_max(int64_t n, int chunks) { return chunks > 1 ? (n + chunks - 1) / chunks : n; }
+
+int reset_workspace(const bode_solve_args* a, cudaStream_t st) {
+  cudaError_t e = cudaMemsetAsync(a->workspace, 0,
+                                  Workspace::kHeader + Workspace::bitmap_bytes(a->max_steps), st);
+  return e == cudaSuccess ? BODE_OK : cuda_fail(e, "workspace reset");
+}
+
+// Solve rows [lo, hi) of the batch described by `a` (device pointers).  The
+// iteration bitmap and max n_steps accumulate across chunks, so n_f_evals
+// stays batch-global; the queue counter is reset per chunk.
+int run_chunk(const bode_solve_args* a, int64_t lo, int64_t hi, const Layout& L, cudaStream_t st) {
+  const int64_t n = hi - lo, d = a->d;
+  const int n_inst = __builtin_popcount(a->dyn.inst_mask);
+  char* ws = (char*)a->workspace;
+  cudaError_t e = cudaMemsetAsync(ws, 0, 8, st);  // queue counter
+  if (e != cudaSuccess) return cuda_fail(e, "queue reset");
+
+  SolveParams P;
+  memset(&P, 0, sizeof(P));
+  P.n = n;
+  P.dyn = make_dyn(a->dyn);
+  if (P.dyn.inst) P.dyn.inst += lo * n_inst;
+  P.ctrl = make_ctrl(a->ctrl, error_order_of(a->method));
+  P.y0 = a->y0 + lo * d;
+  P.t_start = a->t_start + lo;
+  P.t_end = a->t_end + lo;
+  P.t_eval = a->t_eval;
+  if (a->t_eval_offsets) {  // absolute row indices into t_eval / ys
+    P.t_eval_offsets = a->t_eval_offsets + lo;
+    P.ys = a->ys;
+  } else {
+    P.t_eval_len = a->t_eval_len;
+    P.ys = a->ys ? a->ys + lo * a->t_eval_len * d : nullptr;
+  }
+  P.atol_v = a->atol_v ? a->atol_v + lo : nullptr;
+  P.rtol_v = a->rtol_v ? a->rtol_v + lo : nullptr;
+  P.atol = a->atol;
+  P.rtol = a->rtol;
+  P.max_steps = a->max_steps;
+  P.dt0_mode = a->dt0_mode;
+  P.dt0 = a->dt0;
+  P.dt0_v = a->dt0_v ? a->dt0_v + lo : nullptr;
+  P.n_emitted = a->n_emitted + lo;
+  P.n_steps = a->n_steps + lo;
+  P.n_accepted = a->n_accepted + lo;
+  P.final_dt = a->final_dt + lo;
+  P.status = a->status + lo;
+  P.trace_cap = a->trace_cap;
+  P.trace_t = a->trace_t ? a->trace_t + lo * a->trace_cap : nullptr;
+  P.trace_dt = a->trace_dt ? a->trace_dt + lo * a->trace_cap : nullptr;
+  P.trace_accept = a->trace_accept ? a->trace_accept + lo * a->trace_cap : nullptr;
+  P.queue = (unsigned long long*)ws;
+  P.max_n = (unsigned long long*)(ws + 8);
+  P.refresh = (uint32_t*)(ws + Workspace::kHeader);
+  const size_t words = Workspace::bitmap_words(a->max_steps);
+  P.smem_words = words * 4 <= 32 * 1024 ? (int32_t)words : 0;  // per-block shared bitmap
+  P.f0 = (double*)(ws + L.f0);
+  if (a->order) {
+    if (lo != 0 || hi != a->n) return fail(BODE_EINVAL, "an explicit order cannot be chunked");
+    P.order = a->order;
+  } else if (a->cost_hint) {
+    int64_t* order = nullptr;
+    e = lpt_order(a->cost_hint + lo, n, ws + L.lpt, &order, st);
+    if (e != cudaSuccess) return cuda_fail(e, "LPT order");
+    P.order = order;
+  }
+  if (a->dyn.kind == BODE_DYN_MLP) {
+    e = mlp_solve(a, P, ws + L.mlp, st);
+    return e == cudaSuccess ? BODE_OK : cuda_fail(e, "mlp solve");
+  }
+  switch (a->method) {
+    case BODE_METHOD_DOPRI5: e = solve_dopri5(a->mode, a->dyn.kind, d, P, a->threads_per_block, a->blocks, st); break;
+    case BODE_METHOD_TSIT5: e = solve_tsit5(a->mode, a->dyn.kind, d, P, a->threads_per_block, a->blocks, st); break;
+    default: e = solve_heun(a->mode, a->dyn.kind, d, P, a->threads_per_block, a->blocks, st); break;
+  }
+  return e == cudaSuccess ? BODE_OK : cuda_fail(e, "solve launch");
+}
+
+int finalize(const bode_solve_args* a, cudaStream_t st) {
+  char* ws = (char*)a->workspace;
+  bode_finalize_kernel<<<1, 256, 0, st>>>((unsigned long long*)(ws + 8),
+                                          (uint32_t*)(ws + Workspace::kHeader),
+                                          stages_of(a->method), fsal_of(a->method), a->n_f_evals);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? BODE_OK : cuda_fail(e, "finalize launch");
+}
+
+// keep freed device memory in the stream-ordered pool across calls instead
+// of returning it to the driver at every synchronisation
+void retain_pool() {
+  static std::once_flag once;
+  std::call_once(once, [] {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t thr = ~0ull;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+  });
 }
 
 }  // namespace
@@ -113,165 +230,212 @@ const char* bode_last_error(void) { return g_err.c_str(); }
 
 size_t bode_workspace_size(const bode_solve_args* a) {
   if (validate(a) != BODE_OK) return 0;
-  return ws_bytes(a);
+  return layout(a, a->n).total;
 }
 
 int bode_solve(const bode_solve_args* a) {
   int rc = validate(a);
   if (rc != BODE_OK) return rc;
-  const size_t need = ws_bytes(a);
-  if (!a->workspace || a->workspace_bytes < need)
+  const Layout L = layout(a, a->n);
+  if (!a->workspace || a->workspace_bytes < L.total)
     return fail(BODE_EINVAL, "workspace too small (see bode_workspace_size)");
   cudaStream_t st = (cudaStream_t)a->stream;
-  const size_t words = Workspace::bitmap_words(a->max_steps);
-  cudaError_t e = cudaMemsetAsync(a->workspace, 0,
-                                  Workspace::kHeader + Workspace::bitmap_bytes(a->max_steps), st);
-  if (e != cudaSuccess) return cuda_fail(e, "workspace reset");
-
-  SolveParams P;
-  memset(&P, 0, sizeof(P));
-  P.n = a->n;
-  P.dyn = make_dyn(a->dyn);
-  P.ctrl = make_ctrl(a->ctrl, error_order_of(a->method));
-  P.y0 = a->y0;
-  P.t_start = a->t_start;
-  P.t_end = a->t_end;
-  P.t_eval = a->t_eval;
-  P.t_eval_offsets = a->t_eval_offsets;
-  P.t_eval_len = a->t_eval_offsets ? 0 : a->t_eval_len;
-  P.atol_v = a->atol_v;
-  P.rtol_v = a->rtol_v;
-  P.atol = a->atol;
-  P.rtol = a->rtol;
-  P.max_steps = a->max_steps;
-  P.dt0_mode = a->dt0_mode;
-  P.dt0 = a->dt0;
-  P.dt0_v = a->dt0_v;
-  P.order = a->order;
-  P.ys = a->ys;
-  P.n_emitted = a->n_emitted;
-  P.n_steps = a->n_steps;
-  P.n_accepted = a->n_accepted;
-  P.final_dt = a->final_dt;
-  P.status = a->status;
-  P.trace_t = a->trace_t;
-  P.trace_dt = a->trace_dt;
-  P.trace_accept = a->trace_accept;
-  P.trace_cap = a->trace_cap;
-  char* ws = (char*)a->workspace;
-  P.queue = (unsigned long long*)ws;
-  P.max_n = (unsigned long long*)(ws + 8);
-  P.refresh = (uint32_t*)(ws + Workspace::kHeader);
-  P.f0 = (double*)(ws + Workspace::f0_offset(a->max_steps));
-  // per-block shared bitmap when it fits comfortably (<= 32 KB)
-  P.smem_words = words * 4 <= 32 * 1024 ? (int32_t)words : 0;
-
-  if (a->dyn.kind == BODE_DYN_MLP) {
-    e = mlp_solve(a, P, ws + Workspace::bytes(a->max_steps, a->n, a->d), st);
-    if (e != cudaSuccess) return cuda_fail(e, "mlp solve");
-  } else {
-    switch (a->method) {
-      case BODE_METHOD_DOPRI5: e = solve_dopri5(a->mode, a->dyn.kind, a->d, P, a->threads_per_block, a->blocks, st); break;
-      case BODE_METHOD_TSIT5: e = solve_tsit5(a->mode, a->dyn.kind, a->d, P, a->threads_per_block, a->blocks, st); break;
-      default: e = solve_heun(a->mode, a->dyn.kind, a->d, P, a->threads_per_block, a->blocks, st); break;
-    }
-    if (e != cudaSuccess) return cuda_fail(e, "solve launch");
-  }
-  bode_finalize_kernel<<<1, 256, 0, st>>>(P.max_n, P.refresh, stages_of(a->method),
-                                          fsal_of(a->method), a->n_f_evals);
-  e = cudaGetLastError();
-  if (e != cudaSuccess) return cuda_fail(e, "finalize launch");
-  return BODE_OK;
+  if ((rc = reset_workspace(a, st)) != BODE_OK) return rc;
+  if ((rc = run_chunk(a, 0, a->n, L, st)) != BODE_OK) return rc;
+  return finalize(a, st);
 }
 
 int bode_solve_host(const bode_solve_args* h) {
   int rc = validate(h);
   if (rc != BODE_OK) return rc;
+  retain_pool();
   const int64_t n = h->n, d = h->d;
-  const int64_t n_te = h->t_eval_offsets ? h->t_eval_offsets[n] : h->t_eval_len;
-  const int64_t ys_rows = h->t_eval_offsets ? n_te : n * h->t_eval_len;
+  const bool csr = h->t_eval_offsets != nullptr;
+  const int64_t n_te = csr ? h->t_eval_offsets[n] : h->t_eval_len;
+  const int64_t ys_rows = csr ? n_te : n * h->t_eval_len;
   const int n_inst = __builtin_popcount(h->dyn.inst_mask);
+  int chunks = h->pipeline_chunks > 1 ? h->pipeline_chunks : 1;
+  if (h->order || h->trace_cap > 0 || h->dyn.kind == BODE_DYN_MLP) chunks = 1;
+  if (chunks > n) chunks = (int)n;
+  const int64_t cmax = chunk_max(n, chunks);
 
-  struct Blk {
-    const void* src;
-    void* dst_host;
-    size_t bytes;
-    size_t off;
+  // one device block for every array; per-instance arrays are copied in
+  // chunk slices so chunk k can start as soon as its own rows landed
+  struct Arr {
+    const void* hsrc;   // host input (or null)
+    void* hdst;         // host output (or null)
+    size_t row_bytes;   // bytes per instance row (0: whole array, chunk 0)
+    size_t bytes;       // total bytes
+    size_t off;         // device offset
+    const void** in_field;
+    void** out_field;
   };
-  std::vector<Blk> ins, outs;
+  bode_solve_args a = *h;
+  std::vector<Arr> arrs;
   size_t total = 0;
-  auto add = [&](std::vector<Blk>& v, const void* src, void* dsth, size_t bytes) -> size_t {
+  auto place = [&](size_t bytes) {
     const size_t off = total;
-    v.push_back({src, dsth, bytes, off});
     total += (bytes + 255) & ~(size_t)255;
     return off;
   };
-  bode_solve_args a = *h;
-  std::vector<std::pair<const void**, size_t>> in_ptrs;
-  auto in = [&](const void** field, size_t bytes) {
-    if (*field && bytes) in_ptrs.push_back({field, add(ins, *field, nullptr, bytes)});
+  auto in = [&](const void** field, size_t row_bytes, size_t bytes) {
+    if (*field && bytes) arrs.push_back({*field, nullptr, row_bytes, bytes, place(bytes), field, nullptr});
   };
-  in((const void**)&a.y0, sizeof(double) * n * d);
-  in((const void**)&a.t_start, sizeof(double) * n);
-  in((const void**)&a.t_end, sizeof(double) * n);
-  in((const void**)&a.t_eval, sizeof(double) * n_te);
-  in((const void**)&a.t_eval_offsets, h->t_eval_offsets ? sizeof(int64_t) * (n + 1) : 0);
-  in((const void**)&a.atol_v, sizeof(double) * n);
-  in((const void**)&a.rtol_v, sizeof(double) * n);
-  in((const void**)&a.dt0_v, a.dt0_mode == BODE_DT0_ARRAY ? sizeof(double) * n : 0);
-  in((const void**)&a.order, sizeof(int64_t) * n);
-  in((const void**)&a.dyn.inst_params, sizeof(double) * n * n_inst);
+  auto out = [&](void** field, size_t row_bytes, size_t bytes) {
+    if (*field && bytes) arrs.push_back({nullptr, *field, row_bytes, bytes, place(bytes), nullptr, field});
+  };
+  in((const void**)&a.y0, 8 * d, 8 * n * d);
+  in((const void**)&a.t_start, 8, 8 * n);
+  in((const void**)&a.t_end, 8, 8 * n);
+  in((const void**)&a.t_eval, 0, 8 * n_te);
+  in((const void**)&a.t_eval_offsets, 0, csr ? 8 * (n + 1) : 0);
+  in((const void**)&a.atol_v, 8, 8 * n);
+  in((const void**)&a.rtol_v, 8, 8 * n);
+  in((const void**)&a.dt0_v, 8, a.dt0_mode == BODE_DT0_ARRAY ? 8 * n : 0);
+  in((const void**)&a.order, 0, 8 * n);
+  in((const void**)&a.cost_hint, 8, 8 * n);
+  in((const void**)&a.dyn.inst_params, 8 * n_inst, 8 * n * n_inst);
   if (h->dyn.kind == BODE_DYN_MLP) {
     const int64_t H = h->dyn.hidden;
-    in((const void**)&a.dyn.W1, sizeof(float) * H * d);
-    in((const void**)&a.dyn.b1, sizeof(float) * H);
-    in((const void**)&a.dyn.W2, sizeof(float) * d * H);
-    in((const void**)&a.dyn.b2, sizeof(float) * d);
+    in((const void**)&a.dyn.W1, 0, 4 * H * d);
+    in((const void**)&a.dyn.b1, 0, 4 * H);
+    in((const void**)&a.dyn.W2, 0, 4 * d * H);
+    in((const void**)&a.dyn.b2, 0, 4 * d);
   }
-  std::vector<std::pair<void**, size_t>> out_ptrs;
-  auto out = [&](void** field, size_t bytes) {
-    if (*field && bytes) out_ptrs.push_back({field, add(outs, nullptr, *field, bytes)});
-  };
-  out((void**)&a.ys, sizeof(double) * ys_rows * d);
-  out((void**)&a.n_emitted, sizeof(int64_t) * n);
-  out((void**)&a.n_steps, sizeof(int64_t) * n);
-  out((void**)&a.n_accepted, sizeof(int64_t) * n);
-  out((void**)&a.final_dt, sizeof(double) * n);
-  out((void**)&a.status, sizeof(int32_t) * n);
-  out((void**)&a.n_f_evals, sizeof(int64_t));
-  out((void**)&a.trace_t, sizeof(double) * n * h->trace_cap);
-  out((void**)&a.trace_dt, sizeof(double) * n * h->trace_cap);
-  out((void**)&a.trace_accept, sizeof(uint8_t) * n * h->trace_cap);
-  const size_t ws_off = total;
-  const size_t wsb = ws_bytes(h);
-  total += wsb;
+  const size_t n_in = arrs.size();
+  // ys rows follow the instance order, so they can be fetched per chunk
+  out((void**)&a.ys, 0, 8 * ys_rows * d);
+  out((void**)&a.n_emitted, 8, 8 * n);
+  out((void**)&a.n_steps, 8, 8 * n);
+  out((void**)&a.n_accepted, 8, 8 * n);
+  out((void**)&a.final_dt, 8, 8 * n);
+  out((void**)&a.status, 4, 4 * n);
+  out((void**)&a.trace_t, 8 * h->trace_cap, 8 * n * h->trace_cap);
+  out((void**)&a.trace_dt, 8 * h->trace_cap, 8 * n * h->trace_cap);
+  out((void**)&a.trace_accept, h->trace_cap, n * h->trace_cap);
+  const size_t nfe_off = place(8);
+  const Layout L = layout(h, cmax);
+  const size_t ws_off = place(L.total);
 
   cudaStream_t st = (cudaStream_t)h->stream;
+  cudaStream_t cs = st;  // copy stream (separate only when pipelining)
+  cudaEvent_t ev_in[64], ev_done[64];
+  if (chunks > 64) chunks = 64;
   char* dev = nullptr;
   cudaError_t e = cudaMallocAsync((void**)&dev, total, st);
   if (e != cudaSuccess) return cuda_fail(e, "device allocation");
-  for (auto& p : in_ptrs) {
-    const Blk* b = nullptr;
-    for (auto& x : ins)
-      if (x.off == p.second) b = &x;
-    e = cudaMemcpyAsync(dev + b->off, b->src, b->bytes, cudaMemcpyHostToDevice, st);
-    if (e != cudaSuccess) break;
-    *p.first = dev + b->off;
+  for (auto& x : arrs) {
+    if (x.in_field) *x.in_field = dev + x.off;
+    if (x.out_field) *x.out_field = dev + x.off;
   }
-  for (auto& p : out_ptrs) *p.first = dev + p.second;
+  int64_t* d_nfe = (int64_t*)(dev + nfe_off);
+  a.n_f_evals = d_nfe;
   a.workspace = dev + ws_off;
-  a.workspace_bytes = wsb;
-  if (e == cudaSuccess) {
-    rc = bode_solve(&a);
-    if (rc == BODE_OK) {
-      for (auto& b : outs) {
-        e = cudaMemcpyAsync(b.dst_host, dev + b.off, b.bytes, cudaMemcpyDeviceToHost, st);
-        if (e != cudaSuccess) break;
+  a.workspace_bytes = L.total;
+  if (chunks > 1) {
+    if ((e = cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking)) != cudaSuccess)
+      return cuda_fail(e, "copy stream");
+    for (int k = 0; k < chunks; k++) {
+      cudaEventCreateWithFlags(&ev_in[k], cudaEventDisableTiming);
+      cudaEventCreateWithFlags(&ev_done[k], cudaEventDisableTiming);
+    }
+    cudaEvent_t ready;  // allocation visible to the copy stream
+    cudaEventCreateWithFlags(&ready, cudaEventDisableTiming);
+    cudaEventRecord(ready, st);
+    cudaStreamWaitEvent(cs, ready, 0);
+    cudaEventDestroy(ready);
+  }
+  auto rows = [&](int k, int64_t& lo, int64_t& hi) {
+    lo = (int64_t)k * cmax;
+    hi = lo + cmax < n ? lo + cmax : n;
+  };
+  auto copy_in = [&](int k) -> cudaError_t {
+    int64_t lo, hi;
+    rows(k, lo, hi);
+    for (size_t j = 0; j < n_in; j++) {
+      const Arr& x = arrs[j];
+      size_t o = 0, b = x.bytes;
+      if (x.row_bytes) {
+        o = (size_t)lo * x.row_bytes;
+        b = (size_t)(hi - lo) * x.row_bytes;
+      } else if (k != 0) {
+        continue;  // whole arrays travel with chunk 0
+      }
+      cudaError_t r = cudaMemcpyAsync(dev + x.off + o, (const char*)x.hsrc + o, b,
+                                      cudaMemcpyHostToDevice, cs);
+      if (r != cudaSuccess) return r;
+    }
+    return cudaSuccess;
+  };
+  auto copy_out = [&](int k) -> cudaError_t {
+    int64_t lo, hi;
+    rows(k, lo, hi);
+    for (size_t j = n_in; j < arrs.size(); j++) {
+      const Arr& x = arrs[j];
+      size_t o, b;
+      if (x.row_bytes) {
+        o = (size_t)lo * x.row_bytes;
+        b = (size_t)(hi - lo) * x.row_bytes;
+      } else {  // ys: rows [row_lo, row_hi) of this chunk
+        const int64_t r0 = csr ? h->t_eval_offsets[lo] : lo * h->t_eval_len;
+        const int64_t r1 = csr ? h->t_eval_offsets[hi] : hi * h->t_eval_len;
+        o = (size_t)r0 * 8 * d;
+        b = (size_t)(r1 - r0) * 8 * d;
+      }
+      if (!b) continue;
+      cudaError_t r = cudaMemcpyAsync((char*)x.hdst + o, dev + x.off + o, b,
+                                      cudaMemcpyDeviceToHost, cs);
+      if (r != cudaSuccess) return r;
+    }
+    return cudaSuccess;
+  };
+
+  rc = reset_workspace(&a, st);
+  for (int k = 0; k < chunks && rc == BODE_OK && e == cudaSuccess; k++) {
+    // upload chunk k (the host call returns once its pageable data is
+    // staged, so chunk k-1's solve is already running on the GPU)
+    if ((e = copy_in(k)) != cudaSuccess) break;
+    if (chunks > 1) {
+      cudaEventRecord(ev_in[k], cs);
+      cudaStreamWaitEvent(st, ev_in[k], 0);
+    }
+    int64_t lo, hi;
+    rows(k, lo, hi);
+    if ((rc = run_chunk(&a, lo, hi, L, st)) != BODE_OK) break;
+    if (chunks > 1) {
+      cudaEventRecord(ev_done[k], st);
+      if (k > 0) {  // download chunk k-1 while chunk k computes
+        cudaStreamWaitEvent(cs, ev_done[k - 1], 0);
+        if ((e = copy_out(k - 1)) != cudaSuccess) break;
       }
     }
   }
+  if (rc == BODE_OK && e == cudaSuccess) rc = finalize(&a, st);
+  if (rc == BODE_OK && e == cudaSuccess) {
+    if (chunks > 1) {
+      cudaStreamWaitEvent(cs, ev_done[chunks - 1], 0);
+      e = copy_out(chunks - 1);
+      cudaEvent_t fin;
+      cudaEventCreateWithFlags(&fin, cudaEventDisableTiming);
+      cudaEventRecord(fin, cs);
+      cudaStreamWaitEvent(st, fin, 0);
+      cudaEventDestroy(fin);
+    } else {
+      e = copy_out(0);
+    }
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(h->n_f_evals, d_nfe, 8, cudaMemcpyDeviceToHost, st);
+  }
   cudaFreeAsync(dev, st);
   cudaError_t e2 = cudaStreamSynchronize(st);
+  if (chunks > 1) {
+    cudaStreamSynchronize(cs);
+    for (int k = 0; k < chunks; k++) {
+      cudaEventDestroy(ev_in[k]);
+      cudaEventDestroy(ev_done[k]);
+    }
+    cudaStreamDestroy(cs);
+  }
   if (rc != BODE_OK) return rc;
   if (e != cudaSuccess) return cuda_fail(e, "host<->device copy");
   if (e2 != cudaSuccess) return cuda_fail(e2, "solve");

@@ -1,0 +1,13 @@
+// bode_sched.cuh -- LPT queue ordering (bode_sched.cu).
+#pragma once
+#include <cstddef>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace bode {
+size_t lpt_workspace_bytes(int64_t n);
+// Builds a longest-first permutation of [0, n) from per-instance costs into
+// the workspace; *order_out points into ws.
+cudaError_t lpt_order(const double* cost, int64_t n, void* ws, int64_t** order_out,
+                      cudaStream_t st);
+}  // namespace bode

@@ -209,7 +209,7 @@ def _tol_arrays(tol: Tolerances, n: int):
 def solve(problem: IvpBatch, f, tableau=None, tol: Tolerances | None = None,
           controller: PidCoefficients | None = None, max_steps: int = DEFAULT_MAX_STEPS,
           dt0=None, record_trace: bool = False, *, mode: str = "exact", order=None,
-          cost_hint=None) -> Solution:
+          cost_hint=None, pipeline_chunks: int = 4) -> Solution:
     """Integrate every instance independently with adaptive steps on the GPU
     (reference ``solve``, solver.py:352-369), host arrays in and out."""
     if max_steps < 1:
@@ -258,12 +258,15 @@ def solve(problem: IvpBatch, f, tableau=None, tol: Tolerances | None = None,
         dv = np.ascontiguousarray(np.broadcast_to(np.asarray(dt0, dtype=np.float64), (n,)))
         keep.append(dv)
         a.dt0_mode, a.dt0_v = _abi.DT0_ARRAY, dv.ctypes.data
-    if order is None and cost_hint is not None:
-        order = np.argsort(-np.asarray(cost_hint, dtype=np.float64), kind="stable")
     if order is not None:
         order = np.ascontiguousarray(np.asarray(order, dtype=np.int64))
         keep.append(order)
         a.order = order.ctypes.data
+    elif cost_hint is not None:  # LPT queue order built on the device
+        ch = np.ascontiguousarray(np.broadcast_to(np.asarray(cost_hint, dtype=np.float64), (n,)))
+        keep.append(ch)
+        a.cost_hint = ch.ctypes.data
+    a.pipeline_chunks = int(pipeline_chunks) if n >= 65536 else 1
     ys = np.empty((max(n_rows, 1), d))
     n_emitted = np.empty(n, np.int64)
     n_steps = np.empty(n, np.int64)
@@ -370,10 +373,10 @@ def solve_device(y0, t_start, t_end, f, *, t_eval=None, t_eval_offsets=None, met
         a.dt0_mode, a.dt0_v = _abi.DT0_ARRAY, dptr(dt0.to(torch.float64))
     else:
         a.dt0_mode, a.dt0 = _abi.DT0_SCALAR, float(dt0)
-    if order is None and cost_hint is not None:
-        order = torch.argsort(cost_hint, descending=True, stable=True)
     if order is not None:
         a.order = dptr(order.to(torch.int64))
+    elif cost_hint is not None:  # LPT queue order built on the device
+        a.cost_hint = dptr(torch.as_tensor(cost_hint, dtype=torch.float64, device=dev).expand(n))
     out = dict(
         ys=torch.empty((max(n_rows, 1), d), **f64),
         n_emitted=torch.empty(n, dtype=torch.int64, device=dev),

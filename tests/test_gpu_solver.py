@@ -235,3 +235,23 @@ def test_acceptance_4_large_batch_accuracy():  # tests/test_acceptance.py:116-12
 def test_unregistered_callable_is_rejected():
     with pytest.raises(NotImplementedError):
         bode.solve(_prob(np.ones((1, 1))), lambda t, y: y)
+
+
+def test_pipelined_host_path_matches_single_chunk():
+    """bode_solve_host's chunked copy/compute pipeline (and the on-device LPT
+    order) change only the schedule: every output, including the
+    batch-global n_f_evals, is bit-identical."""
+    rng = np.random.default_rng(21)
+    n = 100_003
+    mu = rng.uniform(1.0, 10.0, n)
+    t_end = rng.uniform(5.0, 20.0, n)
+    te = [np.sort(rng.uniform(0.0, x, rng.integers(0, 4))) for x in t_end]
+    prob = bode.IvpBatch(np.tile([2.0, 0.0], (n, 1)), np.zeros(n), t_end, te)
+    f = bode.vdp_dynamics(bode.VdpParams(mu))
+    a = bode.solve(prob, f, controller=PI42, pipeline_chunks=1)
+    for chunks, cost in ((4, None), (7, mu * t_end), (1, mu * t_end)):
+        b = bode.solve(prob, f, controller=PI42, pipeline_chunks=chunks, cost_hint=cost)
+        assert np.array_equal(a.ys_flat, b.ys_flat)
+        for k in ("n_steps", "n_accepted", "n_f_evals", "final_dt"):
+            assert np.array_equal(getattr(a.stats, k), getattr(b.stats, k)), k
+        assert np.array_equal(a.status, b.status) and np.array_equal(a.n_emitted, b.n_emitted)
