@@ -8,6 +8,7 @@
 #include <cuda_runtime.h>
 
 #include "../../include/bode.h"
+#include "bode_pow.cuh"
 #include "tableau_coeffs.h"
 
 namespace bode {
@@ -45,13 +46,14 @@ __device__ __forceinline__ double np_min(double a, double b) {
 
 // array ** python-float the way NumPy evaluates it (fast_scalar_power
 // short-cuts for 0, +-1, 2, 0.5; controller.py:221-226, :193)
-__device__ __forceinline__ double np_scalar_pow(double x, double e) {
+__device__ __forceinline__ double np_scalar_pow(double x, double e,
+                                                const PowTables& T = g_pow_tables) {
   if (e == 0.0) return 1.0;
   if (e == 1.0) return x;
   if (e == -1.0) return ddiv(1.0, x);
   if (e == 2.0) return __dmul_rn(x, x);
   if (e == 0.5) return dsqrt(x);
-  return pow(x, e);
+  return cr_pow(x, e, T);  // correctly rounded w.h.p. (bode_pow.cuh)
 }
 
 // NumPy pairwise_sum (umath loops_utils.h.src) seeded with 0.0, which is the
@@ -313,14 +315,14 @@ __device__ __forceinline__ double error_norm(const double* e, const double* y0, 
 // adapt_step, controller.py:200-238 (one instance).  dt is dt_used on entry,
 // dt_next on exit; returns accept.
 __device__ __forceinline__ bool adapt(const CtrlParams& C, double norm, double& n1, double& n2,
-                                      double& dt) {
+                                      double& dt, const PowTables& T = g_pow_tables) {
   const bool accept = norm <= 1.0;
   const double a = np_max(norm, 1e-10);
   const double b = np_max(n1, 1e-10);
   const double g = np_max(n2, 1e-10);
-  double factor = __dmul_rn(C.safety, np_scalar_pow(a, C.e1));
-  if (C.e2 != 0.0) factor = __dmul_rn(factor, np_scalar_pow(b, C.e2));
-  if (C.e3 != 0.0) factor = __dmul_rn(factor, np_scalar_pow(g, C.e3));
+  double factor = __dmul_rn(C.safety, np_scalar_pow(a, C.e1, T));
+  if (C.e2 != 0.0) factor = __dmul_rn(factor, np_scalar_pow(b, C.e2, T));
+  if (C.e3 != 0.0) factor = __dmul_rn(factor, np_scalar_pow(g, C.e3, T));
   if (!isfinite(factor)) factor = C.fmin;
   factor = np_min(np_max(factor, C.fmin), C.fmax);
   dt = __dmul_rn(dt, factor);

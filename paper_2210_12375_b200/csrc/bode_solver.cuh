@@ -159,7 +159,7 @@ struct Lane {
   // one iteration of step_once for this row (solver.py:208-282); returns
   // true when the row just rejected and is still running (FSAL refresh at
   // the next iteration, solver.py:220-226)
-  __device__ __forceinline__ bool step(const SolveParams& P) {
+  __device__ __forceinline__ bool step(const SolveParams& P, const PowTables& PT) {
     const int64_t j = nsteps;
     const double remaining = O::sub(t_end, t);
     const bool trunc = fabs(dt) >= fabs(remaining);
@@ -168,7 +168,7 @@ struct Lane {
     rk_step<T, F, O>(f, t, h, y, k, yn, err);
     const double norm = error_norm<D, O>(err, y, yn, atol, rtol);
     double dtn = h;
-    const bool accept = adapt(P.ctrl, norm, n1, n2, dtn);
+    const bool accept = adapt(P.ctrl, norm, n1, n2, dtn, PT);
     nsteps = j + 1;
     if (P.trace_cap > 0 && j < P.trace_cap) {
       const int64_t o = idx * P.trace_cap + j;
@@ -224,8 +224,14 @@ struct Lane {
 template <int M, class F, class O>
 __global__ void __launch_bounds__(128, 4) bode_persistent_kernel(const SolveParams P) {
   extern __shared__ uint32_t s_refresh[];
+  __shared__ PowTables s_pow;  // pow tables: divergent lookups, so shared not constant
   const int lane = threadIdx.x & 31;
   for (int w = threadIdx.x; w < P.smem_words; w += blockDim.x) s_refresh[w] = 0u;
+  {
+    const double* src = &g_pow_tables.log_tab[0][0];
+    double* dst = &s_pow.log_tab[0][0];
+    for (int w = threadIdx.x; w < (int)(sizeof(PowTables) / 8); w += blockDim.x) dst[w] = src[w];
+  }
   __syncthreads();
 
   Lane<M, F, O> L;
@@ -259,7 +265,7 @@ __global__ void __launch_bounds__(128, 4) bode_persistent_kernel(const SolvePara
     }
     if (have) {
       const int64_t j = L.nsteps;
-      if (L.step(P)) {
+      if (L.step(P, s_pow)) {
         const uint64_t bit = (uint64_t)j + 1;
         const uint32_t w = (uint32_t)(bit >> 5), msk = 1u << (bit & 31);
         if (P.smem_words > 0) {
