@@ -176,7 +176,7 @@ typedef struct bode_solve_args {
   int32_t blocks;
   /* optional per-instance cost estimate (n,): when set and `order` is NULL
    * the library queues instances longest-first (LPT) with an on-device
-   * bucketed counting sort (1/16-octave buckets).  Scheduling only: results
+   * bucketed counting sort (1/8-octave buckets).  Scheduling only: results
    * are identical for any order (batch independence). */
   const double* cost_hint;
   /* bode_solve_host only: split the batch into this many chunks and overlap

@@ -10,7 +10,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "_build", "libbode.so")
+LIB_PATH = os.environ.get("BODE_LIB") or os.path.join(HERE, "_build", "libbode.so")
 
 ABI_VERSION = 1
 OK, EINVAL, ECUDA, EUNSUPPORTED = 0, 1, 2, 3

@@ -222,7 +222,9 @@ struct Lane {
 };
 
 template <int M, class F, class O>
-__global__ void __launch_bounds__(128, 4) bode_persistent_kernel(const SolveParams P) {
+// 2-D systems fit 5 blocks of 128 threads per SM (<= 102 registers); wider
+// ones keep 4 (<= 128 registers) to avoid spilling the stage vectors.
+__global__ void __launch_bounds__(128, (F::D <= 2 ? 5 : 4)) bode_persistent_kernel(const SolveParams P) {
   extern __shared__ uint32_t s_refresh[];
   __shared__ PowTables s_pow;  // pow tables: divergent lookups, so shared not constant
   const int lane = threadIdx.x & 31;
