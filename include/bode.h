@@ -184,6 +184,14 @@ typedef struct bode_solve_args {
    * (0 or 1 = no pipelining).  n_f_evals stays batch-global. */
   int32_t pipeline_chunks;
   int32_t _pad2;
+  /* optional outputs for combining n_f_evals across shards (multi-GPU):
+   * the largest n_steps of this solve and a byte per loop iteration j in
+   * [0, max_steps + 2) that is 1 iff some instance rejected at iteration
+   * j-1 and was still running at j (an FSAL refresh evaluation,
+   * solver.py:220-226).  The global count is 1 + (S-1) * max_j + #{j >= 1 :
+   * OR over shards of map[j]} (FSAL), 1 + S * max_j otherwise. */
+  int64_t* max_iterations_out;
+  uint8_t* refresh_map_out;
 } bode_solve_args;
 
 int bode_abi_version(void);

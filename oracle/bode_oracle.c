@@ -525,6 +525,13 @@ int oracle_solve(const bode_solve_args* A, int nthreads) {
   if (A->n_f_evals)
     A->n_f_evals[0] = T.fsal ? 1 + (int64_t)(T.S - 1) * max_n + refreshes
                              : 1 + (int64_t)T.S * max_n;
+  if (A->max_iterations_out) A->max_iterations_out[0] = max_n;
+  if (A->refresh_map_out)
+    for (int64_t j = 0; j < A->max_steps + 2; j++) {
+      uint8_t any = 0;
+      for (int w = 0; w < nthreads; w++) any |= jobs[w].refresh[j];
+      A->refresh_map_out[j] = any;
+    }
   for (int w = 0; w < nthreads; w++) free(jobs[w].refresh);
   free(jobs);
   free(th);

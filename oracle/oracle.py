@@ -62,7 +62,8 @@ class Args(C.Structure):
                 ("workspace", C.c_void_p), ("workspace_bytes", C.c_size_t),
                 ("stream", C.c_void_p), ("threads_per_block", C.c_int32),
                 ("blocks", C.c_int32), ("cost_hint", C.c_void_p),
-                ("pipeline_chunks", C.c_int32), ("_pad2", C.c_int32)]
+                ("pipeline_chunks", C.c_int32), ("_pad2", C.c_int32),
+                ("max_iterations_out", C.c_void_p), ("refresh_map_out", C.c_void_p)]
 
 
 _lib = None
@@ -129,7 +130,7 @@ def make_dyn(name, inst=None, shared=(), mlp=None, keep=None):
 
 def solve(y0, t_start, t_end, t_eval, dyn, method="dopri5", atol=1e-6, rtol=1e-6,
           ctrl=None, max_steps=10_000, dt0=None, trace=False, nthreads=None,
-          with_ys=True):
+          with_ys=True, with_refresh=False):
     """Solve on the CPU oracle.  ``t_eval`` is a list of arrays (ragged) or a
     single 1-D array shared by all instances.  Returns a dict shaped like
     the golden fixtures."""
@@ -197,6 +198,11 @@ def solve(y0, t_start, t_end, t_eval, dyn, method="dopri5", atol=1e-6, rtol=1e-6
         a.trace_t, a.trace_dt, a.trace_accept = (_p(out["trace_t"]), _p(out["trace_dt"]),
                                                  _p(out["trace_accept"]))
     a.trace_cap = cap
+    if with_refresh:
+        out["max_iterations"] = np.zeros(1, np.int64)
+        out["refresh_map"] = np.zeros(max_steps + 2, np.uint8)
+        a.max_iterations_out = _p(out["max_iterations"])
+        a.refresh_map_out = _p(out["refresh_map"])
     nthreads = nthreads or min(os.cpu_count() or 1, 64)
     lib().oracle_solve(C.byref(a), int(nthreads))
     if with_ys:

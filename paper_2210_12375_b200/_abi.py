@@ -57,7 +57,8 @@ class SolveArgs(C.Structure):
                 ("workspace", C.c_void_p), ("workspace_bytes", C.c_size_t),
                 ("stream", C.c_void_p), ("threads_per_block", C.c_int32),
                 ("blocks", C.c_int32), ("cost_hint", C.c_void_p),
-                ("pipeline_chunks", C.c_int32), ("_pad2", C.c_int32)]
+                ("pipeline_chunks", C.c_int32), ("_pad2", C.c_int32),
+                ("max_iterations_out", C.c_void_p), ("refresh_map_out", C.c_void_p)]
 
 
 # every symbol include/bode.h declares, with its ctypes signature

@@ -198,7 +198,9 @@ int finalize(const bode_solve_args* a, cudaStream_t st) {
   char* ws = (char*)a->workspace;
   bode_finalize_kernel<<<1, 256, 0, st>>>((unsigned long long*)(ws + 8),
                                           (uint32_t*)(ws + Workspace::kHeader),
-                                          stages_of(a->method), fsal_of(a->method), a->n_f_evals);
+                                          stages_of(a->method), fsal_of(a->method), a->n_f_evals,
+                                          a->max_iterations_out, a->refresh_map_out,
+                                          a->max_steps + 2);
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? BODE_OK : cuda_fail(e, "finalize launch");
 }
@@ -313,6 +315,8 @@ int bode_solve_host(const bode_solve_args* h) {
   out((void**)&a.trace_t, 8 * h->trace_cap, 8 * n * h->trace_cap);
   out((void**)&a.trace_dt, 8 * h->trace_cap, 8 * n * h->trace_cap);
   out((void**)&a.trace_accept, h->trace_cap, n * h->trace_cap);
+  out((void**)&a.max_iterations_out, 0, 8);
+  out((void**)&a.refresh_map_out, 0, (size_t)h->max_steps + 2);
   const size_t nfe_off = place(8);
   const Layout L = layout(h, cmax);
   const size_t ws_off = place(L.total);
@@ -376,11 +380,15 @@ int bode_solve_host(const bode_solve_args* h) {
       if (x.row_bytes) {
         o = (size_t)lo * x.row_bytes;
         b = (size_t)(hi - lo) * x.row_bytes;
-      } else {  // ys: rows [row_lo, row_hi) of this chunk
+      } else if (x.out_field == (void**)&a.ys) {  // ys: rows [row_lo, row_hi) of this chunk
         const int64_t r0 = csr ? h->t_eval_offsets[lo] : lo * h->t_eval_len;
         const int64_t r1 = csr ? h->t_eval_offsets[hi] : hi * h->t_eval_len;
         o = (size_t)r0 * 8 * d;
         b = (size_t)(r1 - r0) * 8 * d;
+      } else {  // whole small outputs (written by the finaliser) travel last
+        if (k != chunks - 1) continue;
+        o = 0;
+        b = x.bytes;
       }
       if (!b) continue;
       cudaError_t r = cudaMemcpyAsync((char*)x.hdst + o, dev + x.off + o, b,

@@ -306,7 +306,8 @@ __global__ void __launch_bounds__(128) bode_init_kernel(const SolveParams P) {
 // n_f_evals = 1 + (S-1)*max_n + #refresh iterations in [1, max_n)  (FSAL)
 //           = 1 + S*max_n                                        (non-FSAL)
 __global__ void bode_finalize_kernel(const unsigned long long* max_n, const uint32_t* refresh,
-                                     int stages, int fsal, int64_t* n_f_evals);
+                                     int stages, int fsal, int64_t* n_f_evals,
+                                     int64_t* max_out, uint8_t* map_out, int64_t map_len);
 
 template <int M, class F, class O>
 cudaError_t launch_persistent(const SolveParams& P, int threads, int blocks, cudaStream_t st) {

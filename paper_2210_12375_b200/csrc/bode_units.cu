@@ -8,7 +8,15 @@
 namespace bode {
 
 __global__ void bode_finalize_kernel(const unsigned long long* max_n, const uint32_t* refresh,
-                                     int stages, int fsal, int64_t* n_f_evals) {
+                                     int stages, int fsal, int64_t* n_f_evals,
+                                     int64_t* max_out, uint8_t* map_out, int64_t map_len) {
+  if (map_out) {
+    for (int64_t j = threadIdx.x; j < map_len; j += blockDim.x)
+      map_out[j] = (uint8_t)((refresh[j >> 5] >> (j & 31)) & 1u);
+    if (threadIdx.x == 0 && max_out) *max_out = (int64_t)*max_n;
+  } else if (threadIdx.x == 0 && max_out) {
+    *max_out = (int64_t)*max_n;
+  }
   __shared__ unsigned long long s_cnt;
   if (threadIdx.x == 0) s_cnt = 0;
   __syncthreads();

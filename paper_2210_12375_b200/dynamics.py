@@ -94,6 +94,12 @@ class DeviceDynamics:
             mask |= 1 << k
         return shared, mask, cols
 
+    def subset(self, idx) -> "DeviceDynamics":
+        """The same functor restricted to instances ``idx`` (per-instance
+        parameters are sliced, shared ones kept) -- a shard of the batch."""
+        params = {k: (v if np.ndim(v) == 0 else v[idx]) for k, v in self.params.items()}
+        return DeviceDynamics(self.kind, params, self.mlp)
+
     def __call__(self, t, y):
         raise TypeError(f"{self.kind} is a device functor evaluated inside the B200 solver; "
                         "it has no CPU evaluation path")

@@ -209,7 +209,7 @@ def _tol_arrays(tol: Tolerances, n: int):
 def solve(problem: IvpBatch, f, tableau=None, tol: Tolerances | None = None,
           controller: PidCoefficients | None = None, max_steps: int = DEFAULT_MAX_STEPS,
           dt0=None, record_trace: bool = False, *, mode: str = "exact", order=None,
-          cost_hint=None, pipeline_chunks: int = 4) -> Solution:
+          cost_hint=None, pipeline_chunks: int = 4, with_refresh_map: bool = False) -> Solution:
     """Integrate every instance independently with adaptive steps on the GPU
     (reference ``solve``, solver.py:352-369), host arrays in and out."""
     if max_steps < 1:
@@ -282,8 +282,15 @@ def solve(problem: IvpBatch, f, tableau=None, tol: Tolerances | None = None,
         tt, tdt, tacc = np.zeros((n, cap)), np.zeros((n, cap)), np.zeros((n, cap), np.uint8)
         a.trace_t, a.trace_dt, a.trace_accept, a.trace_cap = (tt.ctypes.data, tdt.ctypes.data,
                                                               tacc.ctypes.data, cap)
+    if with_refresh_map:  # for combining n_f_evals across shards (distributed.py)
+        max_it = np.zeros(1, np.int64)
+        rmap = np.zeros(int(max_steps) + 2, np.uint8)
+        a.max_iterations_out, a.refresh_map_out = max_it.ctypes.data, rmap.ctypes.data
     _abi.check(lib.bode_solve_host(_abi.C.byref(a)))
     extra = {}
+    if with_refresh_map:
+        extra["max_iterations"] = int(max_it[0])
+        extra["refresh_map"] = rmap
     if record_trace:
         extra["trace_t"] = [tt[i, :n_steps[i]].copy() for i in range(n)]
         extra["trace_dt"] = [tdt[i, :n_steps[i]].copy() for i in range(n)]

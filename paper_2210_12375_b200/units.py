@@ -32,7 +32,7 @@ def _torch():
 
 def _dev(x, dtype=None):
     torch = _torch()
-    a = np.ascontiguousarray(np.asarray(x, dtype=dtype or np.float64))
+    a = np.array(x, dtype=dtype or np.float64, order="C", copy=True)
     return torch.from_numpy(a).to("cuda")
 
 
