@@ -255,3 +255,41 @@ def test_pipelined_host_path_matches_single_chunk():
         for k in ("n_steps", "n_accepted", "n_f_evals", "final_dt"):
             assert np.array_equal(getattr(a.stats, k), getattr(b.stats, k)), k
         assert np.array_equal(a.status, b.status) and np.array_equal(a.n_emitted, b.n_emitted)
+
+
+def test_mlp_neural_ode_vs_reference_fp32():
+    """C4 (neural ODE, D=64, H=256, tanh): the reference solve with a NumPy
+    fp32 MLP (tests/golden/mlp.npz).  fp32 GEMM summation order differs from
+    OpenBLAS, so step counts are compared in aggregate (2%, north_star) and
+    y(T) at 1e-4 of each instance's scale; statuses must match."""
+    z = np.load(os.path.join(os.path.dirname(__file__), "golden", "mlp.npz"))
+    n = z["y0"].shape[0]
+    prob = bode.IvpBatch(z["y0"], np.zeros(n), np.full(n, 10.0), np.full((n, 1), 10.0))
+    sol = bode.solve(prob, bode.mlp_dynamics(z["W1"], z["b1"], z["W2"], z["b2"]),
+                     max_steps=100_000)
+    assert np.array_equal(sol.status, z["status"])
+    ratio = sol.stats.n_steps.sum() / z["n_steps"].sum()
+    assert abs(ratio - 1.0) < 0.02, ratio
+    ys = sol.ys_flat.reshape(n, -1)
+    rel = np.max(np.abs(ys - z["ys"]), axis=1) / np.max(np.abs(z["ys"]), axis=1)
+    assert np.max(rel) < 1e-4, np.max(rel)
+    # batch-global n_f_evals follows the FSAL formula over the lockstep loop
+    assert sol.stats.n_f_evals[0] >= 1 + 6 * sol.stats.n_steps.max()
+
+
+def test_mlp_matches_oracle_at_scale():
+    z = np.load(os.path.join(os.path.dirname(__file__), "golden", "mlp.npz"))
+    rng = np.random.default_rng(3)
+    n = 2048
+    y0 = rng.normal(size=(n, 64))
+    mlp = (z["W1"], z["b1"], z["W2"], z["b2"])
+    te = np.array([2.5, 5.0, 10.0])
+    sol = bode.solve(bode.IvpBatch(y0, np.zeros(n), np.full(n, 10.0), te),
+                     bode.mlp_dynamics(*mlp), tol=bode.Tolerances(1e-6, 1e-6), max_steps=100_000)
+    ref = O.solve(y0, 0.0, 10.0, te, dict(name="mlp", inst=None, shared=(), mlp=mlp),
+                  atol=1e-6, rtol=1e-6, max_steps=100_000, nthreads=NT)
+    assert np.array_equal(sol.status, ref["status"])
+    assert abs(sol.stats.n_steps.sum() / ref["n_steps"].sum() - 1.0) < 0.02
+    assert np.mean(sol.stats.n_steps == ref["n_steps"]) > 0.9
+    a, b = sol.ys_flat.reshape(n, -1), ref["ys"].reshape(n, -1)
+    assert np.max(np.abs(a - b).max(axis=1) / np.abs(b).max(axis=1)) < 1e-4
