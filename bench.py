@@ -30,7 +30,7 @@ ICTRL = dict(betas=(1.0, 0.0, 0.0), safety=0.9, factor_min=0.2, factor_max=10.0,
 
 # algorithmic flops: per attempted step 82d+20+6*F_f (FSAL,
 # s=7), per emitted point 15d+51; pow counted separately (2 per step with PI42)
-F_F = {"vdp": 5, "lorenz": 8}
+F_F = {"vdp": 5, "lorenz": 8, "mlp": 4 * 64 * 256 + 64 + 256}  # MLP: 2 GEMMs + biases
 
 
 def flops_per_step(dyn, d):
@@ -69,6 +69,19 @@ def make_config(name, rank, n_override=None):
                     y0=np.tile([2.0, 0.0], (n, 1)), t_start=np.zeros(n), t_end=np.full(n, 10.0),
                     mu=mu, method="dopri5", ctrl=PI42, tol=1e-6, max_steps=100_000,
                     cost=mu)
+    if name == "c4":  # neural ODE: SURVEY.md §8(d) C4 weights/inputs
+        n = n_override or 65536
+        rng = np.random.default_rng(0)
+        D, H = 64, 256
+        W1 = (rng.normal(size=(H, D)) / np.sqrt(D)).astype(np.float32)
+        b1 = (0.1 * rng.normal(size=H)).astype(np.float32)
+        W2 = (rng.normal(size=(D, H)) / np.sqrt(H)).astype(np.float32)
+        b2 = (0.1 * rng.normal(size=D)).astype(np.float32)
+        y0 = np.random.default_rng(1 + rank).normal(size=(n, D))
+        return dict(workload="mlp64x256_tanh_64K_dopri5_fp32mlp_fp64state", dyn="mlp", n=n, d=D,
+                    y0=y0, t_start=np.zeros(n), t_end=np.full(n, 10.0),
+                    te2d=np.full((n, 1), 10.0), mu=None, mlp=(W1, b1, W2, b2),
+                    method="dopri5", ctrl=ICTRL, tol=1e-6, max_steps=100_000, cost=None)
     if name == "c3":
         n = n_override or 2 ** 18
         rng = np.random.default_rng(0 if rank == 0 else 1000 + rank)
@@ -101,6 +114,7 @@ def cpu_run(cfg, sample, nthreads):
     else:
         te = cfg.get("te1d")
     dyn = (dict(name="vdp", inst=cfg["mu"][:k, None]) if cfg["dyn"] == "vdp"
+           else dict(name="mlp", inst=None, shared=(), mlp=cfg["mlp"]) if cfg["dyn"] == "mlp"
            else dict(name="lorenz", inst=None, shared=(10.0, 28.0, 8.0 / 3.0)))
     t0 = time.perf_counter()
     r = O.solve(cfg["y0"][:k], cfg["t_start"][:k], cfg["t_end"][:k], te, dyn,
@@ -111,7 +125,7 @@ def cpu_run(cfg, sample, nthreads):
 
 
 def cpu_sample_size(cfg):
-    return {"c2": 262_144, "c5": 16_384, "c3": 4_096, "c1": 256}[cfg["_name"]]
+    return {"c2": 262_144, "c5": 16_384, "c3": 4_096, "c1": 256, "c4": 1024}[cfg["_name"]]
 
 
 def run_reference(args, rank, world):
@@ -229,7 +243,8 @@ def run_bode(args, rank, world, local_rank):
     ts = torch.tensor(cfg["t_start"], **f64)
     tn = torch.tensor(cfg["t_end"], **f64)
     dyn = (bode.vdp_dynamics(bode.VdpParams(torch.tensor(cfg["mu"], **f64)))
-           if cfg["dyn"] == "vdp" else bode.lorenz_dynamics())
+           if cfg["dyn"] == "vdp" else bode.mlp_dynamics(*cfg["mlp"]) if cfg["dyn"] == "mlp"
+           else bode.lorenz_dynamics())
     ctrl = bode.PidCoefficients(*cfg["ctrl"]["betas"])
     te_kw = {}
     if "te2d" in cfg:
@@ -300,6 +315,7 @@ def run_bode(args, rank, world, local_rank):
         prob = bode.IvpBatch(cfg["y0"], cfg["t_start"], cfg["t_end"],
                              cfg.get("te2d", cfg.get("te1d", [np.empty(0)] * n)))
         dyn_h = (bode.vdp_dynamics(bode.VdpParams(cfg["mu"])) if cfg["dyn"] == "vdp"
+                 else bode.mlp_dynamics(*cfg["mlp"]) if cfg["dyn"] == "mlp"
                  else bode.lorenz_dynamics())
         tab = {"dopri5": bode.dopri5, "tsit5": bode.tsit5}[cfg["method"]]()
         kw = dict(tableau=tab, tol=bode.Tolerances(cfg["tol"], cfg["tol"]), controller=ctrl,
@@ -326,6 +342,7 @@ def run_bode(args, rank, world, local_rank):
         h2d = (prob.y0.nbytes + prob.t_start.nbytes + prob.t_end.nbytes + prob.te_values.nbytes
                + (0 if prob.te_shared else prob.te_offsets.nbytes)
                + (cfg["mu"].nbytes if cfg["mu"] is not None else 0)
+               + (sum(w.nbytes for w in cfg["mlp"]) if cfg.get("mlp") else 0)
                + (8 * n if args.lpt and cfg["cost"] is not None else 0))
         d2h = 8 * pts * d + n * (8 + 8 + 8 + 8 + 4) + 8
         e2e = dict(value=e2e_acc / tot, unit="instance-steps/s", h2d_bytes_per_step=int(h2d),
@@ -376,7 +393,7 @@ def main():
     p.add_argument("--steps", type=int, default=10)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="bode", choices=["bode", "reference"])
-    p.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c5"])
+    p.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4", "c5"])
     p.add_argument("--mode", default="exact", choices=["exact", "fast"])
     p.add_argument("--lpt", type=int, default=1, help="cost-sorted (LPT) instance queue")
     p.add_argument("--no-e2e", action="store_true")

@@ -63,7 +63,8 @@ class Args(C.Structure):
                 ("stream", C.c_void_p), ("threads_per_block", C.c_int32),
                 ("blocks", C.c_int32), ("cost_hint", C.c_void_p),
                 ("pipeline_chunks", C.c_int32), ("_pad2", C.c_int32),
-                ("max_iterations_out", C.c_void_p), ("refresh_map_out", C.c_void_p)]
+                ("max_iterations_out", C.c_void_p), ("refresh_map_out", C.c_void_p),
+                ("mlp_backend", C.c_int32), ("_pad3", C.c_int32)]
 
 
 _lib = None

@@ -39,6 +39,7 @@ struct MlpWs {
   uint8_t* trunc;  // (n)
   int32_t* act[2]; // compacted running lists
   int32_t* cnt;    // [0], [1]: list sizes; [2]: iteration
+  float* wprep;    // tcgen05 path: weights pre-split into TF32 hi/lo tiles
 };
 
 size_t align256(size_t b) { return (b + 255) & ~(size_t)255; }
@@ -67,6 +68,7 @@ size_t carve(const bode_solve_args* a, char* base, MlpWs* w) {
   W->act[0] = (int32_t*)take(4 * n);
   W->act[1] = (int32_t*)take(4 * n);
   W->cnt = (int32_t*)take(64);
+  W->wprep = (float*)take(mlp_tc_supported(a->d, a->dyn.hidden) ? mlp_tc_prep_bytes(a->dyn.hidden) : 0);
   return off;
 }
 
@@ -510,10 +512,35 @@ static cudaError_t mlp_solve_m(const bode_solve_args* a, const SolveParams& P, c
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const bool tc_ok = mlp_tc_supported(D, H);
+  if (a->mlp_backend == BODE_MLP_TCGEN05 && !tc_ok) return cudaErrorNotSupported;
+  const bool use_tc = tc_ok && a->mlp_backend != BODE_MLP_CUDA_CORE;
+  if (use_tc && (e = mlp_tc_prep(W1, W2, H, W.wprep, st)) != cudaSuccess) return e;
+  const int max_tiles = (int)((n + 127) / 128);
+  // f(Y) for the compacted fp32 rows in W.Y (init evaluations)
   auto eval = [&](float* out) {
+    if (use_tc) {
+      MlpTcArgs t{n, H, 0, W.y, W.k, W.h, W.act[0], W.cnt, W.Y, W.wprep, b1, b2, out};
+      mlp_tc_launch<M>(t, max_tiles, st);
+      return;
+    }
     // one persistent block per SM; blocks past the live tile count exit
     const unsigned g = grid_for(n, kTile, (unsigned)sms);
     mlp_eval_cc_kernel<<<g, 256, smem, st>>>(W.Y, W.act[0], W.cnt, W1, b1, W2, b2, D, H, out);
+  };
+  // stage s of the current attempt: input formed from y, h and k_0..k_{s-1}
+  auto stage = [&](int s) {
+    if (use_tc) {  // prologue fused into the tensor-core kernel
+      MlpTcArgs t{n, H, s, W.y, W.k, W.h, W.act[0], W.cnt, nullptr, W.wprep, b1, b2,
+                  W.k + (size_t)s * n * D};
+      mlp_tc_launch<M>(t, max_tiles, st);
+      return;
+    }
+    if (s == 0)
+      mlp_state_input_kernel<<<grid_for(n * D), 256, 0, st>>>(W, D);
+    else
+      mlp_stage_input_kernel<M><<<grid_for(n * D), 256, 0, st>>>(W, n, D, s);
+    eval(W.k + (size_t)s * n * D);
   };
   InitArgs I{a->y0, a->t_start, a->t_end, a->atol_v, a->rtol_v, a->atol, a->rtol,
              a->dt0_mode, a->dt0, a->dt0_v, T::ORDER};
@@ -541,14 +568,7 @@ static cudaError_t mlp_solve_m(const bode_solve_args* a, const SolveParams& P, c
   int burst = 4;
   while (true) {
     for (int b = 0; b < burst; b++) {
-      if (!T::FSAL) {
-        mlp_state_input_kernel<<<grid_for(n * D), 256, 0, st>>>(W, D);
-        eval(W.k);
-      }
-      for (int s = 1; s < T::S; s++) {
-        mlp_stage_input_kernel<M><<<grid_for(n * D), 256, 0, st>>>(W, n, D, s);
-        eval(W.k + (size_t)s * n * D);
-      }
+      for (int s = T::FSAL ? 1 : 0; s < T::S; s++) stage(s);
       mlp_control_kernel<M><<<(unsigned)((n + 3) / 4), 128, 0, st>>>(W, A, n, D);
       mlp_copy_list_kernel<<<grid_for(n), 256, 0, st>>>(W);
       mlp_swap_kernel<<<1, 32, 0, st>>>(W);

@@ -29,6 +29,8 @@ __all__ = ["DEFAULT_MAX_STEPS", "SolveStatus", "IvpBatch", "SolveStats", "Soluti
            "solve", "solve_device"]
 
 DEFAULT_MAX_STEPS = 10_000
+# MLP stage evaluation: tcgen05 3xTF32 (auto when d == 64) or CUDA-core fp32
+MLP_BACKENDS = {"auto": 0, "cuda_core": 1, "tcgen05": 2}
 
 
 class SolveStatus(enum.IntEnum):
@@ -209,7 +211,8 @@ def _tol_arrays(tol: Tolerances, n: int):
 def solve(problem: IvpBatch, f, tableau=None, tol: Tolerances | None = None,
           controller: PidCoefficients | None = None, max_steps: int = DEFAULT_MAX_STEPS,
           dt0=None, record_trace: bool = False, *, mode: str = "exact", order=None,
-          cost_hint=None, pipeline_chunks: int = 4, with_refresh_map: bool = False) -> Solution:
+          cost_hint=None, pipeline_chunks: int = 4, with_refresh_map: bool = False,
+          mlp_backend: str = "auto") -> Solution:
     """Integrate every instance independently with adaptive steps on the GPU
     (reference ``solve``, solver.py:352-369), host arrays in and out."""
     if max_steps < 1:
@@ -267,6 +270,7 @@ def solve(problem: IvpBatch, f, tableau=None, tol: Tolerances | None = None,
         keep.append(ch)
         a.cost_hint = ch.ctypes.data
     a.pipeline_chunks = int(pipeline_chunks) if n >= 65536 else 1
+    a.mlp_backend = MLP_BACKENDS[mlp_backend]
     ys = np.empty((max(n_rows, 1), d))
     n_emitted = np.empty(n, np.int64)
     n_steps = np.empty(n, np.int64)
@@ -308,7 +312,7 @@ def solve_device(y0, t_start, t_end, f, *, t_eval=None, t_eval_offsets=None, met
                  atol=1e-6, rtol=1e-6, controller: PidCoefficients | None = None,
                  max_steps: int = DEFAULT_MAX_STEPS, dt0=None, order=None, cost_hint=None,
                  mode: str = "exact", record_trace: bool = False, stream=None,
-                 threads_per_block: int = 0, blocks: int = 0):
+                 threads_per_block: int = 0, blocks: int = 0, mlp_backend: str = "auto"):
     """Device-resident solve on torch CUDA tensors; asynchronous (no host
     sync).  ``t_eval``: None, a 1-D tensor shared by all instances, a 2-D
     (n, m) tensor, or CSR values with ``t_eval_offsets`` (n+1).  ``atol`` /
@@ -404,6 +408,7 @@ def solve_device(y0, t_start, t_end, f, *, t_eval=None, t_eval_offsets=None, met
         a.trace_t, a.trace_dt = out["trace_t"].data_ptr(), out["trace_dt"].data_ptr()
         a.trace_accept, a.trace_cap = out["trace_accept"].data_ptr(), cap
     a.threads_per_block, a.blocks = int(threads_per_block), int(blocks)
+    a.mlp_backend = MLP_BACKENDS[mlp_backend]
     wsb = lib.bode_workspace_size(_abi.C.byref(a))
     if wsb == 0:
         _abi.check(_abi.EINVAL)

@@ -257,16 +257,18 @@ def test_pipelined_host_path_matches_single_chunk():
         assert np.array_equal(a.status, b.status) and np.array_equal(a.n_emitted, b.n_emitted)
 
 
-def test_mlp_neural_ode_vs_reference_fp32():
+@pytest.mark.parametrize("backend", ["tcgen05", "cuda_core"])
+def test_mlp_neural_ode_vs_reference_fp32(backend):
     """C4 (neural ODE, D=64, H=256, tanh): the reference solve with a NumPy
     fp32 MLP (tests/golden/mlp.npz).  fp32 GEMM summation order differs from
-    OpenBLAS, so step counts are compared in aggregate (2%, north_star) and
-    y(T) at 1e-4 of each instance's scale; statuses must match."""
+    OpenBLAS (and 3xTF32 from fp32), so step counts are compared in
+    aggregate (2%, north_star) and y(T) at 1e-4 of each instance's scale;
+    statuses must match."""
     z = np.load(os.path.join(os.path.dirname(__file__), "golden", "mlp.npz"))
     n = z["y0"].shape[0]
     prob = bode.IvpBatch(z["y0"], np.zeros(n), np.full(n, 10.0), np.full((n, 1), 10.0))
     sol = bode.solve(prob, bode.mlp_dynamics(z["W1"], z["b1"], z["W2"], z["b2"]),
-                     max_steps=100_000)
+                     max_steps=100_000, mlp_backend=backend)
     assert np.array_equal(sol.status, z["status"])
     ratio = sol.stats.n_steps.sum() / z["n_steps"].sum()
     assert abs(ratio - 1.0) < 0.02, ratio
@@ -277,7 +279,8 @@ def test_mlp_neural_ode_vs_reference_fp32():
     assert sol.stats.n_f_evals[0] >= 1 + 6 * sol.stats.n_steps.max()
 
 
-def test_mlp_matches_oracle_at_scale():
+@pytest.mark.parametrize("backend", ["tcgen05", "cuda_core"])
+def test_mlp_matches_oracle_at_scale(backend):
     z = np.load(os.path.join(os.path.dirname(__file__), "golden", "mlp.npz"))
     rng = np.random.default_rng(3)
     n = 2048
@@ -285,7 +288,8 @@ def test_mlp_matches_oracle_at_scale():
     mlp = (z["W1"], z["b1"], z["W2"], z["b2"])
     te = np.array([2.5, 5.0, 10.0])
     sol = bode.solve(bode.IvpBatch(y0, np.zeros(n), np.full(n, 10.0), te),
-                     bode.mlp_dynamics(*mlp), tol=bode.Tolerances(1e-6, 1e-6), max_steps=100_000)
+                     bode.mlp_dynamics(*mlp), tol=bode.Tolerances(1e-6, 1e-6), max_steps=100_000,
+                     mlp_backend=backend)
     ref = O.solve(y0, 0.0, 10.0, te, dict(name="mlp", inst=None, shared=(), mlp=mlp),
                   atol=1e-6, rtol=1e-6, max_steps=100_000, nthreads=NT)
     assert np.array_equal(sol.status, ref["status"])
