@@ -192,36 +192,49 @@ __global__ void __launch_bounds__(128, 1) mlp_tc_kernel(MlpTcArgs A) {
   const uint32_t w2h = smem_u32(S.w2[0]), w2l = smem_u32(S.w2[1]);
 
   for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    // ---- prologue: stage input rows -> TF32 hi/lo operand tiles
+    // ---- prologue: stage input rows -> TF32 hi/lo operand tiles.  A warp
+    // fills whole 8x4 core matrices (128 contiguous bytes: conflict-free
+    // stores); its lanes read 8 rows x 4 consecutive columns per core
+    // matrix, 16 consecutive core matrices covering the same 8 rows.
     const int p = tile * kRows + tid;
     const bool live = p < cnt;
     const int64_t i = live ? (A.act ? A.act[p] : p) : 0;
     {
       float* ah = reinterpret_cast<float*>(S.a_hi);
       float* al = reinterpret_cast<float*>(S.a_lo);
-      for (int k = 0; k < kD; k++) {
-        float x = 0.0f;
-        if (live) {
-          if (A.Yin) {
-            x = A.Yin[(size_t)p * kD + k];
-          } else if (A.stage == 0) {
-            x = (float)A.y[i * kD + k];
-          } else {
-            double s = 0.0;
+      const int lane = tid & 31;
+      for (int g = warp; g < kRows / 8; g += 4) {   // 8-row group
+        const int r = g * 8 + (lane >> 2);
+        const int pr = tile * kRows + r;
+        const bool lv = pr < cnt;
+        const int64_t ir = lv ? (A.act ? A.act[pr] : pr) : 0;
+        const double hr = (lv && !A.Yin && A.stage > 0) ? A.h[ir] : 0.0;
+#pragma unroll 4
+        for (int q = 0; q < kD / 4; q++) {            // 4-column chunk
+          const int k = q * 4 + (lane & 3);
+          float x = 0.0f;
+          if (lv) {
+            if (A.Yin) {
+              x = A.Yin[(size_t)pr * kD + k];
+            } else if (A.stage == 0) {
+              x = (float)__ldg(A.y + ir * kD + k);
+            } else {
+              double s = 0.0;
 #pragma unroll
-            for (int j = 0; j < T::S; j++) {
-              if (j >= A.stage) break;
-              const double kj = (double)A.k[((int64_t)j * A.n + i) * kD + k];
-              s = j == 0 ? ExactOps::mul(T::a(A.stage, 0), kj)
-                         : ExactOps::mad(T::a(A.stage, j), kj, s);
+              for (int j = 0; j < T::S; j++) {
+                if (j >= A.stage) break;
+                const double kj = (double)__ldg(A.k + ((int64_t)j * A.n + ir) * kD + k);
+                s = j == 0 ? ExactOps::mul(T::a(A.stage, 0), kj)
+                           : ExactOps::mad(T::a(A.stage, j), kj, s);
+              }
+              x = (float)ExactOps::mad(hr, s, __ldg(A.y + ir * kD + k));
             }
-            x = (float)ExactOps::mad(A.h[i], s, A.y[i * kD + k]);
           }
+          const float hi = tf32_hi(x);
+          const int o = (g * 16 + q) * 32 + lane;  // core matrix (g, q), element lane
+          ah[o] = hi;
+          al[o] = x - hi;
         }
-        const float hi = tf32_hi(x);
-        const uint32_t o = cm_off(tid, k) >> 2;
-        ah[o] = hi;
-        al[o] = x - hi;
       }
     }
     fence_async_smem();
