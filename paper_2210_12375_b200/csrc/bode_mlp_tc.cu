@@ -169,39 +169,56 @@ template <int M>
 __device__ __forceinline__ void produce_tile(const MlpTcArgs& A, int tile, int cnt, uint8_t* ahi,
                                              uint8_t* alo, int pwarp, int lane) {
   using T = Tab<M>;
-  float* ah = reinterpret_cast<float*>(ahi);
-  float* al = reinterpret_cast<float*>(alo);
-  for (int g = pwarp; g < kRows / 8; g += 4) {  // 8-row group
-    const int r = g * 8 + (lane >> 2);
+  // lane -> (row r of an 8-row group, 4-column chunk q): every load is a
+  // 16/32-byte vector, all of a lane's loads are issued before the fp64
+  // combination, and the 16-byte result rows land in core matrix (g, q)
+  const int stage = A.Yin ? -1 : A.stage;
+  for (int it = pwarp; it < kRows / 8 * 4; it += 4) {  // 16 row groups x 4 column quarters
+    const int g = it >> 2, r = g * 8 + (lane & 7);
+    const int q = (it & 3) * 4 + (lane >> 3);           // 4-column chunk 0..15
     const int pr = tile * kRows + r;
     const bool lv = pr < cnt;
     const int64_t ir = lv ? (A.act ? A.act[pr] : pr) : 0;
-    const double hr = (lv && !A.Yin && A.stage > 0) ? A.h[ir] : 0.0;
-#pragma unroll 4
-    for (int q = 0; q < kD / 4; q++) {  // 4-column chunk
-      const int k = q * 4 + (lane & 3);
-      float x = 0.0f;
-      if (lv) {
-        if (A.Yin) {
-          x = A.Yin[(size_t)pr * kD + k];
-        } else if (A.stage == 0) {
-          x = (float)__ldg(A.y + ir * kD + k);
-        } else {
-          double s = 0.0;
+    float x[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+    if (lv) {
+      if (stage < 0) {
+        const float4 v = *reinterpret_cast<const float4*>(A.Yin + (size_t)pr * kD + 4 * q);
+        x[0] = v.x, x[1] = v.y, x[2] = v.z, x[3] = v.w;
+      } else {
+        const double2* yp = reinterpret_cast<const double2*>(A.y + ir * kD + 4 * q);
+        const double2 y01 = __ldg(yp), y23 = __ldg(yp + 1);
+        const double yv[4] = {y01.x, y01.y, y23.x, y23.y};
+        if (stage == 0) {
 #pragma unroll
-          for (int j = 0; j < T::S; j++) {
-            if (j >= A.stage) break;
-            const double kj = (double)__ldg(A.k + ((int64_t)j * A.n + ir) * kD + k);
-            s = j == 0 ? ExactOps::mul(T::a(A.stage, 0), kj) : ExactOps::mad(T::a(A.stage, j), kj, s);
+          for (int e = 0; e < 4; e++) x[e] = (float)yv[e];
+        } else {
+          float4 kv[T::S];
+#pragma unroll
+          for (int j = 0; j < T::S; j++)
+            if (j < stage)
+              kv[j] = __ldg(reinterpret_cast<const float4*>(A.k + ((int64_t)j * A.n + ir) * kD + 4 * q));
+          const double hr = A.h[ir];
+#pragma unroll
+          for (int e = 0; e < 4; e++) {
+            double s = 0.0;
+#pragma unroll
+            for (int j = 0; j < T::S; j++) {
+              if (j >= stage) break;
+              const float kf = e == 0 ? kv[j].x : e == 1 ? kv[j].y : e == 2 ? kv[j].z : kv[j].w;
+              s = j == 0 ? ExactOps::mul(T::a(stage, 0), (double)kf)
+                         : ExactOps::mad(T::a(stage, j), (double)kf, s);
+            }
+            x[e] = (float)ExactOps::mad(hr, s, yv[e]);
           }
-          x = (float)ExactOps::mad(hr, s, __ldg(A.y + ir * kD + k));
         }
       }
-      const float hi = tf32_hi(x);
-      const int o = (g * 16 + q) * 32 + lane;  // core matrix (g, q): 128 contiguous bytes
-      ah[o] = hi;
-      al[o] = x - hi;
     }
+    float4 hi, lo;
+    hi.x = tf32_hi(x[0]), hi.y = tf32_hi(x[1]), hi.z = tf32_hi(x[2]), hi.w = tf32_hi(x[3]);
+    lo.x = x[0] - hi.x, lo.y = x[1] - hi.y, lo.z = x[2] - hi.z, lo.w = x[3] - hi.w;
+    const uint32_t o = (uint32_t)((g * 16 + q) * 128 + (r & 7) * 16);
+    *reinterpret_cast<float4*>(ahi + o) = hi;
+    *reinterpret_cast<float4*>(alo + o) = lo;
   }
 }
 
