@@ -333,6 +333,53 @@ __device__ __forceinline__ bool adapt(const CtrlParams& C, double norm, double& 
   return accept;
 }
 
+__device__ __forceinline__ bool np_special_exponent(double e) {
+  return e == 0.0 || e == 1.0 || e == -1.0 || e == 2.0 || e == 0.5;
+}
+
+// x**e given log(x) (when known): the same operations as np_scalar_pow
+// (special exponents, then cr_pow = cr_log + cr_exp_mul), so results are
+// bit-identical to the uncached path.
+__device__ __forceinline__ double pow_logged(double x, double e, bool ok, double lh, double ll,
+                                             const PowTables& T) {
+  if (np_special_exponent(e)) return np_scalar_pow(x, e, T);
+  return (ok && isfinite(e)) ? cr_exp_mul(e, lh, ll, x, T) : pow(x, e);
+}
+
+// adapt() for the persistent solver: the PID term n_prev^(-beta2/k) reuses
+// log(n_prev), computed one step earlier as log of that step's norm, so a
+// PI step costs one log + two exp instead of two full pows.  n1 >= 1e-10
+// always holds (initialised to 1, then max(norm, NORM_FLOOR)), hence
+// max(n1, NORM_FLOOR) == n1.  Bit-identical to adapt().
+struct LogCache {
+  double h, l;
+  bool ok;  // false: log unknown (x = 1 at start, or x = inf) -> libm path
+};
+
+__device__ __forceinline__ bool adapt_cached(const CtrlParams& C, double norm, double& n1,
+                                             double& n2, LogCache& L1, double& dt,
+                                             const PowTables& T) {
+  const bool accept = norm <= 1.0;
+  const double a = np_max(norm, 1e-10);
+  const double g = np_max(n2, 1e-10);
+  LogCache La;
+  La.ok = false;
+  if (!np_special_exponent(C.e1) || (C.e2 != 0.0 && !np_special_exponent(C.e2)))
+    La.ok = cr_log(a, T, La.h, La.l);
+  double factor = __dmul_rn(C.safety, pow_logged(a, C.e1, La.ok, La.h, La.l, T));
+  if (C.e2 != 0.0) factor = __dmul_rn(factor, pow_logged(n1, C.e2, L1.ok, L1.h, L1.l, T));
+  if (C.e3 != 0.0) factor = __dmul_rn(factor, np_scalar_pow(g, C.e3, T));
+  if (!isfinite(factor)) factor = C.fmin;
+  factor = np_min(np_max(factor, C.fmin), C.fmax);
+  dt = __dmul_rn(dt, factor);
+  if (C.hist || accept) {
+    n2 = n1;
+    n1 = a;
+    L1 = La;
+  }
+  return accept;
+}
+
 // initial_step, controller.py:145-197 (one instance).  Returns dt (NaN when
 // f0 is non-finite) and writes f0.
 template <class F, class O>

@@ -98,12 +98,11 @@ BODE_HD void two_sum(double a, double b, double& s, double& err) {
 
 }  // namespace powimpl
 
-// Correctly rounded (w.h.p.) x**e for x > 0 finite, e finite; everything
-// else -- and results near overflow/underflow -- goes to the libm pow.
-BODE_HD double cr_pow(double x, double e, const PowTables& T) {
+// log(x) as a double-double (lh + ll, error < 2^-68 absolute) for x > 0
+// finite; returns false (and leaves lh/ll unset) for anything else.
+BODE_HD bool cr_log(double x, const PowTables& T, double& lh, double& ll) {
   using namespace powimpl;
-  if (!(x > 0.0) || !(x < INFINITY) || !(e == e) || e == INFINITY || e == -INFINITY)
-    return pow(x, e);
+  if (!(x > 0.0) || !(x < INFINITY)) return false;
   int64_t ix = bits(x);
   int k = 0;
   if (ix < 0x0010000000000000LL) {  // subnormal: normalise
@@ -144,8 +143,14 @@ BODE_HD double cr_pow(double x, double e, const PowTables& T) {
   lo = sub(lo, mul(r, p_lo));
   lo = add(lo, mul(sq, p_lo));
   lo = add(lo, q);
-  double lh, ll;
   two_sum(s3, lo, lh, ll);
+  return true;
+}
+
+// exp(e * (lh + ll)), correctly rounded w.h.p.; `x` (= exp(lh + ll)) is only
+// used for the libm fallback near overflow/underflow.
+BODE_HD double cr_exp_mul(double e, double lh, double ll, double x, const PowTables& T) {
+  using namespace powimpl;
   // y = e * log(x) in double-double
   const double yh = mul(e, lh);
   const double yl = fma_(e, ll, fma_(e, lh, -yh));
@@ -184,6 +189,14 @@ BODE_HD double cr_pow(double x, double e, const PowTables& T) {
   const double res = add(S, tail);
   // scale by 2^ke (result stays normal: |y| < 700)
   return from_bits(bits(res) + (ke << 52));
+}
+
+// Correctly rounded (w.h.p.) x**e for x > 0 finite, e finite; everything
+// else -- and results near overflow/underflow -- goes to the libm pow.
+BODE_HD double cr_pow(double x, double e, const PowTables& T) {
+  double lh, ll;
+  if (!(e == e) || e == INFINITY || e == -INFINITY || !cr_log(x, T, lh, ll)) return pow(x, e);
+  return cr_exp_mul(e, lh, ll, x, T);
 }
 
 }  // namespace bode

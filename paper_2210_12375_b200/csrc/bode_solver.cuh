@@ -74,6 +74,7 @@ struct Lane {
   double y[D];
   double k[S][D];  // k[0] is the FSAL cache f0
   double t, dt, t_end, atol, rtol, n1, n2;
+  LogCache L1;  // log(n1) for the PID history term (adapt_cached)
   int64_t idx, nsteps, nacc, cursor, m;
   const double* te;
   double* ys;
@@ -154,6 +155,7 @@ struct Lane {
     dt = P.final_dt[i];
     cursor = P.n_emitted[i];
     status = BODE_RUNNING;
+    L1.ok = cr_log(1.0, g_pow_tables, L1.h, L1.l);
   }
 
   // one iteration of step_once for this row (solver.py:208-282); returns
@@ -168,7 +170,7 @@ struct Lane {
     rk_step<T, F, O>(f, t, h, y, k, yn, err);
     const double norm = error_norm<D, O>(err, y, yn, atol, rtol);
     double dtn = h;
-    const bool accept = adapt(P.ctrl, norm, n1, n2, dtn, PT);
+    const bool accept = adapt_cached(P.ctrl, norm, n1, n2, L1, dtn, PT);
     nsteps = j + 1;
     if (P.trace_cap > 0 && j < P.trace_cap) {
       const int64_t o = idx * P.trace_cap + j;
