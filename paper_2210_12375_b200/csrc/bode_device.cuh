@@ -117,21 +117,32 @@ static __constant__ double c_tab[3][98] = {BODE_DOPRI5_FLAT_INIT, BODE_TSIT5_FLA
                                            BODE_HEUN_FLAT_INIT};
 
 template <int M> struct TabShape;
+// za/zb/ze/zw: the same coefficients as compile-time constants, used only to
+// drop terms whose coefficient is exactly zero (they fold away when unrolled)
+#define BODE_TAB_ZEROS(name)                                                        \
+  static __device__ __forceinline__ constexpr double za(int i, int j) { return bode_##name##_a(i, j); } \
+  static __device__ __forceinline__ constexpr double zb(int i) { return bode_##name##_b(i); }           \
+  static __device__ __forceinline__ constexpr double ze(int i) { return bode_##name##_berr(i); }        \
+  static __device__ __forceinline__ constexpr double zw(int i, int j) { return bode_##name##_interp(i, j); }
 template <> struct TabShape<BODE_METHOD_DOPRI5> {
   static constexpr int S = BODE_DOPRI5_STAGES, ORDER = BODE_DOPRI5_ORDER,
                        ERR_ORDER = BODE_DOPRI5_ERROR_ORDER, NI = BODE_DOPRI5_NINTERP;
   static constexpr bool FSAL = BODE_DOPRI5_FSAL;
+  BODE_TAB_ZEROS(dopri5)
 };
 template <> struct TabShape<BODE_METHOD_TSIT5> {
   static constexpr int S = BODE_TSIT5_STAGES, ORDER = BODE_TSIT5_ORDER,
                        ERR_ORDER = BODE_TSIT5_ERROR_ORDER, NI = BODE_TSIT5_NINTERP;
   static constexpr bool FSAL = BODE_TSIT5_FSAL;
+  BODE_TAB_ZEROS(tsit5)
 };
 template <> struct TabShape<BODE_METHOD_HEUN> {
   static constexpr int S = BODE_HEUN_STAGES, ORDER = BODE_HEUN_ORDER,
                        ERR_ORDER = BODE_HEUN_ERROR_ORDER, NI = BODE_HEUN_NINTERP;
   static constexpr bool FSAL = BODE_HEUN_FSAL;
+  BODE_TAB_ZEROS(heun)
 };
+#undef BODE_TAB_ZEROS
 
 template <int M>
 struct Tab : TabShape<M> {
@@ -433,6 +444,13 @@ __device__ __forceinline__ double initial_step(const F& f, double t0, const doub
 template <class T, class F, class O>
 __device__ __forceinline__ void rk_step(const F& f, double t, double h, const double* y,
                                         double (*k)[F::D], double* y_next, double* err) {
+  // Terms with a zero coefficient (dopri5: a61, b1, b6, e1; tsit5: b6) add
+  // exactly +-0 in the reference, so they are skipped -- except that 0*inf
+  // and 0*NaN are NaN there: a non-finite skipped stage value is replayed by
+  // making y_next / err NaN, which is what the reference's sums produce.
+  // (The stage-6 input skips a61*k1; k1 non-finite already makes the a21
+  // term, hence every later stage and err, non-finite.)  The only
+  // representable difference left is the sign of an exactly-zero sum.
   constexpr int D = F::D, S = T::S;
   if constexpr (!T::FSAL) f(t, y, k[0]);
 #pragma unroll
@@ -442,7 +460,8 @@ __device__ __forceinline__ void rk_step(const F& f, double t, double h, const do
     for (int c = 0; c < D; c++) {
       double s = O::mul(T::a(i, 0), k[0][c]);
 #pragma unroll
-      for (int j = 1; j < i; j++) s = O::mad(T::a(i, j), k[j][c], s);
+      for (int j = 1; j < i; j++)
+        if (T::za(i, j) != 0.0) s = O::mad(T::a(i, j), k[j][c], s);
       ys[c] = O::mad(h, s, y[c]);
     }
     f(O::mad(T::c(i), h, t), ys, k[i]);
@@ -451,13 +470,19 @@ __device__ __forceinline__ void rk_step(const F& f, double t, double h, const do
   for (int c = 0; c < D; c++) {
     double s = O::mul(T::b(0), k[0][c]);
     double e = O::mul(T::e(0), k[0][c]);
+    bool skipped_nonfinite = false;
 #pragma unroll
     for (int i = 1; i < S; i++) {
-      s = O::mad(T::b(i), k[i][c], s);
-      e = O::mad(T::e(i), k[i][c], e);
+      if (T::zb(i) != 0.0) s = O::mad(T::b(i), k[i][c], s);
+      if (T::ze(i) != 0.0) e = O::mad(T::e(i), k[i][c], e);
+      if (T::zb(i) == 0.0 || T::ze(i) == 0.0) skipped_nonfinite |= !isfinite(k[i][c]);
     }
     y_next[c] = O::mad(h, s, y[c]);
     err[c] = O::mul(h, e);
+    if (skipped_nonfinite) {
+      y_next[c] = __longlong_as_double(0x7ff8000000000000LL);
+      err[c] = y_next[c];
+    }
   }
 }
 
@@ -478,7 +503,12 @@ __device__ __forceinline__ void interpolate(const double (*k)[D], const double* 
   for (int c = 0; c < D; c++) {
     double s = O::mul(w[0], k[0][c]);
 #pragma unroll
-    for (int i = 1; i < S; i++) s = O::mad(w[i], k[i][c], s);
+    for (int i = 1; i < S; i++) {
+      bool zero_row = true;  // dopri5 row 1: w_1(theta) == 0 (k_1 finite on accepted steps)
+#pragma unroll
+      for (int j = 0; j < M; j++) zero_row &= T::zw(i, j) == 0.0;
+      if (!zero_row) s = O::mad(w[i], k[i][c], s);
+    }
     out[c] = O::mad(h, s, y0[c]);
   }
 }
