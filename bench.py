@@ -204,6 +204,15 @@ class ClockSampler:
                     reasons=reasons, samples=len(rows))
 
 
+def measured_peak(key):
+    """Driver-measured roofline denominators (MEASURED_PEAKS.json); fallback
+    per /opt/skills/guides/B200_PROFILING.md when the file is absent."""
+    try:
+        return float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))[key])
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}[key]
+
+
 def fp64_peak(torch, lib, dev):
     """Measured DFMA throughput (bode_probe_fp64), TFLOP/s."""
     out = torch.zeros(1, dtype=torch.float64, device=dev)
@@ -255,17 +264,19 @@ def run_bode(args, rank, world, local_rank):
     flush = torch.empty(256 * 2 ** 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
     st = torch.cuda.current_stream(dev)
 
-    def one_step():
+    is_mlp = cfg["dyn"] == "mlp"
+
+    def one_step(prof=None):
         return bode.solve_device(y0, ts, tn, dyn, method=cfg["method"], atol=cfg["tol"],
                                  rtol=cfg["tol"], controller=ctrl, max_steps=cfg["max_steps"],
-                                 mode=args.mode, cost_hint=cost, **te_kw)
+                                 mode=args.mode, cost_hint=cost, prof_events=prof, **te_kw)
 
     for _ in range(args.warmup):
         out = one_step()
     torch.cuda.synchronize(dev)
     if dist:
         dist.barrier()
-    times, accepted, attempted = [], 0, 0
+    times, kern_times, accepted, attempted = [], [], 0, 0
     kern_ms = 0.0
     clock_path = os.path.join(tempfile.gettempdir(), f"bode_clocks_rank{rank}_{os.getpid()}.csv")
     with ClockSampler(clock_path) as clk:
@@ -273,13 +284,19 @@ def run_bode(args, rank, world, local_rank):
             flush.zero_()
             torch.cuda.synchronize(dev)
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            k0, k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            k0.record(st)  # materialise the cudaEvent_t handles (torch creates them lazily);
+            k1.record(st)  # bode_solve re-records both around the persistent launch
             e0.record(st)
-            out = one_step()
+            out = one_step(None if is_mlp else (k0, k1))
             e1.record(st)
             e1.synchronize()
             times.append(e0.elapsed_time(e1))
+            # the dominant kernel alone (persistent integrator), same stream
+            kern_times.append(times[-1] if is_mlp else k0.elapsed_time(k1))
             accepted += int(out["n_accepted"].sum())
             attempted += int(out["n_steps"].sum())
+            launches_per_step = out["launches"]  # kernels of ours in this solve
         time.sleep(0.25)
     torch.cuda.synchronize(dev)
     total_ms = float(np.sum(times))
@@ -293,21 +310,42 @@ def run_bode(args, rank, world, local_rank):
         accepted, attempted = int(aa[0].item()), int(aa[1].item())
     value = accepted / (total_ms / 1e3)
 
-    # ---- roofline: the persistent kernel alone (events on its stream)
-    peak_fp64 = fp64_peak(torch, lib, dev)
+    # ---- roofline of the dominant kernel, timed with events inside the timed
+    # steps above (bode_solve records them around the persistent launch)
     pts = n_points(cfg)
-    flops_launch = (flops_per_step(cfg["dyn"], d) * (attempted / args.steps / max(world, 1))
-                    + flops_per_point(d) * pts)
-    # one extra timed solve, split: the solve is memset + persistent + finalize
-    flush.zero_()
-    torch.cuda.synchronize(dev)
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(st)
-    one_step()
-    e1.record(st)
-    e1.synchronize()
-    kern_ms = e0.elapsed_time(e1)
-    achieved = flops_launch / (kern_ms / 1e3) / 1e12
+    kern_ms = float(np.mean(kern_times))
+    att_launch = attempted / args.steps / max(world, 1)
+    traffic = None
+    try:
+        tj = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))[args.config]
+        traffic = tj["dram_read_bytes"] + tj["dram_write_bytes"]
+    except Exception:
+        pass
+    if is_mlp:
+        # tensor-pipe bound: algorithmic MLP GEMM flops (4*D*H per f-eval: 6 FSAL
+        # stages per attempted step + 2 init evaluations per instance); peak =
+        # TF32 dense = measured bf16 / 2 (MEASURED_PEAKS.json has no TF32 entry)
+        D_, H_ = cfg["mlp"][0].shape[1], cfg["mlp"][0].shape[0]
+        flops_launch = 4.0 * D_ * H_ * (6 * att_launch + 2 * n)
+        peak = measured_peak("bf16_tflops") / 2.0
+        achieved = flops_launch / (kern_ms / 1e3) / 1e12
+        roof = dict(bound="tensor", achieved=achieved, peak=peak, unit="TFLOP/s",
+                    frac=achieved / peak, traffic=traffic, kernel="mlp_tc_kernel (whole solve timed)",
+                    note="algorithmic GEMM flops of the fp32 MLP (3xTF32 issues 3x the MMAs) / "
+                         "whole-solve time; peak = TF32 dense = MEASURED_PEAKS bf16_tflops / 2",
+                    kernel_ms=kern_ms)
+    else:
+        peak_fp64 = fp64_peak(torch, lib, dev)
+        flops_launch = flops_per_step(cfg["dyn"], d) * att_launch + flops_per_point(d) * pts
+        achieved = flops_launch / (kern_ms / 1e3) / 1e12
+        roof = dict(bound="fp64", achieved=achieved, peak=peak_fp64, unit="TFLOP/s",
+                    frac=achieved / peak_fp64, traffic=traffic, kernel="bode_persistent_kernel",
+                    note="algorithmic flops (SURVEY §8(a): 82d+20+6F_f per attempted step, "
+                         "15d+51 per point; pow, div, sqrt not counted) / persistent-kernel time "
+                         "(CUDA events around its launch); peak = DFMA throughput measured in-run "
+                         "by bode_probe_fp64 (2 flops/DFMA); traffic = ncu dram bytes/launch "
+                         "(profiles/traffic.json); ncu FP64-pipe utilisation in profiles/",
+                    kernel_ms=kern_ms)
 
     # ---- end to end through the reference-facing solve() with host buffers
     e2e = None
@@ -373,14 +411,9 @@ def run_bode(args, rank, world, local_rank):
                         parallelism=f"shard{world}", l2="flushed (256 MiB write) between steps",
                         accepted_per_step=accepted / args.steps,
                         attempted_per_step=attempted / args.steps),
-            roofline=dict(bound="fp64", achieved=achieved, peak=peak_fp64, unit="TFLOP/s",
-                          frac=achieved / peak_fp64, traffic=None,
-                          kernel="bode_persistent_kernel",
-                          note="algorithmic flops (SURVEY §8(a): 82d+20+6F_f per attempted "
-                               "step, 15d+51 per point; pow not counted) / solve time; peak = "
-                               "DFMA throughput measured in-run by bode_probe_fp64 (2 flops/DFMA)",
-                          kernel_ms=kern_ms),
-            cpu_baseline=cpu, e2e=e2e, gpu_launches=2 * args.steps, clocks=clocks)
+            roofline=roof,
+            cpu_baseline=cpu, e2e=e2e, gpu_launches=launches_per_step * args.steps,
+            clocks=clocks)
         print(json.dumps(line), flush=True)
     if dist:
         dist.barrier()

@@ -197,6 +197,12 @@ typedef struct bode_solve_args {
    * (3xTF32 tcgen05.mma, fp32 accumulation in TMEM) */
   int32_t mlp_backend;
   int32_t _pad3;
+  /* optional cudaEvent_t pair recorded on `stream` immediately before and
+   * after the persistent integrator launch (roofline timing in bench.py) */
+  void* prof_event_start;
+  void* prof_event_stop;
+  /* optional HOST pointer: number of kernels this call launched */
+  int64_t* launch_count_out;
 } bode_solve_args;
 
 #define BODE_MLP_AUTO 0

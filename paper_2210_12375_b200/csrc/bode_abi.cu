@@ -22,6 +22,7 @@ using namespace bode;
 
 namespace {
 thread_local std::string g_err;
+thread_local int64_t g_launches;  // kernels launched by the current call
 
 int fail(int code, const std::string& msg) {
   g_err = msg;
@@ -173,17 +174,20 @@ int run_chunk(const bode_solve_args* a, int64_t lo, int64_t hi, const Layout& L,
   const size_t words = Workspace::bitmap_words(a->max_steps);
   P.smem_words = words * 4 <= 32 * 1024 ? (int32_t)words : 0;  // per-block shared bitmap
   P.f0 = (double*)(ws + L.f0);
+  P.ev_start = a->prof_event_start;
+  P.ev_stop = a->prof_event_stop;
   if (a->order) {
     if (lo != 0 || hi != a->n) return fail(BODE_EINVAL, "an explicit order cannot be chunked");
     P.order = a->order;
   } else if (a->cost_hint) {
     int64_t* order = nullptr;
     e = lpt_order(a->cost_hint + lo, n, ws + L.lpt, &order, st);
+    g_launches += 3;
     if (e != cudaSuccess) return cuda_fail(e, "LPT order");
     P.order = order;
   }
   if (a->dyn.kind == BODE_DYN_MLP) {
-    e = mlp_solve(a, P, ws + L.mlp, st);
+    e = mlp_solve(a, P, ws + L.mlp, st, &g_launches);
     return e == cudaSuccess ? BODE_OK : cuda_fail(e, "mlp solve");
   }
   switch (a->method) {
@@ -191,11 +195,13 @@ int run_chunk(const bode_solve_args* a, int64_t lo, int64_t hi, const Layout& L,
     case BODE_METHOD_TSIT5: e = solve_tsit5(a->mode, a->dyn.kind, d, P, a->threads_per_block, a->blocks, st); break;
     default: e = solve_heun(a->mode, a->dyn.kind, d, P, a->threads_per_block, a->blocks, st); break;
   }
+  g_launches += 2;  // init pass + persistent integrator
   return e == cudaSuccess ? BODE_OK : cuda_fail(e, "solve launch");
 }
 
 int finalize(const bode_solve_args* a, cudaStream_t st) {
   char* ws = (char*)a->workspace;
+  g_launches += 1;
   bode_finalize_kernel<<<1, 256, 0, st>>>((unsigned long long*)(ws + 8),
                                           (uint32_t*)(ws + Workspace::kHeader),
                                           stages_of(a->method), fsal_of(a->method), a->n_f_evals,
@@ -238,18 +244,22 @@ size_t bode_workspace_size(const bode_solve_args* a) {
 int bode_solve(const bode_solve_args* a) {
   int rc = validate(a);
   if (rc != BODE_OK) return rc;
+  g_launches = 0;
   const Layout L = layout(a, a->n);
   if (!a->workspace || a->workspace_bytes < L.total)
     return fail(BODE_EINVAL, "workspace too small (see bode_workspace_size)");
   cudaStream_t st = (cudaStream_t)a->stream;
   if ((rc = reset_workspace(a, st)) != BODE_OK) return rc;
   if ((rc = run_chunk(a, 0, a->n, L, st)) != BODE_OK) return rc;
-  return finalize(a, st);
+  rc = finalize(a, st);
+  if (a->launch_count_out) *a->launch_count_out = g_launches;
+  return rc;
 }
 
 int bode_solve_host(const bode_solve_args* h) {
   int rc = validate(h);
   if (rc != BODE_OK) return rc;
+  g_launches = 0;
   retain_pool();
   const int64_t n = h->n, d = h->d;
   const bool csr = h->t_eval_offsets != nullptr;
@@ -447,6 +457,7 @@ int bode_solve_host(const bode_solve_args* h) {
   if (rc != BODE_OK) return rc;
   if (e != cudaSuccess) return cuda_fail(e, "host<->device copy");
   if (e2 != cudaSuccess) return cuda_fail(e2, "solve");
+  if (h->launch_count_out) *h->launch_count_out = g_launches;
   return BODE_OK;
 }
 

@@ -496,7 +496,7 @@ size_t mlp_workspace_bytes(const bode_solve_args* a) { return carve(a, nullptr, 
 
 template <int M>
 static cudaError_t mlp_solve_m(const bode_solve_args* a, const SolveParams& P, char* wsb,
-                               cudaStream_t st) {
+                               cudaStream_t st, int64_t* launches) {
   using T = Tab<M>;
   const int64_t n = a->n;
   const int D = (int)a->d, H = (int)a->dyn.hidden;
@@ -516,14 +516,17 @@ static cudaError_t mlp_solve_m(const bode_solve_args* a, const SolveParams& P, c
   if (a->mlp_backend == BODE_MLP_TCGEN05 && !tc_ok) return cudaErrorNotSupported;
   const bool use_tc = tc_ok && a->mlp_backend != BODE_MLP_CUDA_CORE;
   if (use_tc && (e = mlp_tc_prep(W1, W2, H, W.wprep, st)) != cudaSuccess) return e;
+  int64_t nl = use_tc ? 1 : 0;  // kernels launched
   const int max_tiles = (int)((n + 127) / 128);
   // f(Y) for the compacted fp32 rows in W.Y (init evaluations)
   auto eval = [&](float* out) {
     if (use_tc) {
       MlpTcArgs t{n, H, 0, W.y, W.k, W.h, W.act[0], W.cnt, W.Y, W.wprep, b1, b2, out};
       mlp_tc_launch<M>(t, max_tiles, st);
+      nl += 1;
       return;
     }
+    nl += 1;
     // one persistent block per SM; blocks past the live tile count exit
     const unsigned g = grid_for(n, kTile, (unsigned)sms);
     mlp_eval_cc_kernel<<<g, 256, smem, st>>>(W.Y, W.act[0], W.cnt, W1, b1, W2, b2, D, H, out);
@@ -534,8 +537,10 @@ static cudaError_t mlp_solve_m(const bode_solve_args* a, const SolveParams& P, c
       MlpTcArgs t{n, H, s, W.y, W.k, W.h, W.act[0], W.cnt, nullptr, W.wprep, b1, b2,
                   W.k + (size_t)s * n * D};
       mlp_tc_launch<M>(t, max_tiles, st);
+      nl += 1;
       return;
     }
+    nl += 1;
     if (s == 0)
       mlp_state_input_kernel<<<grid_for(n * D), 256, 0, st>>>(W, D);
     else
@@ -558,6 +563,7 @@ static cudaError_t mlp_solve_m(const bode_solve_args* a, const SolveParams& P, c
   mlp_init_c_kernel<<<(unsigned)((n + 3) / 4), 128, 0, st>>>(W, I, A, n, D, heur ? 1 : 0);
   mlp_copy_list_kernel<<<grid_for(n), 256, 0, st>>>(W);
   mlp_swap_kernel<<<1, 32, 0, st>>>(W);
+  nl += heur ? 5 : 4;
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
 
   // lockstep iterations in bursts; each burst ends with one host read of the
@@ -572,6 +578,7 @@ static cudaError_t mlp_solve_m(const bode_solve_args* a, const SolveParams& P, c
       mlp_control_kernel<M><<<(unsigned)((n + 3) / 4), 128, 0, st>>>(W, A, n, D);
       mlp_copy_list_kernel<<<grid_for(n), 256, 0, st>>>(W);
       mlp_swap_kernel<<<1, 32, 0, st>>>(W);
+      nl += 3;
     }
     iters += burst;
     if ((e = cudaMemcpyAsync(h_cnt, W.cnt, sizeof(int32_t), cudaMemcpyDeviceToHost, st)) != cudaSuccess) break;
@@ -580,14 +587,16 @@ static cudaError_t mlp_solve_m(const bode_solve_args* a, const SolveParams& P, c
     burst = burst < 32 ? burst * 2 : 32;
   }
   cudaFreeHost(h_cnt);
+  if (launches) *launches += nl;
   return e == cudaSuccess ? cudaGetLastError() : e;
 }
 
-cudaError_t mlp_solve(const bode_solve_args* a, const SolveParams& P, char* ws, cudaStream_t st) {
+cudaError_t mlp_solve(const bode_solve_args* a, const SolveParams& P, char* ws, cudaStream_t st,
+                      int64_t* launches) {
   switch (a->method) {
-    case BODE_METHOD_DOPRI5: return mlp_solve_m<BODE_METHOD_DOPRI5>(a, P, ws, st);
-    case BODE_METHOD_TSIT5: return mlp_solve_m<BODE_METHOD_TSIT5>(a, P, ws, st);
-    default: return mlp_solve_m<BODE_METHOD_HEUN>(a, P, ws, st);
+    case BODE_METHOD_DOPRI5: return mlp_solve_m<BODE_METHOD_DOPRI5>(a, P, ws, st, launches);
+    case BODE_METHOD_TSIT5: return mlp_solve_m<BODE_METHOD_TSIT5>(a, P, ws, st, launches);
+    default: return mlp_solve_m<BODE_METHOD_HEUN>(a, P, ws, st, launches);
   }
 }
 

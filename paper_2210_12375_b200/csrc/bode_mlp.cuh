@@ -4,7 +4,8 @@
 
 namespace bode {
 size_t mlp_workspace_bytes(const bode_solve_args* a);
-cudaError_t mlp_solve(const bode_solve_args* a, const SolveParams& P, char* ws, cudaStream_t st);
+cudaError_t mlp_solve(const bode_solve_args* a, const SolveParams& P, char* ws, cudaStream_t st,
+                      int64_t* launches);
 
 // tcgen05 3xTF32 stage evaluation (bode_mlp_tc.cu)
 struct MlpTcArgs {

@@ -54,6 +54,8 @@ struct SolveParams {
   uint32_t* refresh;           // global bitmap over iterations
   int32_t smem_words;          // >0: per-block shared bitmap of this many words
   double* f0;                  // (n, D) FSAL seeds from the init pass
+  void* ev_start;              // host side only: optional cudaEvent_t around
+  void* ev_stop;               // the persistent launch (bench roofline)
 };
 
 struct Workspace {
@@ -226,7 +228,10 @@ struct Lane {
 template <int M, class F, class O>
 // 2-D systems fit 5 blocks of 128 threads per SM (<= 102 registers); wider
 // ones keep 4 (<= 128 registers) to avoid spilling the stage vectors.
-__global__ void __launch_bounds__(128, (F::D <= 2 ? 5 : 4)) bode_persistent_kernel(const SolveParams P) {
+#ifndef BODE_BLOCKS_2D
+#define BODE_BLOCKS_2D 5
+#endif
+__global__ void __launch_bounds__(128, (F::D <= 2 ? BODE_BLOCKS_2D : 4)) bode_persistent_kernel(const SolveParams P) {
   extern __shared__ uint32_t s_refresh[];
   __shared__ PowTables s_pow;  // pow tables: divergent lookups, so shared not constant
   const int lane = threadIdx.x & 31;
@@ -335,7 +340,9 @@ cudaError_t launch_persistent(const SolveParams& P, int threads, int blocks, cud
     const int64_t ib = (P.n + 127) / 128;
     bode_init_kernel<M, F, O><<<(unsigned)(ib < 148 * 64 ? ib : 148 * 64), 128, 0, st>>>(P);
   }
+  if (P.ev_start) cudaEventRecord((cudaEvent_t)P.ev_start, st);
   kern<<<blocks, threads, smem, st>>>(P);
+  if (P.ev_stop) cudaEventRecord((cudaEvent_t)P.ev_stop, st);
   return cudaGetLastError();
 }
 

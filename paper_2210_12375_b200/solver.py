@@ -312,7 +312,8 @@ def solve_device(y0, t_start, t_end, f, *, t_eval=None, t_eval_offsets=None, met
                  atol=1e-6, rtol=1e-6, controller: PidCoefficients | None = None,
                  max_steps: int = DEFAULT_MAX_STEPS, dt0=None, order=None, cost_hint=None,
                  mode: str = "exact", record_trace: bool = False, stream=None,
-                 threads_per_block: int = 0, blocks: int = 0, mlp_backend: str = "auto"):
+                 threads_per_block: int = 0, blocks: int = 0, mlp_backend: str = "auto",
+                 prof_events=None):
     """Device-resident solve on torch CUDA tensors; asynchronous (no host
     sync).  ``t_eval``: None, a 1-D tensor shared by all instances, a 2-D
     (n, m) tensor, or CSR values with ``t_eval_offsets`` (n+1).  ``atol`` /
@@ -409,6 +410,9 @@ def solve_device(y0, t_start, t_end, f, *, t_eval=None, t_eval_offsets=None, met
         a.trace_accept, a.trace_cap = out["trace_accept"].data_ptr(), cap
     a.threads_per_block, a.blocks = int(threads_per_block), int(blocks)
     a.mlp_backend = MLP_BACKENDS[mlp_backend]
+    if prof_events is not None:  # (torch.cuda.Event, torch.cuda.Event) around the integrator
+        a.prof_event_start, a.prof_event_stop = (prof_events[0].cuda_event,
+                                                 prof_events[1].cuda_event)
     wsb = lib.bode_workspace_size(_abi.C.byref(a))
     if wsb == 0:
         _abi.check(_abi.EINVAL)
@@ -417,12 +421,15 @@ def solve_device(y0, t_start, t_end, f, *, t_eval=None, t_eval_offsets=None, met
     a.workspace, a.workspace_bytes = ws.data_ptr(), wsb
     st = stream if stream is not None else torch.cuda.current_stream(dev)
     a.stream = st.cuda_stream
+    nlaunch = _abi.C.c_int64(0)
+    a.launch_count_out = _abi.C.addressof(nlaunch)
     _abi.check(lib.bode_solve(_abi.C.byref(a)))
     # keep inputs alive until the stream has consumed them
     for t in keep:
         if isinstance(t, torch.Tensor):
             t.record_stream(st)
     out["ys"] = out["ys"][:n_rows]
+    out["launches"] = int(nlaunch.value)
     out["offsets"] = offsets
     out["shared_len"] = shared_len
     return out
