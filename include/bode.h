@@ -39,7 +39,7 @@
 extern "C" {
 #endif
 
-#define BODE_ABI_VERSION 1
+#define BODE_ABI_VERSION 2
 
 /* return codes */
 #define BODE_OK 0
@@ -160,7 +160,7 @@ typedef struct bode_solve_args {
   int64_t* n_steps;     /* (n,) */
   int64_t* n_accepted;  /* (n,) */
   double* final_dt;     /* (n,) */
-  int32_t* status;      /* (n,) */
+  int64_t* status;      /* (n,) SolveStatus codes, int64 like the reference */
   int64_t* n_f_evals;   /* (1,) batch-global count (solver.py:184,224,239) */
   /* optional record_trace (solver.py:196-199,257-261): (n, trace_cap) */
   double* trace_t;

@@ -143,7 +143,7 @@ def solve(y0, t_start, t_end, t_eval, dyn, method="dopri5", atol=1e-6, rtol=1e-6
     ts = _f64(np.broadcast_to(t_start, (n,)))
     tn = _f64(np.broadcast_to(t_end, (n,)))
     a = Args()
-    a.abi_version = 1
+    a.abi_version = 2
     a.method = METHODS[method]
     a.n, a.d = n, d
     a.dyn = make_dyn(dyn["name"], dyn.get("inst"), dyn.get("shared", ()), dyn.get("mlp"), keep)
@@ -188,7 +188,7 @@ def solve(y0, t_start, t_end, t_eval, dyn, method="dopri5", atol=1e-6, rtol=1e-6
         ys=np.full((max(n_rows, 1), d), np.nan) if with_ys else None,
         n_emitted=np.zeros(n, np.int64), n_steps=np.zeros(n, np.int64),
         n_accepted=np.zeros(n, np.int64), final_dt=np.zeros(n),
-        status=np.zeros(n, np.int32), n_f_evals=np.zeros(1, np.int64))
+        status=np.zeros(n, np.int64), n_f_evals=np.zeros(1, np.int64))
     a.ys = _p(out["ys"])
     a.n_emitted, a.n_steps, a.n_accepted = _p(out["n_emitted"]), _p(out["n_steps"]), _p(out["n_accepted"])
     a.final_dt, a.status, a.n_f_evals = _p(out["final_dt"]), _p(out["status"]), _p(out["n_f_evals"])

@@ -12,7 +12,7 @@ import os
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("BODE_LIB") or os.path.join(HERE, "_build", "libbode.so")
 
-ABI_VERSION = 1
+ABI_VERSION = 2
 OK, EINVAL, ECUDA, EUNSUPPORTED = 0, 1, 2, 3
 METHOD = {"dopri5": 0, "tsit5": 1, "heun": 2}
 MODE = {"exact": 0, "fast": 1}

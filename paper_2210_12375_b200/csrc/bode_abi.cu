@@ -7,13 +7,16 @@
 //   -> n_f_evals finalisation.
 // bode_solve_host adds the host<->device copies and, optionally, a chunked
 // pipeline that overlaps chunk k's solve with the neighbouring chunks' copies.
+#include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
 #include <vector>
 
 #include "bode_dispatch.cuh"
+#include "bode_hostio.cuh"
 #include "bode_mlp.cuh"
 #include "bode_sched.cuh"
 #include "bode_units.cuh"
@@ -102,16 +105,22 @@ int validate(const bode_solve_args* a) {
   return BODE_OK;
 }
 
-// Workspace: [header | iteration bitmap | f0 (n_max x d) | LPT scratch | MLP scratch]
+// Workspace: [header | iteration bitmap | f0 (n x d) | LPT scratch x slots | MLP scratch]
+// Header: queue counter of slot 0 at +0, max n_steps at +8, queue counter of
+// slot 1 at +16.  Pipelined host solves run consecutive chunks on two
+// streams (slots 0/1), so a chunk's solve can fill the SMs the previous
+// chunk's tail leaves idle; each slot has its own queue and LPT scratch, and
+// f0 rows are indexed by absolute instance.
 struct Layout {
-  size_t f0, lpt, mlp, total;
+  size_t f0, lpt, lpt_slot, mlp, total;
 };
 
-Layout layout(const bode_solve_args* a, int64_t n_max) {
+Layout layout(const bode_solve_args* a, int64_t n_chunk, int slots) {
   Layout L;
   L.f0 = Workspace::f0_offset(a->max_steps);
-  L.lpt = L.f0 + ((8 * (size_t)n_max * (size_t)a->d + 255) & ~(size_t)255);
-  L.mlp = L.lpt + (a->cost_hint && !a->order ? ((lpt_workspace_bytes(n_max) + 255) & ~(size_t)255) : 0);
+  L.lpt = L.f0 + ((8 * (size_t)a->n * (size_t)a->d + 255) & ~(size_t)255);
+  L.lpt_slot = a->cost_hint && !a->order ? ((lpt_workspace_bytes(n_chunk) + 255) & ~(size_t)255) : 0;
+  L.mlp = L.lpt + L.lpt_slot * slots;
   L.total = L.mlp + (a->dyn.kind == BODE_DYN_MLP ? mlp_workspace_bytes(a) : 0);
   return L;
 }
@@ -127,11 +136,13 @@ int reset_workspace(const bode_solve_args* a, cudaStream_t st) {
 // Solve rows [lo, hi) of the batch described by `a` (device pointers).  The
 // iteration bitmap and max n_steps accumulate across chunks, so n_f_evals
 // stays batch-global; the queue counter is reset per chunk.
-int run_chunk(const bode_solve_args* a, int64_t lo, int64_t hi, const Layout& L, cudaStream_t st) {
+int run_chunk(const bode_solve_args* a, int64_t lo, int64_t hi, const Layout& L, cudaStream_t st,
+              int slot = 0) {
   const int64_t n = hi - lo, d = a->d;
   const int n_inst = __builtin_popcount(a->dyn.inst_mask);
   char* ws = (char*)a->workspace;
-  cudaError_t e = cudaMemsetAsync(ws, 0, 8, st);  // queue counter
+  const size_t qoff = slot ? 16 : 0;
+  cudaError_t e = cudaMemsetAsync(ws + qoff, 0, 8, st);  // queue counter
   if (e != cudaSuccess) return cuda_fail(e, "queue reset");
 
   SolveParams P;
@@ -168,12 +179,12 @@ int run_chunk(const bode_solve_args* a, int64_t lo, int64_t hi, const Layout& L,
   P.trace_t = a->trace_t ? a->trace_t + lo * a->trace_cap : nullptr;
   P.trace_dt = a->trace_dt ? a->trace_dt + lo * a->trace_cap : nullptr;
   P.trace_accept = a->trace_accept ? a->trace_accept + lo * a->trace_cap : nullptr;
-  P.queue = (unsigned long long*)ws;
+  P.queue = (unsigned long long*)(ws + qoff);
   P.max_n = (unsigned long long*)(ws + 8);
   P.refresh = (uint32_t*)(ws + Workspace::kHeader);
   const size_t words = Workspace::bitmap_words(a->max_steps);
   P.smem_words = words * 4 <= 32 * 1024 ? (int32_t)words : 0;  // per-block shared bitmap
-  P.f0 = (double*)(ws + L.f0);
+  P.f0 = (double*)(ws + L.f0) + lo * d;
   P.ev_start = a->prof_event_start;
   P.ev_stop = a->prof_event_stop;
   if (a->order) {
@@ -181,7 +192,7 @@ int run_chunk(const bode_solve_args* a, int64_t lo, int64_t hi, const Layout& L,
     P.order = a->order;
   } else if (a->cost_hint) {
     int64_t* order = nullptr;
-    e = lpt_order(a->cost_hint + lo, n, ws + L.lpt, &order, st);
+    e = lpt_order(a->cost_hint + lo, n, ws + L.lpt + slot * L.lpt_slot, &order, st);
     g_launches += 3;
     if (e != cudaSuccess) return cuda_fail(e, "LPT order");
     P.order = order;
@@ -238,14 +249,14 @@ const char* bode_last_error(void) { return g_err.c_str(); }
 
 size_t bode_workspace_size(const bode_solve_args* a) {
   if (validate(a) != BODE_OK) return 0;
-  return layout(a, a->n).total;
+  return layout(a, a->n, 1).total;
 }
 
 int bode_solve(const bode_solve_args* a) {
   int rc = validate(a);
   if (rc != BODE_OK) return rc;
   g_launches = 0;
-  const Layout L = layout(a, a->n);
+  const Layout L = layout(a, a->n, 1);
   if (!a->workspace || a->workspace_bytes < L.total)
     return fail(BODE_EINVAL, "workspace too small (see bode_workspace_size)");
   cudaStream_t st = (cudaStream_t)a->stream;
@@ -269,32 +280,50 @@ int bode_solve_host(const bode_solve_args* h) {
   int chunks = h->pipeline_chunks > 1 ? h->pipeline_chunks : 1;
   if (h->order || h->trace_cap > 0 || h->dyn.kind == BODE_DYN_MLP) chunks = 1;
   if (chunks > n) chunks = (int)n;
+  if (chunks > 64) chunks = 64;
   const int64_t cmax = chunk_max(n, chunks);
 
-  // one device block for every array; per-instance arrays are copied in
-  // chunk slices so chunk k can start as soon as its own rows landed
+  // one device block for every array; per-instance arrays move in chunk
+  // slices so chunk k can start as soon as its own rows landed.  Pinned
+  // host arrays are DMA'd directly, pageable ones through the pinned arena.
   struct Arr {
     const void* hsrc;   // host input (or null)
     void* hdst;         // host output (or null)
-    size_t row_bytes;   // bytes per instance row (0: whole array, chunk 0)
+    size_t row_bytes;   // bytes per instance row (0: whole array)
     size_t bytes;       // total bytes
     size_t off;         // device offset
     const void** in_field;
     void** out_field;
+    bool pinned;
+    size_t stage;       // arena offset (pageable arrays)
   };
   bode_solve_args a = *h;
   std::vector<Arr> arrs;
-  size_t total = 0;
+  size_t total = 0, stage_total = 0;
+  size_t stage_max = (size_t)2 << 30;  // larger pageable payloads use driver staging
+  if (const char* e = std::getenv("BODE_STAGING_MAX")) stage_max = (size_t)std::atoll(e);
   auto place = [&](size_t bytes) {
     const size_t off = total;
     total += (bytes + 255) & ~(size_t)255;
     return off;
   };
+  auto add = [&](const void* hs, void* hd, size_t row_bytes, size_t bytes, const void** fi,
+                 void** fo) {
+    Arr x{hs, hd, row_bytes, bytes, place(bytes), fi, fo, false, 0};
+    x.pinned = hostio::is_pinned(hs ? hs : hd);
+    if (!x.pinned && stage_total + bytes <= stage_max) {
+      x.stage = stage_total;
+      stage_total += (bytes + 4095) & ~(size_t)4095;
+    } else if (!x.pinned) {
+      x.stage = SIZE_MAX;  // direct pageable copy
+    }
+    arrs.push_back(x);
+  };
   auto in = [&](const void** field, size_t row_bytes, size_t bytes) {
-    if (*field && bytes) arrs.push_back({*field, nullptr, row_bytes, bytes, place(bytes), field, nullptr});
+    if (*field && bytes) add(*field, nullptr, row_bytes, bytes, field, nullptr);
   };
   auto out = [&](void** field, size_t row_bytes, size_t bytes) {
-    if (*field && bytes) arrs.push_back({nullptr, *field, row_bytes, bytes, place(bytes), nullptr, field});
+    if (*field && bytes) add(nullptr, *field, row_bytes, bytes, nullptr, field);
   };
   in((const void**)&a.y0, 8 * d, 8 * n * d);
   in((const void**)&a.t_start, 8, 8 * n);
@@ -321,138 +350,164 @@ int bode_solve_host(const bode_solve_args* h) {
   out((void**)&a.n_steps, 8, 8 * n);
   out((void**)&a.n_accepted, 8, 8 * n);
   out((void**)&a.final_dt, 8, 8 * n);
-  out((void**)&a.status, 4, 4 * n);
+  out((void**)&a.status, 8, 8 * n);
   out((void**)&a.trace_t, 8 * h->trace_cap, 8 * n * h->trace_cap);
   out((void**)&a.trace_dt, 8 * h->trace_cap, 8 * n * h->trace_cap);
   out((void**)&a.trace_accept, h->trace_cap, n * h->trace_cap);
   out((void**)&a.max_iterations_out, 0, 8);
   out((void**)&a.refresh_map_out, 0, (size_t)h->max_steps + 2);
-  const size_t nfe_off = place(8);
-  const Layout L = layout(h, cmax);
+  out((void**)&a.n_f_evals, 0, 8);
+  const Layout L = layout(h, cmax, chunks > 1 ? 2 : 1);
   const size_t ws_off = place(L.total);
 
+  hostio::Arena& ar = hostio::arena();
+  std::lock_guard<std::mutex> arena_lock(ar.m);  // one staged host solve at a time
+  cudaError_t e = ar.reserve(stage_total);
+  if (e != cudaSuccess) return cuda_fail(e, "pinned staging arena");
+  char* stage = ar.p;
+
   cudaStream_t st = (cudaStream_t)h->stream;
-  cudaStream_t cs = st;  // copy stream (separate only when pipelining)
-  cudaEvent_t ev_in[64], ev_done[64];
-  if (chunks > 64) chunks = 64;
   char* dev = nullptr;
-  cudaError_t e = cudaMallocAsync((void**)&dev, total, st);
+  e = cudaMallocAsync((void**)&dev, total, st);
   if (e != cudaSuccess) return cuda_fail(e, "device allocation");
   for (auto& x : arrs) {
     if (x.in_field) *x.in_field = dev + x.off;
     if (x.out_field) *x.out_field = dev + x.off;
   }
-  int64_t* d_nfe = (int64_t*)(dev + nfe_off);
-  a.n_f_evals = d_nfe;
   a.workspace = dev + ws_off;
   a.workspace_bytes = L.total;
-  if (chunks > 1) {
-    if ((e = cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking)) != cudaSuccess)
-      return cuda_fail(e, "copy stream");
-    for (int k = 0; k < chunks; k++) {
-      cudaEventCreateWithFlags(&ev_in[k], cudaEventDisableTiming);
-      cudaEventCreateWithFlags(&ev_done[k], cudaEventDisableTiming);
-    }
-    cudaEvent_t ready;  // allocation visible to the copy stream
+  // uploads on `cin`, downloads on `cout`, solves on the caller's stream
+  cudaStream_t cin, cout, st2 = st;
+  cudaStreamCreateWithFlags(&cin, cudaStreamNonBlocking);
+  cudaStreamCreateWithFlags(&cout, cudaStreamNonBlocking);
+  if (chunks > 1) cudaStreamCreateWithFlags(&st2, cudaStreamNonBlocking);
+  cudaEvent_t ev_in[64], ev_done[65], ev_out[65];
+  for (int k = 0; k <= chunks; k++) {
+    if (k < chunks) cudaEventCreateWithFlags(&ev_in[k], cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&ev_done[k], cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&ev_out[k], cudaEventDisableTiming);
+  }
+  {
+    cudaEvent_t ready;  // the allocation is visible to the copy streams
     cudaEventCreateWithFlags(&ready, cudaEventDisableTiming);
     cudaEventRecord(ready, st);
-    cudaStreamWaitEvent(cs, ready, 0);
+    cudaStreamWaitEvent(cin, ready, 0);
+    cudaStreamWaitEvent(cout, ready, 0);
+    if (st2 != st) cudaStreamWaitEvent(st2, ready, 0);
     cudaEventDestroy(ready);
   }
   auto rows = [&](int k, int64_t& lo, int64_t& hi) {
     lo = (int64_t)k * cmax;
     hi = lo + cmax < n ? lo + cmax : n;
   };
-  auto copy_in = [&](int k) -> cudaError_t {
+  // byte range [o, o+b) of array x that belongs to chunk k; k == chunks
+  // means "the whole-array outputs written by the finaliser"
+  auto slice = [&](const Arr& x, int k, size_t& o, size_t& b) -> bool {
     int64_t lo, hi;
-    rows(k, lo, hi);
+    if (x.row_bytes) {
+      if (k == chunks) return false;
+      rows(k, lo, hi);
+      o = (size_t)lo * x.row_bytes;
+      b = (size_t)(hi - lo) * x.row_bytes;
+    } else if (x.out_field == (void**)&a.ys) {  // ys rows of this chunk's instances
+      if (k == chunks) return false;
+      rows(k, lo, hi);
+      const int64_t r0 = csr ? h->t_eval_offsets[lo] : lo * h->t_eval_len;
+      const int64_t r1 = csr ? h->t_eval_offsets[hi] : hi * h->t_eval_len;
+      o = (size_t)r0 * 8 * d;
+      b = (size_t)(r1 - r0) * 8 * d;
+    } else {  // whole arrays: inputs with chunk 0, outputs after the finaliser
+      if (k != (x.in_field ? 0 : chunks)) return false;
+      o = 0;
+      b = x.bytes;
+    }
+    return b > 0;
+  };
+  auto copy_in = [&](int k) -> cudaError_t {
     for (size_t j = 0; j < n_in; j++) {
       const Arr& x = arrs[j];
-      size_t o = 0, b = x.bytes;
-      if (x.row_bytes) {
-        o = (size_t)lo * x.row_bytes;
-        b = (size_t)(hi - lo) * x.row_bytes;
-      } else if (k != 0) {
-        continue;  // whole arrays travel with chunk 0
+      size_t o, b;
+      if (!slice(x, k, o, b)) continue;
+      const char* src = (const char*)x.hsrc + o;
+      if (!x.pinned && x.stage != SIZE_MAX) {  // pageable: fill the arena on the host team
+        hostio::par_copy(stage + x.stage + o, src, b);
+        src = stage + x.stage + o;
       }
-      cudaError_t r = cudaMemcpyAsync(dev + x.off + o, (const char*)x.hsrc + o, b,
-                                      cudaMemcpyHostToDevice, cs);
+      cudaError_t r = cudaMemcpyAsync(dev + x.off + o, src, b, cudaMemcpyHostToDevice, cin);
       if (r != cudaSuccess) return r;
     }
     return cudaSuccess;
   };
   auto copy_out = [&](int k) -> cudaError_t {
-    int64_t lo, hi;
-    rows(k, lo, hi);
     for (size_t j = n_in; j < arrs.size(); j++) {
       const Arr& x = arrs[j];
       size_t o, b;
-      if (x.row_bytes) {
-        o = (size_t)lo * x.row_bytes;
-        b = (size_t)(hi - lo) * x.row_bytes;
-      } else if (x.out_field == (void**)&a.ys) {  // ys: rows [row_lo, row_hi) of this chunk
-        const int64_t r0 = csr ? h->t_eval_offsets[lo] : lo * h->t_eval_len;
-        const int64_t r1 = csr ? h->t_eval_offsets[hi] : hi * h->t_eval_len;
-        o = (size_t)r0 * 8 * d;
-        b = (size_t)(r1 - r0) * 8 * d;
-      } else {  // whole small outputs (written by the finaliser) travel last
-        if (k != chunks - 1) continue;
-        o = 0;
-        b = x.bytes;
-      }
-      if (!b) continue;
-      cudaError_t r = cudaMemcpyAsync((char*)x.hdst + o, dev + x.off + o, b,
-                                      cudaMemcpyDeviceToHost, cs);
+      if (!slice(x, k, o, b)) continue;
+      char* dst = (!x.pinned && x.stage != SIZE_MAX) ? stage + x.stage + o : (char*)x.hdst + o;
+      cudaError_t r = cudaMemcpyAsync(dst, dev + x.off + o, b, cudaMemcpyDeviceToHost, cout);
       if (r != cudaSuccess) return r;
     }
     return cudaSuccess;
   };
+  auto drain = [&](int k) {  // arena -> pageable user outputs of chunk k
+    for (size_t j = n_in; j < arrs.size(); j++) {
+      const Arr& x = arrs[j];
+      size_t o, b;
+      if (x.pinned || x.stage == SIZE_MAX || !slice(x, k, o, b)) continue;
+      hostio::par_copy((char*)x.hdst + o, stage + x.stage + o, b);
+    }
+  };
 
   rc = reset_workspace(&a, st);
+  if (st2 != st) {  // the reset is visible to the second chunk stream
+    cudaEventRecord(ev_done[chunks], st);
+    cudaStreamWaitEvent(st2, ev_done[chunks], 0);
+  }
   for (int k = 0; k < chunks && rc == BODE_OK && e == cudaSuccess; k++) {
-    // upload chunk k (the host call returns once its pageable data is
-    // staged, so chunk k-1's solve is already running on the GPU)
+    // while the host stages chunk k, chunk k-1 is already solving
     if ((e = copy_in(k)) != cudaSuccess) break;
-    if (chunks > 1) {
-      cudaEventRecord(ev_in[k], cs);
-      cudaStreamWaitEvent(st, ev_in[k], 0);
-    }
+    cudaStream_t sk = (k & 1) ? st2 : st;
+    cudaEventRecord(ev_in[k], cin);
+    cudaStreamWaitEvent(sk, ev_in[k], 0);
     int64_t lo, hi;
     rows(k, lo, hi);
-    if ((rc = run_chunk(&a, lo, hi, L, st)) != BODE_OK) break;
-    if (chunks > 1) {
-      cudaEventRecord(ev_done[k], st);
-      if (k > 0) {  // download chunk k-1 while chunk k computes
-        cudaStreamWaitEvent(cs, ev_done[k - 1], 0);
-        if ((e = copy_out(k - 1)) != cudaSuccess) break;
-      }
-    }
+    if ((rc = run_chunk(&a, lo, hi, L, sk, k & 1)) != BODE_OK) break;
+    cudaEventRecord(ev_done[k], sk);
+    cudaStreamWaitEvent(cout, ev_done[k], 0);
+    if ((e = copy_out(k)) != cudaSuccess) break;
+    cudaEventRecord(ev_out[k], cout);
+  }
+  if (st2 != st && rc == BODE_OK && e == cudaSuccess) {  // join: last chunk on st2
+    const int last_odd = (chunks - 1) & 1 ? chunks - 1 : chunks - 2;
+    cudaStreamWaitEvent(st, ev_done[last_odd], 0);
   }
   if (rc == BODE_OK && e == cudaSuccess) rc = finalize(&a, st);
   if (rc == BODE_OK && e == cudaSuccess) {
-    if (chunks > 1) {
-      cudaStreamWaitEvent(cs, ev_done[chunks - 1], 0);
-      e = copy_out(chunks - 1);
-      cudaEvent_t fin;
-      cudaEventCreateWithFlags(&fin, cudaEventDisableTiming);
-      cudaEventRecord(fin, cs);
-      cudaStreamWaitEvent(st, fin, 0);
-      cudaEventDestroy(fin);
-    } else {
-      e = copy_out(0);
-    }
-    if (e == cudaSuccess)
-      e = cudaMemcpyAsync(h->n_f_evals, d_nfe, 8, cudaMemcpyDeviceToHost, st);
+    cudaEventRecord(ev_done[chunks], st);
+    cudaStreamWaitEvent(cout, ev_done[chunks], 0);
+    e = copy_out(chunks);
+    cudaEventRecord(ev_out[chunks], cout);
   }
+  const bool ok = rc == BODE_OK && e == cudaSuccess;
+  // drain pageable outputs chunk by chunk while later chunks still solve
+  for (int k = 0; ok && k <= chunks; k++) {
+    if (cudaEventSynchronize(ev_out[k]) != cudaSuccess) break;
+    drain(k);
+  }
+  cudaStreamSynchronize(cin);
+  cudaStreamSynchronize(cout);
   cudaFreeAsync(dev, st);
   cudaError_t e2 = cudaStreamSynchronize(st);
-  if (chunks > 1) {
-    cudaStreamSynchronize(cs);
-    for (int k = 0; k < chunks; k++) {
-      cudaEventDestroy(ev_in[k]);
-      cudaEventDestroy(ev_done[k]);
-    }
-    cudaStreamDestroy(cs);
+  for (int k = 0; k <= chunks; k++) {
+    if (k < chunks) cudaEventDestroy(ev_in[k]);
+    cudaEventDestroy(ev_done[k]);
+    cudaEventDestroy(ev_out[k]);
+  }
+  cudaStreamDestroy(cin);
+  cudaStreamDestroy(cout);
+  if (st2 != st) {
+    cudaStreamSynchronize(st2);
+    cudaStreamDestroy(st2);
   }
   if (rc != BODE_OK) return rc;
   if (e != cudaSuccess) return cuda_fail(e, "host<->device copy");

@@ -173,7 +173,7 @@ struct CtrlArgs {
   int64_t* n_steps;
   int64_t* n_accepted;
   double* final_dt;
-  int32_t* status;
+  int64_t* status;
   int64_t max_steps;
   unsigned long long* max_n;
   uint32_t* refresh;

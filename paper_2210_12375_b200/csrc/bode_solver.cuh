@@ -43,7 +43,7 @@ struct SolveParams {
   int64_t* n_steps;
   int64_t* n_accepted;
   double* final_dt;
-  int32_t* status;
+  int64_t* status;
   double* trace_t;
   double* trace_dt;
   uint8_t* trace_accept;

@@ -249,7 +249,10 @@ def build_struct(dyn: DeviceDynamics, n: int, keep: list, device_arrays=None):
         else:
             if any(_is_tensor(c) for c in cols):
                 raise ValueError("device tensors given to the host solve path")
-            inst = np.ascontiguousarray(np.stack(cols, axis=1))
+            if len(cols) == 1:  # one per-instance slot: pass the caller's array, no copy
+                inst = np.ascontiguousarray(np.asarray(cols[0], dtype=np.float64).reshape(n, 1))
+            else:
+                inst = np.ascontiguousarray(np.stack(cols, axis=1))
         keep.append(inst)
         s.inst_params = ptr(inst)
     if dyn.kind == "mlp":

@@ -36,7 +36,7 @@ def test_library_exports_every_header_symbol():
 def test_workspace_size_and_einval_without_gpu():
     lib = _abi.load()
     a = _abi.SolveArgs()
-    a.abi_version = 1
+    a.abi_version = _abi.ABI_VERSION
     assert lib.bode_workspace_size(C.byref(a)) == 0  # n = 0 is invalid
     assert "instance" in lib.bode_last_error().decode()
     with pytest.raises(ValueError):
