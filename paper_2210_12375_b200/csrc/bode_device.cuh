@@ -36,12 +36,13 @@ struct FastOps {
 __device__ __forceinline__ double ddiv(double a, double b) { return __ddiv_rn(a, b); }
 __device__ __forceinline__ double dsqrt(double a) { return __dsqrt_rn(a); }
 
-// np.maximum / np.minimum: NaN-propagating (unlike fmax/fmin)
+// np.maximum / np.minimum: NaN-propagating (unlike fmax/fmin).  a NaN -> a;
+// b NaN (a not) -> the comparison is false -> b; otherwise the ordinary max.
 __device__ __forceinline__ double np_max(double a, double b) {
-  return (a != a) ? a : ((b != b) ? b : (a >= b ? a : b));
+  return (a >= b || a != a) ? a : b;
 }
 __device__ __forceinline__ double np_min(double a, double b) {
-  return (a != a) ? a : ((b != b) ? b : (a <= b ? a : b));
+  return (a <= b || a != a) ? a : b;
 }
 
 // array ** python-float the way NumPy evaluates it (fast_scalar_power
@@ -354,7 +355,7 @@ __device__ __forceinline__ bool np_special_exponent(double e) {
 __device__ __forceinline__ double pow_logged(double x, double e, bool ok, double lh, double ll,
                                              const PowTables& T) {
   if (np_special_exponent(e)) return np_scalar_pow(x, e, T);
-  return (ok && isfinite(e)) ? cr_exp_mul(e, lh, ll, x, T) : pow(x, e);
+  return (ok && isfinite(e)) ? cr_exp_mul(e, lh, ll, x, T) : pow_fallback(x, e);
 }
 
 // adapt() for the persistent solver: the PID term n_prev^(-beta2/k) reuses

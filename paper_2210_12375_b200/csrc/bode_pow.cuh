@@ -41,6 +41,23 @@ static __device__ const PowTables g_pow_tables = {BODE_POW_LOG_TABLE_INIT, BODE_
 #endif
 static const PowTables h_pow_tables = {BODE_POW_LOG_TABLE_INIT, BODE_POW_EXP_TABLE_INIT};
 
+// Polynomial coefficients and split constants.  On the device they live in
+// the constant bank (FP64 instructions take them via LDCU, two per load)
+// instead of 64-bit immediates, which cost two UMOVs each.
+#define BODE_POW_K_INIT                                                        \
+  {1.0 / 9.0, -0.125, 1.0 / 7.0, -1.0 / 6.0, 0.2, -0.25, 1.0 / 3.0, -0.5,     \
+   1.0 / 5040.0, 1.0 / 720.0, 1.0 / 120.0, 1.0 / 24.0, 1.0 / 6.0, 0.5,        \
+   BODE_POW_LN2_HI, BODE_POW_LN2_LO, BODE_POW_C_HI, BODE_POW_C_LO, BODE_POW_INV_C, 0x1p52}
+#if defined(__CUDACC__)
+static __constant__ double c_pow_k[20] = BODE_POW_K_INIT;
+#endif
+static const double h_pow_k[20] = BODE_POW_K_INIT;
+#if defined(__CUDA_ARCH__)
+#define BODE_PK(i) c_pow_k[i]
+#else
+#define BODE_PK(i) h_pow_k[i]
+#endif
+
 namespace powimpl {
 
 BODE_HD double mul(double a, double b) {
@@ -106,7 +123,7 @@ BODE_HD bool cr_log(double x, const PowTables& T, double& lh, double& ll) {
   int64_t ix = bits(x);
   int k = 0;
   if (ix < 0x0010000000000000LL) {  // subnormal: normalise
-    ix = bits(mul(x, 0x1p52));
+    ix = bits(mul(x, BODE_PK(19)));
     k = -52;
   }
   k += (int)(ix >> 52) - 1023;
@@ -121,25 +138,25 @@ BODE_HD bool cr_log(double x, const PowTables& T, double& lh, double& ll) {
   const double sq_lo = fma_(r, r, -sq);
   // log1p(r) - r + r^2/2 = r^3 (1/3 - r/4 + ... + r^6/9) for |r| < 2^-7.9;
   // the first omitted term r^10/10 is below 2^-82
-  double q = 1.0 / 9.0;
-  q = fma_(q, r, -0.125);
-  q = fma_(q, r, 1.0 / 7.0);
-  q = fma_(q, r, -1.0 / 6.0);
-  q = fma_(q, r, 0.2);
-  q = fma_(q, r, -0.25);
-  q = fma_(q, r, 1.0 / 3.0);
+  double q = BODE_PK(0);
+  q = fma_(q, r, BODE_PK(1));
+  q = fma_(q, r, BODE_PK(2));
+  q = fma_(q, r, BODE_PK(3));
+  q = fma_(q, r, BODE_PK(4));
+  q = fma_(q, r, BODE_PK(5));
+  q = fma_(q, r, BODE_PK(6));
   q = mul(q, mul(sq, r));
   // high parts
   double s1, e1, s2, e2, s3, e3;
-  two_sum(mul((double)k, BODE_POW_LN2_HI), logc_hi, s1, e1);
+  two_sum(mul((double)k, BODE_PK(14)), logc_hi, s1, e1);
   two_sum(s1, r, s2, e2);
-  two_sum(s2, mul(-0.5, sq), s3, e3);
+  two_sum(s2, mul(BODE_PK(7), sq), s3, e3);
   // low parts: exact residuals, table tails, first/second-order p_lo terms
   double lo = add(e1, e2);
   lo = add(lo, e3);
-  lo = add(lo, fma_((double)k, BODE_POW_LN2_LO, logc_lo));
+  lo = add(lo, fma_((double)k, BODE_PK(15), logc_lo));
   lo = add(lo, p_lo);
-  lo = sub(lo, mul(0.5, sq_lo));
+  lo = sub(lo, mul(BODE_PK(13), sq_lo));
   lo = sub(lo, mul(r, p_lo));
   lo = add(lo, mul(sq, p_lo));
   lo = add(lo, q);
@@ -149,32 +166,41 @@ BODE_HD bool cr_log(double x, const PowTables& T, double& lh, double& ll) {
 
 // exp(e * (lh + ll)), correctly rounded w.h.p.; `x` (= exp(lh + ll)) is only
 // used for the libm fallback near overflow/underflow.
+// libm pow for the rare out-of-range cases, kept out of line so its special-
+// case ladder does not bloat (and add registers to) the persistent loop
+#if defined(__CUDACC__)
+static __host__ __device__ __noinline__
+#else
+inline
+#endif
+double pow_fallback(double x, double e) { return pow(x, e); }
+
 BODE_HD double cr_exp_mul(double e, double lh, double ll, double x, const PowTables& T) {
   using namespace powimpl;
   // y = e * log(x) in double-double
   const double yh = mul(e, lh);
   const double yl = fma_(e, ll, fma_(e, lh, -yh));
-  if (!(yh < 700.0 && yh > -700.0)) return pow(x, e);
+  if (!(yh < 700.0 && yh > -700.0)) return pow_fallback(x, e);
   // exp(yh + yl) = 2^(kf/128) * exp(r2)
-  const double kd = rint(mul(yh, BODE_POW_INV_C));
+  const double kd = rint(mul(yh, BODE_PK(18)));
   const int64_t kf = (int64_t)kd;
   const int j = (int)(kf & 127);
   const int64_t ke = (kf - j) / 128;
   // r = y - kd*ln2/128 as rh + rl with |rl| <~ ulp(rh) + |yl|
-  const double t1 = fma_(-kd, BODE_POW_C_HI, yh);  // exact (kd*C_HI exact, Sterbenz)
-  const double pc = mul(kd, BODE_POW_C_LO);
-  const double pc_err = fma_(kd, BODE_POW_C_LO, -pc);
+  const double t1 = fma_(-kd, BODE_PK(16), yh);  // exact (kd*C_HI exact, Sterbenz)
+  const double pc = mul(kd, BODE_PK(17));
+  const double pc_err = fma_(kd, BODE_PK(17), -pc);
   double rh, ea;
   two_sum(t1, -pc, rh, ea);
   const double rl = add(sub(ea, pc_err), yl);
   // exp(rh + rl) - 1 - rh = a + rl*(1 + rh + a),  a = exp(rh) - 1 - rh
   //                        = rh^2 (1/2 + rh/6 + ... + rh^5/5040)
-  double c = 1.0 / 5040.0;
-  c = fma_(c, rh, 1.0 / 720.0);
-  c = fma_(c, rh, 1.0 / 120.0);
-  c = fma_(c, rh, 1.0 / 24.0);
-  c = fma_(c, rh, 1.0 / 6.0);
-  c = fma_(c, rh, 0.5);
+  double c = BODE_PK(8);
+  c = fma_(c, rh, BODE_PK(9));
+  c = fma_(c, rh, BODE_PK(10));
+  c = fma_(c, rh, BODE_PK(11));
+  c = fma_(c, rh, BODE_PK(12));
+  c = fma_(c, rh, BODE_PK(13));
   const double a = mul(mul(rh, rh), c);
   const double pp = add(a, fma_(rl, add(rh, a), rl));
   const double th = T.exp_tab[j][0], tl = T.exp_tab[j][1];
@@ -195,7 +221,7 @@ BODE_HD double cr_exp_mul(double e, double lh, double ll, double x, const PowTab
 // else -- and results near overflow/underflow -- goes to the libm pow.
 BODE_HD double cr_pow(double x, double e, const PowTables& T) {
   double lh, ll;
-  if (!(e == e) || e == INFINITY || e == -INFINITY || !cr_log(x, T, lh, ll)) return pow(x, e);
+  if (!(e == e) || e == INFINITY || e == -INFINITY || !cr_log(x, T, lh, ll)) return pow_fallback(x, e);
   return cr_exp_mul(e, lh, ll, x, T);
 }
 
