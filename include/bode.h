@@ -192,9 +192,11 @@ typedef struct bode_solve_args {
    * OR over shards of map[j]} (FSAL), 1 + S * max_j otherwise. */
   int64_t* max_iterations_out;
   uint8_t* refresh_map_out;
-  /* MLP dynamics only: BODE_MLP_AUTO (tensor cores when d == 64 and
-   * hidden % 64 == 0), BODE_MLP_CUDA_CORE (fp32 FMA) or BODE_MLP_TCGEN05
-   * (3xTF32 tcgen05.mma, fp32 accumulation in TMEM) */
+  /* MLP dynamics only: BODE_MLP_AUTO (= FUSED when d == 64 and hidden is a
+   * multiple of 32 up to 256), BODE_MLP_FUSED (one persistent tcgen05
+   * kernel per solve: stage vectors in TMEM, rows refilled from a queue),
+   * BODE_MLP_CUDA_CORE (lockstep, fp32 FMA) or BODE_MLP_TCGEN05 (lockstep,
+   * per-stage 3xTF32 tcgen05.mma kernels, fp32 accumulation in TMEM) */
   int32_t mlp_backend;
   int32_t _pad3;
   /* optional cudaEvent_t pair recorded on `stream` immediately before and
@@ -208,6 +210,7 @@ typedef struct bode_solve_args {
 #define BODE_MLP_AUTO 0
 #define BODE_MLP_CUDA_CORE 1
 #define BODE_MLP_TCGEN05 2
+#define BODE_MLP_FUSED 3
 
 int bode_abi_version(void);
 /* sizeof(bode_solve_args) as compiled, for binding layout checks */

@@ -513,8 +513,11 @@ static cudaError_t mlp_solve_m(const bode_solve_args* a, const SolveParams& P, c
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const bool tc_ok = mlp_tc_supported(D, H);
+  const bool fused_ok = tc_ok && mlp_fused_supported(D, H, a->method);
   if (a->mlp_backend == BODE_MLP_TCGEN05 && !tc_ok) return cudaErrorNotSupported;
+  if (a->mlp_backend == BODE_MLP_FUSED && !fused_ok) return cudaErrorNotSupported;
   const bool use_tc = tc_ok && a->mlp_backend != BODE_MLP_CUDA_CORE;
+  const bool use_fused = fused_ok && (a->mlp_backend == BODE_MLP_AUTO || a->mlp_backend == BODE_MLP_FUSED);
   if (use_tc && (e = mlp_tc_prep(W1, W2, H, W.wprep, st)) != cudaSuccess) return e;
   int64_t nl = use_tc ? 1 : 0;  // kernels launched
   const int max_tiles = (int)((n + 127) / 128);
@@ -565,6 +568,44 @@ static cudaError_t mlp_solve_m(const bode_solve_args* a, const SolveParams& P, c
   mlp_swap_kernel<<<1, 32, 0, st>>>(W);
   nl += heur ? 5 : 4;
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
+
+  if (use_fused) {  // one persistent launch runs every running instance to the end
+    MlpFusedArgs F;
+    F.H = H;
+    F.max_steps = a->max_steps;
+    F.act = W.act[0];  // running list after the init pass's copy + swap
+    F.count = W.cnt;
+    F.queue = P.queue;
+    F.y = W.y;
+    F.f0 = W.k;
+    F.t = W.t;
+    F.dt = W.dt;
+    F.wprep = W.wprep;
+    F.b1 = b1;
+    F.b2 = b2;
+    F.ctrl = P.ctrl;
+    F.t_end = a->t_end;
+    F.atol_v = a->atol_v;
+    F.rtol_v = a->rtol_v;
+    F.atol = a->atol;
+    F.rtol = a->rtol;
+    F.t_eval = a->t_eval;
+    F.t_eval_offsets = a->t_eval_offsets;
+    F.t_eval_len = a->t_eval_offsets ? 0 : a->t_eval_len;
+    F.ys = a->ys;
+    F.n_emitted = a->n_emitted;
+    F.n_steps = a->n_steps;
+    F.n_accepted = a->n_accepted;
+    F.final_dt = a->final_dt;
+    F.status = a->status;
+    F.max_n = P.max_n;
+    F.refresh = P.refresh;
+    if (P.ev_start) cudaEventRecord((cudaEvent_t)P.ev_start, st);
+    e = mlp_fused_launch<M>(F, st);
+    if (P.ev_stop) cudaEventRecord((cudaEvent_t)P.ev_stop, st);
+    if (launches) *launches += nl + 1;
+    return e;
+  }
 
   // lockstep iterations in bursts; each burst ends with one host read of the
   // running count (kernels of a drained batch exit immediately)

@@ -28,4 +28,40 @@ size_t mlp_tc_prep_bytes(int64_t H);
 cudaError_t mlp_tc_prep(const float* W1, const float* W2, int64_t H, float* out, cudaStream_t st);
 template <int M>
 cudaError_t mlp_tc_launch(const MlpTcArgs& A, int max_tiles, cudaStream_t st);
+
+// fused persistent integrator (bode_mlp_fused.cu): after the init pass, one
+// launch runs every running instance to termination
+struct MlpFusedArgs {
+  int H;
+  int64_t max_steps;
+  const int32_t* act;            // running instances after the init pass
+  const int32_t* count;          // their number (device)
+  unsigned long long* queue;     // position counter, zeroed
+  const double* y;               // (n, 64) initial state
+  const float* f0;               // (n, 64) f(t0, y0) from the init pass
+  const double* t;               // (n) t_start
+  const double* dt;              // (n) first dt
+  const float* wprep;            // weights pre-split by mlp_tc_prep
+  const float* b1;
+  const float* b2;
+  CtrlParams ctrl;
+  const double* t_end;
+  const double* atol_v;
+  const double* rtol_v;
+  double atol, rtol;
+  const double* t_eval;
+  const int64_t* t_eval_offsets;
+  int64_t t_eval_len;
+  double* ys;
+  int64_t* n_emitted;
+  int64_t* n_steps;
+  int64_t* n_accepted;
+  double* final_dt;
+  int64_t* status;
+  unsigned long long* max_n;
+  uint32_t* refresh;
+};
+bool mlp_fused_supported(int64_t D, int64_t H, int method);
+template <int M>
+cudaError_t mlp_fused_launch(const MlpFusedArgs& A, cudaStream_t st);
 }  // namespace bode

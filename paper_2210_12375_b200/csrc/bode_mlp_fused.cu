@@ -1,0 +1,519 @@
+// bode_mlp_fused.cu -- the neural-ODE solve as ONE persistent tcgen05 kernel.
+//
+// Each CTA (one per SM) owns a tile of 128 instances -- one per TMEM lane --
+// and runs the reference's whole per-instance loop (solver.py:208-322) for
+// them: stage inputs, the stage MLPs on the tensor cores, y_next / err, the
+// NumPy-order RMS norm, the PID update, accept/reject, dense output,
+// statuses.  When an instance terminates its row is refilled from a global
+// queue, so there is no lockstep iteration, no per-stage launch and no host
+// round trip; the lockstep path (bode_mlp.cu + bode_mlp_tc.cu) launches 9
+// kernels per iteration and re-reads every stage vector from HBM per stage.
+//
+// TMEM (512 columns x 128 lanes, fp32):
+//   columns 64 s .. 64 s + 63   stage derivative k_s of every row (s < 7)
+//   columns 448 .. 511          two 32-column GEMM1 chunk accumulators
+// Shared memory (~226 KB): y (fp64, [column][row]), the stage-input tile Y_s
+// as TF32 hi/lo core matrices (reused as the y_next buffer by the control
+// step), one hidden chunk H_c hi/lo, a 4-slot ring of 16 KB weight chunks
+// streamed with cp.async.bulk.
+//
+// Warp roles (288 threads):
+//   warps 0-3 (WG0)  row owners: refill, control; plus half of every stage
+//                    input and of every tanh epilogue (columns 0-31 / 0-15)
+//   warps 4-7 (WG1)  the other half of the stage inputs and epilogues
+//   warp 8           one elected thread issues every MMA and weight copy
+// Per stage s and hidden chunk c (3xTF32: hi*hi + hi*lo + lo*hi, fp32 acc):
+//   GEMM1  acc1[c&1] = Y_s W1_c^T        (M=128, N=32, K=64: 24 MMAs)
+//   epi    H_c = tanh(acc1 + b1) -> hi/lo (both groups, 16 columns each)
+//   GEMM2  k_s += H_c W2_c^T             (M=128, N=64, K=32: 12 MMAs)
+// GEMM1 of chunk c+2 is issued as soon as the epilogue of chunk c released
+// its accumulator, so the tensor core works while the epilogue runs.  The
+// MMA sequence (order of chunks, K steps and hi/lo terms) is the lockstep
+// tensor-core path's, so stage values are bit-identical to it; the fp64
+// stage combination, control and dense output replay the reference order.
+#include <cuda_runtime.h>
+
+#include "bode_mlp.cuh"
+#include "bode_tc.cuh"
+
+namespace bode {
+namespace fused {
+using namespace tc;
+
+constexpr int kNS = 4;            // weight ring slots
+constexpr int kWItem = 2 * kW1;   // one W1 or W2 chunk, hi | lo (16 KB)
+constexpr int kThreads = 288;
+constexpr int kMaxChunks = 8;     // H <= 256 (TMEM: 7 x 64 stage columns + 64)
+constexpr uint32_t kColAcc1 = 448;
+
+struct Smem {
+  double ys[kD][kRows];       // 64 KB  state y, [column][row]
+  uint8_t a[2][kATile];       // 64 KB  Y_s hi, lo  |  y_next (fp64 [column][row])
+  uint8_t h[2][kHTile];       // 32 KB  H_c hi, lo
+  uint8_t w[kNS][kWItem];     // 64 KB  weight ring
+  float b2[kD];
+  double hs[kRows];           // dt_used of the pending attempt, per row
+  int32_t act[kRows];         // row holds an instance
+  uint32_t wseq[2 * kMaxChunks];
+  uint64_t a_full, epidone, g1done[2], g2done, stage_done, wfull[kNS], wempty[kNS];
+  uint32_t tmem_base;
+};
+
+__device__ __forceinline__ void store_hilo(uint8_t* hi_base, uint8_t* lo_base, uint32_t off,
+                                           const float* x) {
+  float4 hi, lo;
+  hi.x = tf32_hi(x[0]), hi.y = tf32_hi(x[1]), hi.z = tf32_hi(x[2]), hi.w = tf32_hi(x[3]);
+  lo.x = x[0] - hi.x, lo.y = x[1] - hi.y, lo.z = x[2] - hi.z, lo.w = x[3] - hi.w;
+  *reinterpret_cast<float4*>(hi_base + off) = hi;
+  *reinterpret_cast<float4*>(lo_base + off) = lo;
+}
+
+template <int M>
+__global__ void __launch_bounds__(kThreads, 1) mlp_fused_kernel(const MlpFusedArgs A) {
+  using T = Tab<M>;
+  constexpr int S = T::S;
+  constexpr int S0 = T::FSAL ? 1 : 0;
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int wg = warp >> 2;                 // 0, 1: row groups; 2: MMA warp
+  const int row = (warp & 3) * 32 + lane;   // tile row == TMEM lane (groups 0, 1)
+  const int nc = A.H / kHc;
+
+  if (tid == 0) {
+    mbar_init(&sm.a_full, 256);
+    mbar_init(&sm.epidone, 256);
+    mbar_init(&sm.g1done[0], 1);
+    mbar_init(&sm.g1done[1], 1);
+    mbar_init(&sm.g2done, 1);
+    mbar_init(&sm.stage_done, 1);
+    for (int q = 0; q < kNS; q++) {
+      mbar_init(&sm.wfull[q], 1);
+      mbar_init(&sm.wempty[q], 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    // weight chunks in the order the MMA thread consumes them in one stage:
+    // W1_0, W1_1, then per chunk c: W2_c, W1_{c+2}
+    int p = 0;
+    sm.wseq[p++] = 0;
+    if (nc > 1) sm.wseq[p++] = kWChunk;
+    for (int c = 0; c < nc; c++) {
+      sm.wseq[p++] = (uint32_t)(c * kWChunk + 2 * kW1);
+      if (c + 2 < nc) sm.wseq[p++] = (uint32_t)((c + 2) * kWChunk);
+    }
+  }
+  for (int e = tid; e < kD; e += kThreads) sm.b2[e] = A.b2[e];
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+        smem_u32(&sm.tmem_base)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const uint32_t tmem = sm.tmem_base;
+  const uint32_t lrow = tmem + ((uint32_t)((warp & 3) * 32) << 16);  // this warp's lanes
+  const int count = *A.count;
+
+  // ---- row state (WG0 threads)
+  bool have = false;
+  int64_t idx = 0, nsteps = 0, nacc = 0, cursor = 0, m = 0;
+  double t = 0.0, dt = 0.0, t_end = 0.0, atol = 0.0, rtol = 0.0, n1 = 1.0, n2 = 1.0, h = 0.0;
+  bool trunc = false;
+  const double* te = nullptr;
+  double* yout = nullptr;
+  unsigned long long my_max = 0;
+  // ---- barrier phases
+  uint32_t ph_afull = 0, ph_epi = 0, ph_sd = 0, ph_g1[2] = {0u, 0u};
+  uint32_t g2_base = 0;            // G2 completions before the current stage
+  uint32_t wq_load = 0, wq_use = 0;  // MMA thread: weight items issued / consumed
+  const unsigned lt_mask = (1u << lane) - 1u;
+
+  while (true) {
+    // ================= refill free rows, dt_used of this attempt (WG0)
+    if (wg == 0) {
+      const unsigned need = __ballot_sync(0xffffffffu, !have);
+      bool got = false;
+      if (need) {
+        const int leader = __ffs(need) - 1;
+        unsigned long long base = 0;
+        if (lane == leader) base = atomicAdd(A.queue, (unsigned long long)__popc(need));
+        base = __shfl_sync(0xffffffffu, base, leader);
+        if (!have) {
+          const unsigned long long pos = base + __popc(need & lt_mask);
+          if (pos < (unsigned long long)count) {
+            const int64_t i = A.act[pos];
+            idx = i;
+            t = A.t[i];
+            dt = A.dt[i];
+            t_end = A.t_end[i];
+            atol = A.atol_v ? A.atol_v[i] : A.atol;
+            rtol = A.rtol_v ? A.rtol_v[i] : A.rtol;
+            cursor = A.n_emitted[i];
+            if (A.t_eval_offsets) {
+              const int64_t o = A.t_eval_offsets[i];
+              te = A.t_eval + o;
+              m = A.t_eval_offsets[i + 1] - o;
+              yout = A.ys ? A.ys + o * kD : nullptr;
+            } else {
+              te = A.t_eval;
+              m = A.t_eval_len;
+              yout = A.ys ? A.ys + i * A.t_eval_len * kD : nullptr;
+            }
+            n1 = 1.0;
+            n2 = 1.0;
+            nsteps = 0;
+            nacc = 0;
+            const double2* yp = reinterpret_cast<const double2*>(A.y + i * kD);
+#pragma unroll 8
+            for (int c = 0; c < kD / 2; c++) {
+              const double2 v = yp[c];
+              sm.ys[2 * c][row] = v.x;
+              sm.ys[2 * c + 1][row] = v.y;
+            }
+            have = got = true;
+          }
+        }
+      }
+      if (T::FSAL && __any_sync(0xffffffffu, got)) {  // k_0 = f0 of refilled rows
+#pragma unroll
+        for (int ch = 0; ch < 4; ch++) {
+          float v[16];
+          tmem_ld16(lrow + 16 * ch, v);
+          if (got) {
+            const float4* fp = reinterpret_cast<const float4*>(A.f0 + idx * kD + 16 * ch);
+#pragma unroll
+            for (int q = 0; q < 4; q++) {
+              const float4 f = fp[q];
+              v[4 * q] = f.x, v[4 * q + 1] = f.y, v[4 * q + 2] = f.z, v[4 * q + 3] = f.w;
+            }
+          }
+          tmem_st16(lrow + 16 * ch, v);
+        }
+        tmem_wait_st();
+      }
+      if (have) {
+        const double rem = ExactOps::sub(t_end, t);
+        trunc = fabs(dt) >= fabs(rem);
+        h = trunc ? rem : dt;
+      }
+      sm.hs[row] = h;
+      sm.act[row] = have;
+    }
+    fence_before();
+    const int any = __syncthreads_or(wg == 0 && have);
+    fence_after();
+    if (!any) break;
+
+    for (int s = S0; s < S; s++) {
+      if (wg < 2) {
+        // ============ stage input Y_s = y + h sum_{j<s} a_sj k_j (my 32 columns)
+        {
+          const bool live = sm.act[row] != 0;
+          const double hr = sm.hs[row];
+#pragma unroll
+          for (int ch = 0; ch < 2; ch++) {
+            const int c0 = 32 * wg + 16 * ch;
+            double acc[16];
+#pragma unroll
+            for (int e = 0; e < 16; e++) acc[e] = 0.0;
+#pragma unroll
+            for (int j = 0; j < S - 1; j++) {
+              if (j >= s) break;
+              float kv[16];
+              tmem_ld16(lrow + 64 * j + c0, kv);
+              const double aj = T::a(s, j);
+#pragma unroll
+              for (int e = 0; e < 16; e++)
+                acc[e] = j == 0 ? ExactOps::mul(aj, (double)kv[e])
+                                : ExactOps::mad(aj, (double)kv[e], acc[e]);
+            }
+            float x[16];
+#pragma unroll
+            for (int e = 0; e < 16; e++) {
+              const double y = sm.ys[c0 + e][row];
+              x[e] = live ? (float)(s > 0 ? ExactOps::mad(hr, acc[e], y) : y) : 0.0f;
+            }
+#pragma unroll
+            for (int q = 0; q < 4; q++)
+              store_hilo(sm.a[0], sm.a[1], cm_off(row, c0 + 4 * q, kD), x + 4 * q);
+          }
+        }
+        fence_async_smem();
+        mbar_arrive(&sm.a_full);
+        // ============ tanh epilogues of the hidden chunks
+        for (int c = 0; c < nc; c++) {
+          const int b = c & 1;
+          mbar_wait(&sm.g1done[b], ph_g1[b]);
+          ph_g1[b] ^= 1;
+          fence_after();
+          float v[16];
+          tmem_ld16(lrow + kColAcc1 + 32 * b + 16 * wg, v);
+          const float* b1 = A.b1 + c * kHc + 16 * wg;
+#pragma unroll
+          for (int j = 0; j < 16; j++) v[j] = tanhf(v[j] + __ldg(b1 + j));
+          if (c > 0) {  // GEMM2 of chunk c-1 has finished reading H
+            mbar_wait(&sm.g2done, (g2_base + c - 1) & 1);
+          }
+#pragma unroll
+          for (int q = 0; q < 4; q++)
+            store_hilo(sm.h[0], sm.h[1], cm_off(row, 16 * wg + 4 * q, kHc), v + 4 * q);
+          fence_async_smem();
+          fence_before();
+          mbar_arrive(&sm.epidone);
+        }
+        g2_base += nc;
+        mbar_wait(&sm.stage_done, ph_sd);
+        ph_sd ^= 1;
+        fence_after();
+        // ============ k_s = acc + b2 (the reference adds b2 after the sum)
+#pragma unroll
+        for (int hf = 0; hf < 2; hf++) {
+          const int c0 = 32 * wg + 16 * hf;
+          float v[16];
+          tmem_ld16(lrow + 64 * s + c0, v);
+#pragma unroll
+          for (int j = 0; j < 16; j++) v[j] += sm.b2[c0 + j];
+          tmem_st16(lrow + 64 * s + c0, v);
+        }
+        tmem_wait_st();
+      } else if (lane == 0) {
+        // ============ MMA issue (warp 8, one thread)
+        auto next_w = [&]() -> int {
+          while (wq_load <= wq_use + 2) {  // keep two chunks in flight
+            const int sl = (int)(wq_load % kNS);
+            if (wq_load >= (uint32_t)kNS) mbar_wait(&sm.wempty[sl], ((wq_load / kNS) - 1) & 1);
+            mbar_expect_tx(&sm.wfull[sl], kWItem);
+            bulk_g2s(sm.w[sl], (const char*)A.wprep + sm.wseq[wq_load % (2 * nc)], kWItem,
+                     &sm.wfull[sl]);
+            wq_load++;
+          }
+          const int sl = (int)(wq_use % kNS);
+          mbar_wait(&sm.wfull[sl], (wq_use / kNS) & 1);
+          wq_use++;
+          return sl;
+        };
+        const uint32_t a_hi = smem_u32(sm.a[0]), a_lo = smem_u32(sm.a[1]);
+        const uint32_t h_hi = smem_u32(sm.h[0]), h_lo = smem_u32(sm.h[1]);
+        auto gemm1 = [&](int c) {
+          const int sl = next_w();
+          const uint32_t wh = smem_u32(sm.w[sl]), wl = wh + kW1;
+          const uint32_t aa[3] = {a_hi, a_hi, a_lo}, bb[3] = {wh, wl, wh};
+          const uint32_t acc = tmem + kColAcc1 + 32 * (c & 1);
+#pragma unroll
+          for (int term = 0; term < 3; term++)
+#pragma unroll
+            for (int k = 0; k < kD / 8; k++)
+              mma_tf32(acc, smem_desc(aa[term] + 256 * k, 2048), smem_desc(bb[term] + 256 * k, 2048),
+                       idesc(kHc), (term | k) ? 1u : 0u);
+          mma_commit(&sm.g1done[c & 1]);
+          mma_commit(&sm.wempty[sl]);
+        };
+        auto gemm2 = [&](int c) {
+          const int sl = next_w();
+          const uint32_t wh = smem_u32(sm.w[sl]), wl = wh + kW2;
+          const uint32_t aa[3] = {h_hi, h_hi, h_lo}, bb[3] = {wh, wl, wh};
+          const uint32_t acc = tmem + 64 * s;
+#pragma unroll
+          for (int term = 0; term < 3; term++)
+#pragma unroll
+            for (int k = 0; k < kHc / 8; k++)
+              mma_tf32(acc, smem_desc(aa[term] + 256 * k, 1024), smem_desc(bb[term] + 256 * k, 1024),
+                       idesc(kD), (c | term | k) ? 1u : 0u);
+          mma_commit(&sm.g2done);
+          mma_commit(&sm.wempty[sl]);
+          if (c == nc - 1) mma_commit(&sm.stage_done);
+        };
+        mbar_wait(&sm.a_full, ph_afull);
+        ph_afull ^= 1;
+        fence_after();
+        gemm1(0);
+        if (nc > 1) gemm1(1);
+        for (int c = 0; c < nc; c++) {
+          mbar_wait(&sm.epidone, ph_epi);
+          ph_epi ^= 1;
+          fence_after();
+          gemm2(c);
+          if (c + 2 < nc) gemm1(c + 2);
+        }
+      }
+    }
+
+    // ================= control: the rest of step_once (WG0, one row each)
+    fence_before();
+    if (wg < 2) asm volatile("bar.sync 1, 256;" ::: "memory");
+    fence_after();
+    if (wg == 0) {
+      double* ynb = reinterpret_cast<double*>(sm.a[0]);  // y_next, [column][row]
+      double sq[8];
+#pragma unroll
+      for (int ch = 0; ch < 4; ch++) {
+        double sb[16], se[16];
+#pragma unroll
+        for (int j = 0; j < S; j++) {
+          float kv[16];
+          tmem_ld16(lrow + 64 * j + 16 * ch, kv);
+          const double bj = T::b(j), ej = T::e(j);
+#pragma unroll
+          for (int e = 0; e < 16; e++) {
+            const double kd = (double)kv[e];
+            sb[e] = j == 0 ? ExactOps::mul(bj, kd) : ExactOps::mad(bj, kd, sb[e]);
+            se[e] = j == 0 ? ExactOps::mul(ej, kd) : ExactOps::mad(ej, kd, se[e]);
+          }
+        }
+#pragma unroll
+        for (int e = 0; e < 16; e++) {
+          const int c = 16 * ch + e;
+          const double y = sm.ys[c][row];
+          const double yn = ExactOps::mad(h, sb[e], y);
+          const double err = ExactOps::mul(h, se[e]);
+          const double scale = ExactOps::mad(rtol, np_max(fabs(y), fabs(yn)), atol);
+          const double r = ddiv(err, scale);
+          const double q = ExactOps::mul(r, r);
+          sq[c & 7] = c < 8 ? q : ExactOps::add(sq[c & 7], q);  // NumPy pairwise, n = 64
+          ynb[c * kRows + row] = yn;
+        }
+      }
+      double nrm = ExactOps::add(ExactOps::add(ExactOps::add(sq[0], sq[1]), ExactOps::add(sq[2], sq[3])),
+                                 ExactOps::add(ExactOps::add(sq[4], sq[5]), ExactOps::add(sq[6], sq[7])));
+      nrm = dsqrt(ddiv(nrm, (double)kD));
+      if (!isfinite(nrm)) nrm = __longlong_as_double(0x7ff0000000000000LL);
+      bool accept = false;
+      double dtn = h;
+      if (have) accept = adapt(A.ctrl, nrm, n1, n2, dtn);
+      // dense output for every crossed point (solver.py:284-322), pre-commit state
+      bool pend = have && accept && cursor < m && h != 0.0;
+      while (__any_sync(0xffffffffu, pend)) {
+        double th = 0.0;
+        if (pend) {
+          th = ddiv(ExactOps::sub(te[cursor], t), h);
+          if (!(th <= 1.0)) pend = false;
+          th = np_max(th, 0.0);
+        }
+        if (!__any_sync(0xffffffffu, pend)) break;
+        double w[S];
+#pragma unroll
+        for (int q = 0; q < S; q++) {
+          double v = T::w(q, T::NI - 1);
+#pragma unroll
+          for (int r = T::NI - 2; r >= 0; r--) v = ExactOps::mad(v, th, T::w(q, r));
+          w[q] = ExactOps::mul(v, th);
+        }
+#pragma unroll
+        for (int ch = 0; ch < 4; ch++) {
+          double sa[16];
+#pragma unroll
+          for (int j = 0; j < S; j++) {
+            float kv[16];
+            tmem_ld16(lrow + 64 * j + 16 * ch, kv);
+#pragma unroll
+            for (int e = 0; e < 16; e++)
+              sa[e] = j == 0 ? ExactOps::mul(w[0], (double)kv[e])
+                             : ExactOps::mad(w[j], (double)kv[e], sa[e]);
+          }
+          if (pend && yout) {
+#pragma unroll
+            for (int e = 0; e < 16; e++)
+              yout[cursor * kD + 16 * ch + e] = ExactOps::mad(h, sa[e], sm.ys[16 * ch + e][row]);
+          }
+        }
+        if (pend) {
+          cursor++;
+          pend = cursor < m;
+        }
+      }
+      // commit: y <- y_next, FSAL k_0 <- k_{S-1} on accepted rows
+      if (have && accept) {
+#pragma unroll 8
+        for (int c = 0; c < kD; c++) sm.ys[c][row] = ynb[c * kRows + row];
+      }
+      if (T::FSAL && __any_sync(0xffffffffu, have && accept)) {
+#pragma unroll
+        for (int ch = 0; ch < 4; ch++) {
+          float k0[16], kl[16];
+          tmem_ld16(lrow + 16 * ch, k0);
+          tmem_ld16(lrow + 64 * (S - 1) + 16 * ch, kl);
+          if (have && accept) {
+#pragma unroll
+            for (int e = 0; e < 16; e++) k0[e] = kl[e];
+          }
+          tmem_st16(lrow + 16 * ch, k0);
+        }
+        tmem_wait_st();
+      }
+      if (have) {
+        int status = BODE_RUNNING;
+        if (accept) {
+          nacc++;
+          t = trunc ? t_end : ExactOps::add(t, h);
+          if (trunc) status = BODE_SUCCESS;
+        }
+        nsteps++;
+        dt = dtn;
+        if (status == BODE_RUNNING && ExactOps::add(t, dt) == t) status = BODE_STEP_UNDERFLOW;
+        if (status == BODE_RUNNING && nsteps >= A.max_steps) status = BODE_MAX_STEPS_EXCEEDED;
+        if (!accept && status == BODE_RUNNING) {
+          const uint64_t bit = (uint64_t)nsteps;  // rejected at iteration nsteps-1
+          atomicOr(&A.refresh[bit >> 5], 1u << (bit & 31));
+        }
+        if (status != BODE_RUNNING) {
+          A.n_steps[idx] = nsteps;
+          A.n_accepted[idx] = nacc;
+          A.n_emitted[idx] = cursor;
+          A.final_dt[idx] = dt;
+          A.status[idx] = status;
+          if ((unsigned long long)nsteps > my_max) my_max = (unsigned long long)nsteps;
+          have = false;
+        }
+      }
+    }
+  }
+
+  // ---- teardown: no bulk copy may still be landing in this CTA's smem
+  if (warp == 8 && lane == 0) {
+    for (uint32_t q = wq_use; q < wq_load; q++) mbar_wait(&sm.wfull[q % kNS], (q / kNS) & 1);
+  }
+  if (wg == 0) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const unsigned long long v = __shfl_xor_sync(0xffffffffu, my_max, o);
+      my_max = v > my_max ? v : my_max;
+    }
+    if (lane == 0 && my_max) atomicMax(A.max_n, my_max);
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(sm.tmem_base));
+}
+
+}  // namespace fused
+
+bool mlp_fused_supported(int64_t D, int64_t H, int method) {
+  (void)method;
+  return D == tc::kD && H % tc::kHc == 0 && H / tc::kHc <= fused::kMaxChunks;
+}
+
+template <int M>
+cudaError_t mlp_fused_launch(const MlpFusedArgs& A, cudaStream_t st) {
+  const size_t smem = sizeof(fused::Smem);
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(fused::mlp_fused_kernel<M>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  fused::mlp_fused_kernel<M><<<sms, fused::kThreads, smem, st>>>(A);
+  return cudaGetLastError();
+}
+
+template cudaError_t mlp_fused_launch<BODE_METHOD_DOPRI5>(const MlpFusedArgs&, cudaStream_t);
+template cudaError_t mlp_fused_launch<BODE_METHOD_TSIT5>(const MlpFusedArgs&, cudaStream_t);
+template cudaError_t mlp_fused_launch<BODE_METHOD_HEUN>(const MlpFusedArgs&, cudaStream_t);
+
+}  // namespace bode

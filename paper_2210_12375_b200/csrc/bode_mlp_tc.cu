@@ -22,113 +22,10 @@
 #include <cuda_runtime.h>
 
 #include "bode_mlp.cuh"
+#include "bode_tc.cuh"
 
 namespace bode {
 namespace tc {
-
-constexpr int kD = 64;     // state width handled by this kernel
-constexpr int kHc = 32;    // hidden units per chunk
-constexpr int kRows = 128; // instances per tile (UMMA M)
-constexpr int kATile = kRows * kD * 4;   // 32 KB: 128 x 64 fp32
-constexpr int kHTile = kRows * kHc * 4;  // 16 KB: 128 x 32 fp32
-constexpr int kW1 = kHc * kD * 4;        //  8 KB: 32 x 64 fp32
-constexpr int kW2 = kD * kHc * 4;        //  8 KB: 64 x 32 fp32
-constexpr int kWChunk = 2 * kW1 + 2 * kW2;  // pre-split chunk in global
-
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return (uint32_t)__cvta_generic_to_shared(p);
-}
-// byte offset of (r, k) in a K-major, no-swizzle core-matrix tile with
-// `kcols` K-elements per row: 8-row x 16-byte core matrices, K-chunks 128 B
-// apart (LBO), 8-row groups kcols/4*128 B apart (SBO)
-__host__ __device__ __forceinline__ uint32_t cm_off(int r, int k, int kcols) {
-  return (uint32_t)((r >> 3) * (kcols / 4) * 128 + (k >> 2) * 128 + (r & 7) * 16 + (k & 3) * 4);
-}
-__device__ __forceinline__ uint64_t smem_desc(uint32_t addr, uint32_t sbo) {
-  uint64_t d = (uint64_t)((addr >> 4) & 0x3FFF);
-  d |= (uint64_t)((128u >> 4) & 0x3FFF) << 16;  // LBO
-  d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;   // SBO
-  d |= (uint64_t)1 << 46;                       // descriptor version (Blackwell)
-  return d;                                     // base offset 0, SWIZZLE_NONE
-}
-// kind::tf32, fp32 accumulate, A/B K-major, M = 128
-constexpr uint32_t idesc(int N) {
-  return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(N >> 3) << 17) | ((128u >> 4) << 24);
-}
-
-__device__ __forceinline__ float tf32_hi(float x) {
-  uint32_t r;
-  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
-  return __uint_as_float(r);
-}
-__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count));
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)),
-               "r"(bytes));
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t phase) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-      "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(b)),
-      "r"(phase)
-      : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* b) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
-          "r"(smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(b))
-      : "memory");
-}
-__device__ __forceinline__ void mma_tf32(uint32_t tmem, uint64_t a, uint64_t b, uint32_t id,
-                                         uint32_t acc) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem),
-      "l"(a), "l"(b), "r"(id), "r"(acc));
-}
-__device__ __forceinline__ void mma_commit(uint64_t* b) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                   smem_u32(b))
-               : "memory");
-}
-__device__ __forceinline__ void fence_before() {
-  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-}
-__device__ __forceinline__ void fence_after() {
-  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-}
-__device__ __forceinline__ void fence_async_smem() {
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-}
-__device__ __forceinline__ void group_sync(int id) {  // one 128-thread warp group
-  asm volatile("bar.sync %0, 128;" ::"r"(id) : "memory");
-}
-
-#define BODE_R8(i) "=r"(r[i]), "=r"(r[i + 1]), "=r"(r[i + 2]), "=r"(r[i + 3]), \
-                   "=r"(r[i + 4]), "=r"(r[i + 5]), "=r"(r[i + 6]), "=r"(r[i + 7])
-// N consecutive fp32 TMEM columns of this thread's lane (32x32b shape)
-__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
-  uint32_t r[32];
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
-      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-      : BODE_R8(0), BODE_R8(8), BODE_R8(16), BODE_R8(24)
-      : "r"(taddr));
-  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-  for (int j = 0; j < 32; j++) v[j] = __uint_as_float(r[j]);
-}
-#undef BODE_R8
 
 struct Smem {
   uint8_t a[2][2][kATile];  // [buffer][hi, lo]

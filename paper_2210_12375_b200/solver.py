@@ -29,8 +29,9 @@ __all__ = ["DEFAULT_MAX_STEPS", "SolveStatus", "IvpBatch", "SolveStats", "Soluti
            "solve", "solve_device", "pinned", "host_empty"]
 
 DEFAULT_MAX_STEPS = 10_000
-# MLP stage evaluation: tcgen05 3xTF32 (auto when d == 64) or CUDA-core fp32
-MLP_BACKENDS = {"auto": 0, "cuda_core": 1, "tcgen05": 2}
+# MLP path: fused persistent tcgen05 kernel (auto when d == 64), lockstep
+# per-stage tcgen05 3xTF32 kernels, or lockstep CUDA-core fp32
+MLP_BACKENDS = {"auto": 0, "cuda_core": 1, "tcgen05": 2, "fused": 3}
 
 
 # host arrays up to this size are page-locked (DMA at ~50 GB/s instead of a
