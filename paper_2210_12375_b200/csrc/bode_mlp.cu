@@ -600,8 +600,31 @@ static cudaError_t mlp_solve_m(const bode_solve_args* a, const SolveParams& P, c
     F.status = a->status;
     F.max_n = P.max_n;
     F.refresh = P.refresh;
+    F.prof = nullptr;
+#ifdef BODE_FUSED_PROF
+    static unsigned long long* prof_buf = nullptr;
+    if (!prof_buf) cudaMalloc(&prof_buf, 148 * 3 * 32 * 8);
+    cudaMemsetAsync(prof_buf, 0, 148 * 3 * 32 * 8, st);
+    F.prof = prof_buf;
+#endif
     if (P.ev_start) cudaEventRecord((cudaEvent_t)P.ev_start, st);
     e = mlp_fused_launch<M>(F, st);
+#ifdef BODE_FUSED_PROF
+    {
+      unsigned long long h[148 * 3 * 32];
+      cudaMemcpyAsync(h, prof_buf, sizeof(h), cudaMemcpyDeviceToHost, st);
+      cudaStreamSynchronize(st);
+      for (int v = 0; v < 3; v++) {
+        double acc[32] = {0};
+        for (int b = 0; b < 148; b++)
+          for (int k = 0; k < 32; k++) acc[k] += h[(b * 3 + v) * 32 + k] / 148.0;
+        fprintf(stderr, "fused prof view %d:", v);
+        for (int k = 0; k < 32; k++)
+          if (acc[k] != 0) fprintf(stderr, " [%d]=%.0f", k, acc[k]);
+        fprintf(stderr, "\n");
+      }
+    }
+#endif
     if (P.ev_stop) cudaEventRecord((cudaEvent_t)P.ev_stop, st);
     if (launches) *launches += nl + 1;
     return e;

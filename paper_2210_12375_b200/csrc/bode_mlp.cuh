@@ -60,6 +60,7 @@ struct MlpFusedArgs {
   int64_t* status;
   unsigned long long* max_n;
   uint32_t* refresh;
+  unsigned long long* prof;      // debug builds (-DBODE_FUSED_PROF): (grid*3, 32) cycles
 };
 bool mlp_fused_supported(int64_t D, int64_t H, int method);
 template <int M>

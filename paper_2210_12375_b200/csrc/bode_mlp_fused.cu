@@ -40,22 +40,43 @@ namespace bode {
 namespace fused {
 using namespace tc;
 
+// -DBODE_FUSED_PROF: per-CTA cycle counters of each phase (debug builds)
+#ifdef BODE_FUSED_PROF
+#define PROF_DECL unsigned long long pf[32] = {0}; long long pt = clock64();
+#define PROF_MARK(k) { const long long now = clock64(); pf[k] += now - pt; pt = now; }
+#else
+#define PROF_DECL
+#define PROF_MARK(k)
+#endif
+
 constexpr int kNS = 4;            // weight ring slots
 constexpr int kWItem = 2 * kW1;   // one W1 or W2 chunk, hi | lo (16 KB)
-constexpr int kThreads = 288;
+constexpr int kThreads = 320;
 constexpr int kMaxChunks = 8;     // H <= 256 (TMEM: 7 x 64 stage columns + 64)
-constexpr uint32_t kColAcc1 = 448;
+constexpr int kItemsMax = 16;     // weight items per stage (H / 16)
+
+// GEMM1 unit width of stage s: stage vectors k_0..k_s occupy TMEM columns
+// [0, 64 (s+1)); the two GEMM1 accumulators take the top 2 W columns, and a
+// wider unit means fewer, more efficient MMAs (measured on B200: a
+// kind::tf32 M=128 MMA costs 46 / 54 / 66 cycles at N = 32 / 64 / 128 --
+// smem operand bandwidth -- for 1x / 2x / 4x the work).
+__host__ __device__ __forceinline__ int unit_width(int s, int H) {
+  const int free_cols = 512 - 64 * (s + 1);
+  if (free_cols >= 256 && H % 128 == 0) return 128;
+  if (free_cols >= 128 && H % 64 == 0) return 64;
+  return 32;
+}
 
 struct Smem {
   double ys[kD][kRows];       // 64 KB  state y, [column][row]
   uint8_t a[2][kATile];       // 64 KB  Y_s hi, lo  |  y_next (fp64 [column][row])
-  uint8_t h[2][kHTile];       // 32 KB  H_c hi, lo
+  uint8_t h[2][2][kHTile / 2]; // 32 KB  [group][hi, lo] 16-column halves of H_c
   uint8_t w[kNS][kWItem];     // 64 KB  weight ring
   float b2[kD];
   double hs[kRows];           // dt_used of the pending attempt, per row
   int32_t act[kRows];         // row holds an instance
-  uint32_t wseq[2 * kMaxChunks];
-  uint64_t a_full, epidone, g1done[2], g2done, stage_done, wfull[kNS], wempty[kNS];
+  uint32_t seq[7][kItemsMax];  // weight item byte offsets, per stage, in consumption order
+  uint64_t a_full, epidone[2], g1done[2], g2done[2], stage_done, wfull[kNS], wempty[kNS];
   uint32_t tmem_base;
 };
 
@@ -82,24 +103,35 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_fused_kernel(const MlpFusedAr
 
   if (tid == 0) {
     mbar_init(&sm.a_full, 256);
-    mbar_init(&sm.epidone, 256);
+    mbar_init(&sm.epidone[0], 128);
+    mbar_init(&sm.epidone[1], 128);
     mbar_init(&sm.g1done[0], 1);
     mbar_init(&sm.g1done[1], 1);
-    mbar_init(&sm.g2done, 1);
+    mbar_init(&sm.g2done[0], 1);
+    mbar_init(&sm.g2done[1], 1);
     mbar_init(&sm.stage_done, 1);
     for (int q = 0; q < kNS; q++) {
       mbar_init(&sm.wfull[q], 1);
       mbar_init(&sm.wempty[q], 1);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    // weight chunks in the order the MMA thread consumes them in one stage:
-    // W1_0, W1_1, then per chunk c: W2_c, W1_{c+2}
-    int p = 0;
-    sm.wseq[p++] = 0;
-    if (nc > 1) sm.wseq[p++] = kWChunk;
-    for (int c = 0; c < nc; c++) {
-      sm.wseq[p++] = (uint32_t)(c * kWChunk + 2 * kW1);
-      if (c + 2 < nc) sm.wseq[p++] = (uint32_t)((c + 2) * kWChunk);
+    // weight items in the order the MMA thread consumes them in stage s:
+    // the K slices of GEMM1 units 0 and 1, then per 32-column hidden chunk q
+    // the W2 chunk of q and, after a unit's last chunk, unit u+2's slices
+    for (int st = S0; st < S; st++) {
+      const int Wd = unit_width(st, A.H), nu = A.H / Wd, spu = Wd / kHc;
+      int p = 0;
+      auto g1items = [&](int u) {
+        for (int q = 0; q < spu; q++)  // spu K slices of 16 KB per unit
+          sm.seq[st][p++] = Wd == kHc ? (uint32_t)(u * kWChunk)
+                                      : (uint32_t)(mlp_w1_items_offset(A.H, Wd) + (size_t)(u * spu + q) * 16384);
+      };
+      g1items(0);
+      if (nu > 1) g1items(1);
+      for (int q = 0; q < nc; q++) {
+        sm.seq[st][p++] = (uint32_t)(q * kWChunk + 2 * kW1);
+        if (q % spu == spu - 1 && q / spu + 2 < nu) g1items(q / spu + 2);
+      }
     }
   }
   for (int e = tid; e < kD; e += kThreads) sm.b2[e] = A.b2[e];
@@ -128,6 +160,7 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_fused_kernel(const MlpFusedAr
   uint32_t g2_base = 0;            // G2 completions before the current stage
   uint32_t wq_load = 0, wq_use = 0;  // MMA thread: weight items issued / consumed
   const unsigned lt_mask = (1u << lane) - 1u;
+  PROF_DECL
 
   while (true) {
     // ================= refill free rows, dt_used of this attempt (WG0)
@@ -200,9 +233,11 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_fused_kernel(const MlpFusedAr
       sm.hs[row] = h;
       sm.act[row] = have;
     }
+    PROF_MARK(0)
     fence_before();
     const int any = __syncthreads_or(wg == 0 && have);
     fence_after();
+    PROF_MARK(1)
     if (!any) break;
 
     for (int s = S0; s < S; s++) {
@@ -241,31 +276,41 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_fused_kernel(const MlpFusedAr
         }
         fence_async_smem();
         mbar_arrive(&sm.a_full);
+        PROF_MARK(2)
         // ============ tanh epilogues of the hidden chunks
+        const int Wd = unit_width(s, A.H), spu = Wd / kHc;
+        const uint32_t acc1_base = 512 - 2 * Wd;
         for (int c = 0; c < nc; c++) {
-          const int b = c & 1;
-          mbar_wait(&sm.g1done[b], ph_g1[b]);
-          ph_g1[b] ^= 1;
-          fence_after();
+          const int u = c / spu, b = u & 1;
+          if (c % spu == 0) {
+            mbar_wait(&sm.g1done[b], ph_g1[b]);
+            ph_g1[b] ^= 1;
+            fence_after();
+          }
+          PROF_MARK(3)
           float v[16];
-          tmem_ld16(lrow + kColAcc1 + 32 * b + 16 * wg, v);
+          tmem_ld16(lrow + acc1_base + Wd * b + 32 * (c % spu) + 16 * wg, v);
           const float* b1 = A.b1 + c * kHc + 16 * wg;
 #pragma unroll
           for (int j = 0; j < 16; j++) v[j] = tanhf(v[j] + __ldg(b1 + j));
+          PROF_MARK(4)
           if (c > 0) {  // GEMM2 of chunk c-1 has finished reading H
-            mbar_wait(&sm.g2done, (g2_base + c - 1) & 1);
+            mbar_wait(&sm.g2done[wg], (g2_base + c - 1) & 1);
           }
+          PROF_MARK(5)
 #pragma unroll
           for (int q = 0; q < 4; q++)
-            store_hilo(sm.h[0], sm.h[1], cm_off(row, 16 * wg + 4 * q, kHc), v + 4 * q);
+            store_hilo(sm.h[wg][0], sm.h[wg][1], cm_off(row, 4 * q, 16), v + 4 * q);
           fence_async_smem();
           fence_before();
-          mbar_arrive(&sm.epidone);
+          mbar_arrive(&sm.epidone[wg]);
+          PROF_MARK(6)
         }
         g2_base += nc;
         mbar_wait(&sm.stage_done, ph_sd);
         ph_sd ^= 1;
         fence_after();
+        PROF_MARK(7)
         // ============ k_s = acc + b2 (the reference adds b2 after the sum)
 #pragma unroll
         for (int hf = 0; hf < 2; hf++) {
@@ -277,72 +322,121 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_fused_kernel(const MlpFusedAr
           tmem_st16(lrow + 64 * s + c0, v);
         }
         tmem_wait_st();
-      } else if (lane == 0) {
-        // ============ MMA issue (warp 8, one thread)
-        auto next_w = [&]() -> int {
-          while (wq_load <= wq_use + 2) {  // keep two chunks in flight
-            const int sl = (int)(wq_load % kNS);
-            if (wq_load >= (uint32_t)kNS) mbar_wait(&sm.wempty[sl], ((wq_load / kNS) - 1) & 1);
-            mbar_expect_tx(&sm.wfull[sl], kWItem);
-            bulk_g2s(sm.w[sl], (const char*)A.wprep + sm.wseq[wq_load % (2 * nc)], kWItem,
-                     &sm.wfull[sl]);
-            wq_load++;
-          }
-          const int sl = (int)(wq_use % kNS);
+        PROF_MARK(8)
+      } else if (warp == 8) {
+        // ============ MMA issue.  The whole warp runs this code so descriptors
+        // and TMEM addresses stay in uniform registers; one elected lane
+        // issues each MMA / commit.  Weights arrive from the loader warp.
+        auto next_w = [&]() -> uint32_t {
+          const uint32_t sl = wq_use % kNS;
+          PROF_MARK(20)
           mbar_wait(&sm.wfull[sl], (wq_use / kNS) & 1);
+          PROF_MARK(18)
           wq_use++;
           return sl;
         };
-        const uint32_t a_hi = smem_u32(sm.a[0]), a_lo = smem_u32(sm.a[1]);
-        const uint32_t h_hi = smem_u32(sm.h[0]), h_lo = smem_u32(sm.h[1]);
-        auto gemm1 = [&](int c) {
-          const int sl = next_w();
-          const uint32_t wh = smem_u32(sm.w[sl]), wl = wh + kW1;
-          const uint32_t aa[3] = {a_hi, a_hi, a_lo}, bb[3] = {wh, wl, wh};
-          const uint32_t acc = tmem + kColAcc1 + 32 * (c & 1);
-#pragma unroll
-          for (int term = 0; term < 3; term++)
-#pragma unroll
-            for (int k = 0; k < kD / 8; k++)
-              mma_tf32(acc, smem_desc(aa[term] + 256 * k, 2048), smem_desc(bb[term] + 256 * k, 2048),
-                       idesc(kHc), (term | k) ? 1u : 0u);
-          mma_commit(&sm.g1done[c & 1]);
-          mma_commit(&sm.wempty[sl]);
+        // descriptor of K step k = descriptor of the tile + 16 k (256 B >> 4)
+        const uint64_t dA_hi = smem_desc(smem_u32(sm.a[0]), 2048);
+        const uint64_t dA_lo = smem_desc(smem_u32(sm.a[1]), 2048);
+        const uint64_t dW2 = smem_desc(smem_u32(sm.w[0]), 1024);
+        const int Wd = unit_width(s, A.H), spu = Wd / kHc, nu = A.H / Wd;
+        const int KS = 2048 / Wd;                     // K per 16 KB item
+        const uint32_t acc1_base = 512 - 2 * Wd;
+        // GEMM1 unit u: acc1[u&1] (N = Wd) = Y_s W1[u Wd .. u Wd + Wd)^T,
+        // K-step major, the three 3xTF32 products inner
+        auto gemm1 = [&](int u) {
+          const uint32_t acc = tmem + acc1_base + Wd * (u & 1);
+          for (int q = 0; q < spu; q++) {
+            const uint32_t sl = next_w();
+            const uint64_t wdesc = smem_desc(smem_u32(sm.w[sl]), (uint32_t)(KS * 32));
+            const uint64_t wh = wdesc, wl = wdesc + (8192 >> 4);
+            PROF_MARK(20)
+            if (elect_one()) {
+              fence_after();
+              for (int kl = 0; kl < KS / 8; kl++) {
+                const int k = q * (KS / 8) + kl;
+                mma_tf32(acc, dA_hi + 16 * k, wh + 16 * kl, idesc(Wd), k ? 1u : 0u);
+                mma_tf32(acc, dA_hi + 16 * k, wl + 16 * kl, idesc(Wd), 1u);
+                mma_tf32(acc, dA_lo + 16 * k, wh + 16 * kl, idesc(Wd), 1u);
+              }
+              mma_commit(&sm.wempty[sl]);
+              if (q == spu - 1) mma_commit(&sm.g1done[u & 1]);
+            }
+            __syncwarp();
+            PROF_MARK(22)
+          }
         };
-        auto gemm2 = [&](int c) {
-          const int sl = next_w();
-          const uint32_t wh = smem_u32(sm.w[sl]), wl = wh + kW2;
-          const uint32_t aa[3] = {h_hi, h_hi, h_lo}, bb[3] = {wh, wl, wh};
+        // GEMM2 of hidden chunk c, half g (K steps 2g, 2g+1): A = group g's
+        // 16-column H buffer, so each group refills its buffer as soon as its
+        // own half has been read
+        auto gemm2_half = [&](int c, int g, uint32_t sl) {
+          const uint64_t wh = dW2 + (uint64_t)((sl * kWItem) >> 4), wl = wh + (kW2 >> 4);
+          const uint64_t hh = smem_desc(smem_u32(sm.h[g][0]), 512), hl = smem_desc(smem_u32(sm.h[g][1]), 512);
           const uint32_t acc = tmem + 64 * s;
+          PROF_MARK(20)
+          if (elect_one()) {
+            fence_after();
 #pragma unroll
-          for (int term = 0; term < 3; term++)
-#pragma unroll
-            for (int k = 0; k < kHc / 8; k++)
-              mma_tf32(acc, smem_desc(aa[term] + 256 * k, 1024), smem_desc(bb[term] + 256 * k, 1024),
-                       idesc(kD), (c | term | k) ? 1u : 0u);
-          mma_commit(&sm.g2done);
-          mma_commit(&sm.wempty[sl]);
-          if (c == nc - 1) mma_commit(&sm.stage_done);
+            for (int kk = 0; kk < 2; kk++) {
+              const int k = 2 * g + kk;
+              mma_tf32(acc, hh + 16 * kk, wh + 16 * k, idesc(kD), (c | k) ? 1u : 0u);
+              mma_tf32(acc, hh + 16 * kk, wl + 16 * k, idesc(kD), 1u);
+              mma_tf32(acc, hl + 16 * kk, wh + 16 * k, idesc(kD), 1u);
+            }
+            mma_commit(&sm.g2done[g]);
+            if (g == 1) {
+              mma_commit(&sm.wempty[sl]);
+              if (c == nc - 1) mma_commit(&sm.stage_done);
+            }
+          }
+          __syncwarp();
+          PROF_MARK(23)
         };
+        PROF_MARK(20)
         mbar_wait(&sm.a_full, ph_afull);
         ph_afull ^= 1;
         fence_after();
+        PROF_MARK(16)
         gemm1(0);
-        if (nc > 1) gemm1(1);
+        if (nu > 1) gemm1(1);
         for (int c = 0; c < nc; c++) {
-          mbar_wait(&sm.epidone, ph_epi);
+          const uint32_t sl = next_w();
+#pragma unroll
+          for (int g = 0; g < 2; g++) {
+            PROF_MARK(20)
+            mbar_wait(&sm.epidone[g], ph_epi);
+            fence_after();
+            PROF_MARK(17)
+            gemm2_half(c, g, sl);
+          }
           ph_epi ^= 1;
-          fence_after();
-          gemm2(c);
-          if (c + 2 < nc) gemm1(c + 2);
+          if (c % spu == spu - 1 && c / spu + 2 < nu) gemm1(c / spu + 2);
+        }
+        PROF_MARK(20)
+      } else if (s == S0) {
+        // ============ weight loader (warp 9): every item of this step, in
+        // consumption order, as ring slots free up
+        const uint32_t per = (uint32_t)(A.H / 16);  // items per stage
+        const uint32_t n_items = per * (uint32_t)(S - S0);
+        for (uint32_t i = 0; i < n_items; i++, wq_load++) {
+          const uint32_t sl = wq_load % kNS;
+          if (wq_load >= (uint32_t)kNS) mbar_wait(&sm.wempty[sl], ((wq_load / kNS) - 1) & 1);
+          if (elect_one()) {
+            mbar_expect_tx(&sm.wfull[sl], kWItem);
+            bulk_g2s(sm.w[sl], (const char*)A.wprep + sm.seq[S0 + i / per][i % per], kWItem,
+                     &sm.wfull[sl]);
+          }
+          __syncwarp();
         }
       }
     }
 
     // ================= control: the rest of step_once (WG0, one row each)
     fence_before();
+    PROF_MARK(21)
     if (wg < 2) asm volatile("bar.sync 1, 256;" ::: "memory");
     fence_after();
+    PROF_MARK(9)
     if (wg == 0) {
       double* ynb = reinterpret_cast<double*>(sm.a[0]);  // y_next, [column][row]
       double sq[8];
@@ -467,12 +561,20 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_fused_kernel(const MlpFusedAr
         }
       }
     }
+#ifdef BODE_FUSED_PROF
+    PROF_MARK(10)
+    pf[30] += 1;
+#endif
   }
+#ifdef BODE_FUSED_PROF
+  if (A.prof && (tid == 0 || tid == 128 || tid == 256)) {
+    for (int k = 0; k < 32; k++) A.prof[(blockIdx.x * 3 + (tid >> 7)) * 32 + k] = pf[k];
+  }
+#endif
 
   // ---- teardown: no bulk copy may still be landing in this CTA's smem
-  if (warp == 8 && lane == 0) {
-    for (uint32_t q = wq_use; q < wq_load; q++) mbar_wait(&sm.wfull[q % kNS], (q / kNS) & 1);
-  }
+  // (the loader issues exactly the items the MMA warp consumes, so no bulk
+  // copy is in flight here)
   if (wg == 0) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {

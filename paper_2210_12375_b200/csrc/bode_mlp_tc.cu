@@ -60,6 +60,24 @@ __global__ void mlp_tc_prep_kernel(const float* __restrict__ W1, const float* __
       *(float*)(base + 2 * kW1 + kW2 + cm_off(o, j, kHc)) = w - hi;
     }
   }
+  // W1 again as 16 KB items for wide GEMM1 units (bode_mlp_fused.cu): for
+  // unit width Wd in {64, 128}, item (unit u, K slice q) holds rows
+  // [u Wd, u Wd + Wd) x K [q KS, q KS + KS), KS = 2048 / Wd, hi then lo
+  const int tot1 = H * kD;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < 2 * tot1; e += gridDim.x * blockDim.x) {
+    const int which = e / tot1, rem = e % tot1;
+    const int Wd = which == 0 ? 64 : 128;
+    if (H % Wd) continue;
+    const int KS = 2048 / Wd;
+    const int j = rem / kD, k = rem % kD;  // hidden row, input column
+    const int u = j / Wd, r = j % Wd, q = k / KS, kk = k % KS;
+    char* item = (char*)out + mlp_w1_items_offset(H, Wd) + (size_t)(u * (kD / KS) + q) * 16384;
+    const uint32_t o = (uint32_t)((r >> 3) * (KS / 4) * 128 + (kk >> 2) * 128 + (r & 7) * 16 + (kk & 3) * 4);
+    const float w = W1[(size_t)j * kD + k];
+    const float hi = tf32_hi(w);
+    *(float*)(item + o) = hi;
+    *(float*)(item + 8192 + o) = w - hi;
+  }
 }
 
 template <int M>
@@ -201,9 +219,9 @@ __global__ void __launch_bounds__(256, 1) mlp_tc_kernel(MlpTcArgs A) {
           fence_after();
           const uint32_t aa[3] = {a_hi, a_hi, a_lo}, bb[3] = {w1h, w1l, w1h};
 #pragma unroll
-          for (int term = 0; term < 3; term++)
+          for (int s = 0; s < kD / 8; s++)
 #pragma unroll
-            for (int s = 0; s < kD / 8; s++)
+            for (int term = 0; term < 3; term++)
               mma_tf32(acc1, smem_desc(aa[term] + 256 * s, 2048), smem_desc(bb[term] + 256 * s, 2048),
                        idesc(kHc), (term | s) ? 1u : 0u);
           mma_commit(&S.mb_g1);
@@ -238,9 +256,9 @@ __global__ void __launch_bounds__(256, 1) mlp_tc_kernel(MlpTcArgs A) {
           fence_after();
           const uint32_t aa[3] = {h_hi, h_hi, h_lo}, bb[3] = {w2h, w2l, w2h};
 #pragma unroll
-          for (int term = 0; term < 3; term++)
+          for (int s = 0; s < kHc / 8; s++)
 #pragma unroll
-            for (int s = 0; s < kHc / 8; s++)
+            for (int term = 0; term < 3; term++)
               mma_tf32(acc2, smem_desc(aa[term] + 256 * s, 1024), smem_desc(bb[term] + 256 * s, 1024),
                        idesc(kD), (c | term | s) ? 1u : 0u);
           mma_commit(&S.mb_g2);
@@ -283,7 +301,7 @@ __global__ void __launch_bounds__(256, 1) mlp_tc_kernel(MlpTcArgs A) {
 
 }  // namespace tc
 
-size_t mlp_tc_prep_bytes(int64_t H) { return (size_t)(H / tc::kHc) * tc::kWChunk; }
+size_t mlp_tc_prep_bytes(int64_t H) { return mlp_w1_items_offset(H, 256); }
 
 bool mlp_tc_supported(int64_t D, int64_t H) { return D == tc::kD && H % tc::kHc == 0 && H <= 1024; }
 

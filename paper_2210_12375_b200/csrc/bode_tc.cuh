@@ -17,6 +17,17 @@ constexpr int kW1 = kHc * kD * 4;        //  8 KB: 32 x 64 fp32
 constexpr int kW2 = kD * kHc * 4;        //  8 KB: 64 x 32 fp32
 constexpr int kWChunk = 2 * kW1 + 2 * kW2;  // pre-split chunk in global
 
+}  // namespace tc
+// Byte offset, in the pre-split weight buffer, of the W1 items for GEMM1
+// unit width Wd: [H/32 chunks of 32 KB][Wd = 64 items: H/32 x 16 KB]
+// [Wd = 128 items: H/32 x 16 KB] (Wd = 32 items are the chunks' W1 halves;
+// Wd = 256 gives the total size).
+__host__ __device__ __forceinline__ size_t mlp_w1_items_offset(int64_t H, int Wd) {
+  const size_t chunk = (size_t)(H / tc::kHc) * tc::kWChunk, items = (size_t)(H / tc::kHc) * 16384;
+  return Wd <= 64 ? chunk : Wd == 128 ? chunk + items : chunk + 2 * items;
+}
+namespace tc {
+
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
 }
@@ -76,6 +87,16 @@ __device__ __forceinline__ void mma_tf32(uint32_t tmem, uint64_t a, uint64_t b, 
       "setp.ne.b32 p, %4, 0;\n\t"
       "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem),
       "l"(a), "l"(b), "r"(id), "r"(acc));
+}
+// true in exactly one lane of the (converged) warp
+__device__ __forceinline__ bool elect_one() {
+  uint32_t p = 0;
+  asm volatile(
+      "{\n\t.reg .pred P;\n\t"
+      "elect.sync _|P, 0xffffffff;\n\t"
+      "selp.b32 %0, 1, 0, P;\n\t}"
+      : "=r"(p));
+  return p != 0;
 }
 __device__ __forceinline__ void mma_commit(uint64_t* b) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
