@@ -75,6 +75,7 @@ struct Smem {
   float b2[kD];
   double hs[kRows];           // dt_used of the pending attempt, per row
   int32_t act[kRows];         // row holds an instance
+  int32_t ridx[kRows];        // instance just loaded into the row (-1: none)
   uint32_t seq[7][kItemsMax];  // weight item byte offsets, per stage, in consumption order
   uint64_t a_full, epidone[2], g1done[2], g2done[2], stage_done, wfull[kNS], wempty[kNS];
   uint32_t tmem_base;
@@ -163,10 +164,36 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_fused_kernel(const MlpFusedAr
   PROF_DECL
 
   while (true) {
-    // ================= refill free rows, dt_used of this attempt (WG0)
+    // ================= refill free rows (WG0 takes instances from the queue;
+    // both row groups keep identical copies of the row state)
+    auto load_row = [&](int64_t i) {
+      idx = i;
+      t = A.t[i];
+      dt = A.dt[i];
+      t_end = A.t_end[i];
+      atol = A.atol_v ? A.atol_v[i] : A.atol;
+      rtol = A.rtol_v ? A.rtol_v[i] : A.rtol;
+      cursor = A.n_emitted[i];
+      if (A.t_eval_offsets) {
+        const int64_t o = A.t_eval_offsets[i];
+        te = A.t_eval + o;
+        m = A.t_eval_offsets[i + 1] - o;
+        yout = A.ys ? A.ys + o * kD : nullptr;
+      } else {
+        te = A.t_eval;
+        m = A.t_eval_len;
+        yout = A.ys ? A.ys + i * A.t_eval_len * kD : nullptr;
+      }
+      n1 = 1.0;
+      n2 = 1.0;
+      nsteps = 0;
+      nacc = 0;
+      have = true;
+    };
     if (wg == 0) {
       const unsigned need = __ballot_sync(0xffffffffu, !have);
       bool got = false;
+      int32_t rid = -1;
       if (need) {
         const int leader = __ffs(need) - 1;
         unsigned long long base = 0;
@@ -176,27 +203,8 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_fused_kernel(const MlpFusedAr
           const unsigned long long pos = base + __popc(need & lt_mask);
           if (pos < (unsigned long long)count) {
             const int64_t i = A.act[pos];
-            idx = i;
-            t = A.t[i];
-            dt = A.dt[i];
-            t_end = A.t_end[i];
-            atol = A.atol_v ? A.atol_v[i] : A.atol;
-            rtol = A.rtol_v ? A.rtol_v[i] : A.rtol;
-            cursor = A.n_emitted[i];
-            if (A.t_eval_offsets) {
-              const int64_t o = A.t_eval_offsets[i];
-              te = A.t_eval + o;
-              m = A.t_eval_offsets[i + 1] - o;
-              yout = A.ys ? A.ys + o * kD : nullptr;
-            } else {
-              te = A.t_eval;
-              m = A.t_eval_len;
-              yout = A.ys ? A.ys + i * A.t_eval_len * kD : nullptr;
-            }
-            n1 = 1.0;
-            n2 = 1.0;
-            nsteps = 0;
-            nacc = 0;
+            rid = (int32_t)i;
+            load_row(i);
             const double2* yp = reinterpret_cast<const double2*>(A.y + i * kD);
 #pragma unroll 8
             for (int c = 0; c < kD / 2; c++) {
@@ -204,10 +212,11 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_fused_kernel(const MlpFusedAr
               sm.ys[2 * c][row] = v.x;
               sm.ys[2 * c + 1][row] = v.y;
             }
-            have = got = true;
+            got = true;
           }
         }
       }
+      sm.ridx[row] = rid;
       if (T::FSAL && __any_sync(0xffffffffu, got)) {  // k_0 = f0 of refilled rows
 #pragma unroll
         for (int ch = 0; ch < 4; ch++) {
@@ -239,6 +248,15 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_fused_kernel(const MlpFusedAr
     fence_after();
     PROF_MARK(1)
     if (!any) break;
+    if (wg == 1) {  // mirror WG0's row state
+      const int32_t rid = sm.ridx[row];
+      if (rid >= 0) load_row(rid);
+      if (have) {
+        const double rem = ExactOps::sub(t_end, t);
+        trunc = fabs(dt) >= fabs(rem);
+        h = trunc ? rem : dt;
+      }
+    }
 
     for (int s = S0; s < S; s++) {
       if (wg < 2) {
@@ -431,22 +449,27 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_fused_kernel(const MlpFusedAr
       }
     }
 
-    // ================= control: the rest of step_once (WG0, one row each)
+    // ================= control: the rest of step_once.  Each row group
+    // handles its 32 columns; the NumPy-order norm is finished by both groups
+    // from the exchanged partial sums, so both keep identical row state.
     fence_before();
     PROF_MARK(21)
     if (wg < 2) asm volatile("bar.sync 1, 256;" ::: "memory");
     fence_after();
     PROF_MARK(9)
-    if (wg == 0) {
-      double* ynb = reinterpret_cast<double*>(sm.a[0]);  // y_next, [column][row]
+    if (wg < 2) {
+      double* ynb = reinterpret_cast<double*>(sm.a[0]);   // y_next, [column][row]
+      double* p0 = reinterpret_cast<double*>(sm.w[0]);    // group 0's 8 partial sums
+      double* q1 = reinterpret_cast<double*>(sm.h);       // group 1's squared ratios
       double sq[8];
 #pragma unroll
-      for (int ch = 0; ch < 4; ch++) {
+      for (int ch = 0; ch < 2; ch++) {
+        const int c0 = 32 * wg + 16 * ch;
         double sb[16], se[16];
 #pragma unroll
         for (int j = 0; j < S; j++) {
           float kv[16];
-          tmem_ld16(lrow + 64 * j + 16 * ch, kv);
+          tmem_ld16(lrow + 64 * j + c0, kv);
           const double bj = T::b(j), ej = T::e(j);
 #pragma unroll
           for (int e = 0; e < 16; e++) {
@@ -457,17 +480,30 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_fused_kernel(const MlpFusedAr
         }
 #pragma unroll
         for (int e = 0; e < 16; e++) {
-          const int c = 16 * ch + e;
+          const int c = c0 + e;
           const double y = sm.ys[c][row];
           const double yn = ExactOps::mad(h, sb[e], y);
           const double err = ExactOps::mul(h, se[e]);
           const double scale = ExactOps::mad(rtol, np_max(fabs(y), fabs(yn)), atol);
           const double r = ddiv(err, scale);
           const double q = ExactOps::mul(r, r);
-          sq[c & 7] = c < 8 ? q : ExactOps::add(sq[c & 7], q);  // NumPy pairwise, n = 64
+          if (wg == 0) {
+            sq[c & 7] = c < 8 ? q : ExactOps::add(sq[c & 7], q);  // NumPy pairwise, n = 64
+          } else {
+            q1[(c - 32) * kRows + row] = q;
+          }
           ynb[c * kRows + row] = yn;
         }
       }
+      if (wg == 0) {
+#pragma unroll
+        for (int j = 0; j < 8; j++) p0[j * kRows + row] = sq[j];
+      }
+      asm volatile("bar.sync 1, 256;" ::: "memory");
+#pragma unroll
+      for (int j = 0; j < 8; j++) sq[j] = p0[j * kRows + row];
+#pragma unroll
+      for (int c = 32; c < kD; c++) sq[c & 7] = ExactOps::add(sq[c & 7], q1[(c - 32) * kRows + row]);
       double nrm = ExactOps::add(ExactOps::add(ExactOps::add(sq[0], sq[1]), ExactOps::add(sq[2], sq[3])),
                                  ExactOps::add(ExactOps::add(sq[4], sq[5]), ExactOps::add(sq[6], sq[7])));
       nrm = dsqrt(ddiv(nrm, (double)kD));
@@ -494,12 +530,13 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_fused_kernel(const MlpFusedAr
           w[q] = ExactOps::mul(v, th);
         }
 #pragma unroll
-        for (int ch = 0; ch < 4; ch++) {
+        for (int ch = 0; ch < 2; ch++) {
+          const int c0 = 32 * wg + 16 * ch;
           double sa[16];
 #pragma unroll
           for (int j = 0; j < S; j++) {
             float kv[16];
-            tmem_ld16(lrow + 64 * j + 16 * ch, kv);
+            tmem_ld16(lrow + 64 * j + c0, kv);
 #pragma unroll
             for (int e = 0; e < 16; e++)
               sa[e] = j == 0 ? ExactOps::mul(w[0], (double)kv[e])
@@ -508,7 +545,7 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_fused_kernel(const MlpFusedAr
           if (pend && yout) {
 #pragma unroll
             for (int e = 0; e < 16; e++)
-              yout[cursor * kD + 16 * ch + e] = ExactOps::mad(h, sa[e], sm.ys[16 * ch + e][row]);
+              yout[cursor * kD + c0 + e] = ExactOps::mad(h, sa[e], sm.ys[c0 + e][row]);
           }
         }
         if (pend) {
@@ -516,22 +553,23 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_fused_kernel(const MlpFusedAr
           pend = cursor < m;
         }
       }
-      // commit: y <- y_next, FSAL k_0 <- k_{S-1} on accepted rows
+      // commit: y <- y_next, FSAL k_0 <- k_{S-1} on accepted rows (my columns)
       if (have && accept) {
 #pragma unroll 8
-        for (int c = 0; c < kD; c++) sm.ys[c][row] = ynb[c * kRows + row];
+        for (int c = 32 * wg; c < 32 * wg + 32; c++) sm.ys[c][row] = ynb[c * kRows + row];
       }
       if (T::FSAL && __any_sync(0xffffffffu, have && accept)) {
 #pragma unroll
-        for (int ch = 0; ch < 4; ch++) {
+        for (int ch = 0; ch < 2; ch++) {
+          const int c0 = 32 * wg + 16 * ch;
           float k0[16], kl[16];
-          tmem_ld16(lrow + 16 * ch, k0);
-          tmem_ld16(lrow + 64 * (S - 1) + 16 * ch, kl);
+          tmem_ld16(lrow + c0, k0);
+          tmem_ld16(lrow + 64 * (S - 1) + c0, kl);
           if (have && accept) {
 #pragma unroll
             for (int e = 0; e < 16; e++) k0[e] = kl[e];
           }
-          tmem_st16(lrow + 16 * ch, k0);
+          tmem_st16(lrow + c0, k0);
         }
         tmem_wait_st();
       }
@@ -546,17 +584,19 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_fused_kernel(const MlpFusedAr
         dt = dtn;
         if (status == BODE_RUNNING && ExactOps::add(t, dt) == t) status = BODE_STEP_UNDERFLOW;
         if (status == BODE_RUNNING && nsteps >= A.max_steps) status = BODE_MAX_STEPS_EXCEEDED;
-        if (!accept && status == BODE_RUNNING) {
+        if (wg == 0 && !accept && status == BODE_RUNNING) {
           const uint64_t bit = (uint64_t)nsteps;  // rejected at iteration nsteps-1
           atomicOr(&A.refresh[bit >> 5], 1u << (bit & 31));
         }
         if (status != BODE_RUNNING) {
-          A.n_steps[idx] = nsteps;
-          A.n_accepted[idx] = nacc;
-          A.n_emitted[idx] = cursor;
-          A.final_dt[idx] = dt;
-          A.status[idx] = status;
-          if ((unsigned long long)nsteps > my_max) my_max = (unsigned long long)nsteps;
+          if (wg == 0) {
+            A.n_steps[idx] = nsteps;
+            A.n_accepted[idx] = nacc;
+            A.n_emitted[idx] = cursor;
+            A.final_dt[idx] = dt;
+            A.status[idx] = status;
+            if ((unsigned long long)nsteps > my_max) my_max = (unsigned long long)nsteps;
+          }
           have = false;
         }
       }
