@@ -231,6 +231,23 @@ def fp64_peak(torch, lib, dev):
     return best
 
 
+def tf32_peak(torch, lib, dev):
+    """Measured tcgen05 kind::tf32 throughput (bode_probe_tf32), TFLOP/s."""
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    reps = 4000
+    st = torch.cuda.current_stream(dev)
+    best = 0.0
+    for _ in range(4):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        lib.bode_probe_tf32(reps, sms, st.cuda_stream)
+        e1.record(st)
+        e1.synchronize()
+        secs = e0.elapsed_time(e1) / 1e3
+        best = max(best, 2.0 * 128 * 256 * 8 * 8 * reps * sms / secs / 1e12)
+    return best
+
+
 def run_bode(args, rank, world, local_rank):
     import torch
 
@@ -288,12 +305,12 @@ def run_bode(args, rank, world, local_rank):
             k0.record(st)  # materialise the cudaEvent_t handles (torch creates them lazily);
             k1.record(st)  # bode_solve re-records both around the persistent launch
             e0.record(st)
-            out = one_step(None if is_mlp else (k0, k1))
+            out = one_step((k0, k1))
             e1.record(st)
             e1.synchronize()
             times.append(e0.elapsed_time(e1))
             # the dominant kernel alone (persistent integrator), same stream
-            kern_times.append(times[-1] if is_mlp else k0.elapsed_time(k1))
+            kern_times.append(k0.elapsed_time(k1))
             accepted += int(out["n_accepted"].sum())
             attempted += int(out["n_steps"].sum())
             launches_per_step = out["launches"]  # kernels of ours in this solve
@@ -322,18 +339,21 @@ def run_bode(args, rank, world, local_rank):
     except Exception:
         pass
     if is_mlp:
-        # tensor-pipe bound: algorithmic MLP GEMM flops (4*D*H per f-eval: 6 FSAL
-        # stages per attempted step + 2 init evaluations per instance); peak =
-        # TF32 dense = measured bf16 / 2 (MEASURED_PEAKS.json has no TF32 entry)
+        # tensor-pipe bound: algorithmic MLP GEMM flops (4*D*H per f-eval, 6 FSAL
+        # stages per attempted step) of the fused persistent kernel (the init
+        # pass's two evaluations per instance run before it); peak = TF32
+        # tcgen05 throughput measured in-run by bode_probe_tf32
         D_, H_ = cfg["mlp"][0].shape[1], cfg["mlp"][0].shape[0]
-        flops_launch = 4.0 * D_ * H_ * (6 * att_launch + 2 * n)
-        peak = measured_peak("bf16_tflops") / 2.0
+        flops_launch = 4.0 * D_ * H_ * 6 * att_launch
+        peak = tf32_peak(torch, lib, dev)
         achieved = flops_launch / (kern_ms / 1e3) / 1e12
         roof = dict(bound="tensor", achieved=achieved, peak=peak, unit="TFLOP/s",
-                    frac=achieved / peak, traffic=traffic, kernel="mlp_tc_kernel (whole solve timed)",
-                    note="algorithmic GEMM flops of the fp32 MLP (3xTF32 issues 3x the MMAs) / "
-                         "whole-solve time; peak = TF32 dense = MEASURED_PEAKS bf16_tflops / 2",
-                    kernel_ms=kern_ms)
+                    frac=achieved / peak, traffic=traffic, kernel="mlp_fused_kernel",
+                    note="algorithmic GEMM flops of the fp32 MLP (3xTF32 issues 3x the MMAs: "
+                         "tensor-pipe work = 3 x achieved) / fused-kernel time (CUDA events "
+                         "around its launch); peak = tcgen05 kind::tf32 M=128 N=256 throughput "
+                         "measured in-run by bode_probe_tf32",
+                    mma_issue_frac=3 * achieved / peak, kernel_ms=kern_ms)
     else:
         peak_fp64 = fp64_peak(torch, lib, dev)
         flops_launch = flops_per_step(cfg["dyn"], d) * att_launch + flops_per_point(d) * pts

@@ -261,6 +261,11 @@ int bode_initial_step(const bode_dynamics* dyn, int64_t n, int64_t d,
  * launch gives the FP64 roofline denominator (2 flops per DFMA). */
 int bode_probe_fp64(int64_t iters, int32_t blocks, double* out, void* stream);
 
+/* Measurement utility: `blocks` CTAs (one per SM) each issue reps x 8
+ * tcgen05.mma kind::tf32 M=128 N=256 K=8 back to back; a timed launch gives
+ * the TF32 tensor roofline denominator (2*128*256*8 flops per MMA). */
+int bode_probe_tf32(int32_t reps, int32_t blocks, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

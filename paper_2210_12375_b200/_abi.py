@@ -80,6 +80,7 @@ SIGNATURES = {
     "bode_initial_step": ([_P, _I64, _I64, _P, _P, _I32, _P, _P, _D, _D, _P, _P, _P, _P],
                           C.c_int),
     "bode_probe_fp64": ([_I64, _I32, _P, _P], C.c_int),
+    "bode_probe_tf32": ([_I32, _I32, _P], C.c_int),
 }
 
 _lib = None

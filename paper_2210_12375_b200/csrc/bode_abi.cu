@@ -237,6 +237,33 @@ void retain_pool() {
   });
 }
 
+// per-device streams/events of bode_solve_host, created on first use
+struct HostStreams {
+  cudaStream_t cin, cout, st2;
+  cudaEvent_t ev_in[64], ev_done[65], ev_out[65], ready;
+};
+HostStreams& host_streams() {
+  static std::mutex m;
+  static HostStreams* per_dev[64] = {nullptr};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> g(m);
+  if (!per_dev[dev]) {
+    HostStreams* h = new HostStreams;
+    cudaStreamCreateWithFlags(&h->cin, cudaStreamNonBlocking);
+    cudaStreamCreateWithFlags(&h->cout, cudaStreamNonBlocking);
+    cudaStreamCreateWithFlags(&h->st2, cudaStreamNonBlocking);
+    for (int k = 0; k < 65; k++) {
+      if (k < 64) cudaEventCreateWithFlags(&h->ev_in[k], cudaEventDisableTiming);
+      cudaEventCreateWithFlags(&h->ev_done[k], cudaEventDisableTiming);
+      cudaEventCreateWithFlags(&h->ev_out[k], cudaEventDisableTiming);
+    }
+    cudaEventCreateWithFlags(&h->ready, cudaEventDisableTiming);
+    per_dev[dev] = h;
+  }
+  return *per_dev[dev];
+}
+
 }  // namespace
 
 extern "C" {
@@ -377,24 +404,19 @@ int bode_solve_host(const bode_solve_args* h) {
   a.workspace = dev + ws_off;
   a.workspace_bytes = L.total;
   // uploads on `cin`, downloads on `cout`, solves on the caller's stream
-  cudaStream_t cin, cout, st2 = st;
-  cudaStreamCreateWithFlags(&cin, cudaStreamNonBlocking);
-  cudaStreamCreateWithFlags(&cout, cudaStreamNonBlocking);
-  if (chunks > 1) cudaStreamCreateWithFlags(&st2, cudaStreamNonBlocking);
-  cudaEvent_t ev_in[64], ev_done[65], ev_out[65];
-  for (int k = 0; k <= chunks; k++) {
-    if (k < chunks) cudaEventCreateWithFlags(&ev_in[k], cudaEventDisableTiming);
-    cudaEventCreateWithFlags(&ev_done[k], cudaEventDisableTiming);
-    cudaEventCreateWithFlags(&ev_out[k], cudaEventDisableTiming);
-  }
+  // copy streams and the second chunk stream are created once per device and
+  // reused (the arena lock serialises host solves); events likewise
+  HostStreams& hs = host_streams();
+  cudaStream_t cin = hs.cin, cout = hs.cout, st2 = chunks > 1 ? hs.st2 : st;
+  cudaEvent_t* ev_in = hs.ev_in;
+  cudaEvent_t* ev_done = hs.ev_done;
+  cudaEvent_t* ev_out = hs.ev_out;
   {
-    cudaEvent_t ready;  // the allocation is visible to the copy streams
-    cudaEventCreateWithFlags(&ready, cudaEventDisableTiming);
+    cudaEvent_t ready = hs.ready;  // the allocation is visible to the copy streams
     cudaEventRecord(ready, st);
     cudaStreamWaitEvent(cin, ready, 0);
     cudaStreamWaitEvent(cout, ready, 0);
     if (st2 != st) cudaStreamWaitEvent(st2, ready, 0);
-    cudaEventDestroy(ready);
   }
   auto rows = [&](int k, int64_t& lo, int64_t& hi) {
     lo = (int64_t)k * cmax;
@@ -498,17 +520,7 @@ int bode_solve_host(const bode_solve_args* h) {
   cudaStreamSynchronize(cout);
   cudaFreeAsync(dev, st);
   cudaError_t e2 = cudaStreamSynchronize(st);
-  for (int k = 0; k <= chunks; k++) {
-    if (k < chunks) cudaEventDestroy(ev_in[k]);
-    cudaEventDestroy(ev_done[k]);
-    cudaEventDestroy(ev_out[k]);
-  }
-  cudaStreamDestroy(cin);
-  cudaStreamDestroy(cout);
-  if (st2 != st) {
-    cudaStreamSynchronize(st2);
-    cudaStreamDestroy(st2);
-  }
+  if (st2 != st) cudaStreamSynchronize(st2);
   if (rc != BODE_OK) return rc;
   if (e != cudaSuccess) return cuda_fail(e, "host<->device copy");
   if (e2 != cudaSuccess) return cuda_fail(e2, "solve");

@@ -34,8 +34,11 @@ DEFAULT_MAX_STEPS = 10_000
 MLP_BACKENDS = {"auto": 0, "cuda_core": 1, "tcgen05": 2, "fused": 3}
 
 
-# host arrays up to this size are page-locked (DMA at ~50 GB/s instead of a
-# driver-staged pageable copy at 13-19 GB/s, measured on the B200 box)
+# host arrays in [PIN_MIN_BYTES, PIN_MAX_BYTES] are page-locked (DMA at ~50
+# GB/s instead of a driver-staged pageable copy at 13-19 GB/s, measured on
+# the B200 box); below the minimum the pinned-allocator call costs more than
+# the copy it saves
+PIN_MIN_BYTES = 1 << 20
 PIN_MAX_BYTES = 1 << 30
 
 
@@ -47,7 +50,7 @@ def host_empty(shape, dtype=np.float64) -> np.ndarray:
     alive and returns it to the cache when collected)."""
     dtype = np.dtype(dtype)
     nbytes = int(np.prod(shape)) * dtype.itemsize
-    if 0 < nbytes <= PIN_MAX_BYTES:
+    if PIN_MIN_BYTES <= nbytes <= PIN_MAX_BYTES:
         try:
             import torch
             if torch.cuda.is_available():

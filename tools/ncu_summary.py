@@ -33,11 +33,14 @@ def launches(path):
     for r in rows[hi + 1:]:
         if len(r) > vi and r[vi]:
             tot[r[ki]].append(float(r[vi].replace(",", "")) * scale.get(r[ui], 1.0))
-    grand = sum(sum(v) for v in tot.values())
-    print("| kernel | launches | total us | mean us | share |")
+    # the roofline probes (bench.py's in-run peak measurement) are not part of
+    # the solve: listed, but excluded from the shares
+    grand = sum(sum(v) for k, v in tot.items() if "probe" not in k)
+    print("| kernel | launches | total us | mean us | share of solve |")
     print("|---|---|---|---|---|")
     for k, v in sorted(tot.items(), key=lambda x: -sum(x[1])):
-        print(f"| `{k[:90]}` | {len(v)} | {sum(v):.1f} | {sum(v)/len(v):.1f} | {sum(v)/grand:.1%} |")
+        share = "probe (excluded)" if "probe" in k else f"{sum(v)/grand:.1%}"
+        print(f"| `{k[:90]}` | {len(v)} | {sum(v):.1f} | {sum(v)/len(v):.1f} | {share} |")
 
 
 def full(path):
