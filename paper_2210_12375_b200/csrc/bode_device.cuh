@@ -365,9 +365,18 @@ __device__ __forceinline__ double pow_logged(double x, double e, bool ok, double
 // max(n1, NORM_FLOOR) == n1.  Bit-identical to adapt().
 struct LogCache {
   double h, l;
-  bool ok;  // false: log unknown (x = 1 at start, or x = inf) -> libm path
+  bool ok;  // false: log unknown (x = inf) -> libm path
 };
 
+// fast mode: x**e from a plain-double log (few ulp), special exponents as
+// NumPy evaluates them
+__device__ __forceinline__ double pow_logged_fast(double x, double e, bool ok, double Lh,
+                                                  double Ll, const PowTables& T) {
+  if (np_special_exponent(e)) return np_scalar_pow(x, e, T);
+  return (ok && isfinite(e)) ? fast_exp_mul(e, Lh, Ll, x, T) : pow_fallback(x, e);
+}
+
+template <class O>
 __device__ __forceinline__ bool adapt_cached(const CtrlParams& C, double norm, double& n1,
                                              double& n2, LogCache& L1, double& dt,
                                              const PowTables& T) {
@@ -376,10 +385,17 @@ __device__ __forceinline__ bool adapt_cached(const CtrlParams& C, double norm, d
   const double g = np_max(n2, 1e-10);
   LogCache La;
   La.ok = false;
-  if (!np_special_exponent(C.e1) || (C.e2 != 0.0 && !np_special_exponent(C.e2)))
-    La.ok = cr_log(a, T, La.h, La.l);
-  double factor = __dmul_rn(C.safety, pow_logged(a, C.e1, La.ok, La.h, La.l, T));
-  if (C.e2 != 0.0) factor = __dmul_rn(factor, pow_logged(n1, C.e2, L1.ok, L1.h, L1.l, T));
+  const bool need_log = !np_special_exponent(C.e1) || (C.e2 != 0.0 && !np_special_exponent(C.e2));
+  double factor;
+  if constexpr (O::kFast) {
+    if (need_log) La.ok = fast_log(a, T, La.h, La.l);
+    factor = __dmul_rn(C.safety, pow_logged_fast(a, C.e1, La.ok, La.h, La.l, T));
+    if (C.e2 != 0.0) factor = __dmul_rn(factor, pow_logged_fast(n1, C.e2, L1.ok, L1.h, L1.l, T));
+  } else {
+    if (need_log) La.ok = cr_log(a, T, La.h, La.l);
+    factor = __dmul_rn(C.safety, pow_logged(a, C.e1, La.ok, La.h, La.l, T));
+    if (C.e2 != 0.0) factor = __dmul_rn(factor, pow_logged(n1, C.e2, L1.ok, L1.h, L1.l, T));
+  }
   if (C.e3 != 0.0) factor = __dmul_rn(factor, np_scalar_pow(g, C.e3, T));
   if (!isfinite(factor)) factor = C.fmin;
   factor = np_min(np_max(factor, C.fmin), C.fmax);

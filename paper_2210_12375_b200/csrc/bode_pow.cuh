@@ -217,6 +217,64 @@ BODE_HD double cr_exp_mul(double e, double lh, double ll, double x, const PowTab
   return from_bits(bits(res) + (ke << 52));
 }
 
+// ---- BODE_MODE_FAST variants: plain double arithmetic with FMA on the same
+// tables -- within ~1 ulp instead of correctly rounded (the fast mode already
+// gives up bit-identity by contracting a*b+c); ~16 + 15 FP64 operations for
+// a log and an exp instead of ~50 + ~45.
+// log(x) = Lh + Ll, |Ll| < 2^-7, error < 2^-60 absolute; false for x <= 0 /
+// non-finite
+BODE_HD bool fast_log(double x, const PowTables& T, double& Lh, double& Ll) {
+  using namespace powimpl;
+  if (!(x > 0.0) || !(x < INFINITY)) return false;
+  int64_t ix = bits(x);
+  int k = 0;
+  if (ix < 0x0010000000000000LL) {  // subnormal: normalise
+    ix = bits(mul(x, BODE_PK(19)));
+    k = -52;
+  }
+  k += (int)(ix >> 52) - 1023;
+  const int i = (int)((ix >> 45) & 127);
+  const double m = from_bits((ix & 0x000FFFFFFFFFFFFFLL) | 0x3FF0000000000000LL);
+  const double r = fma_(m, T.log_tab[i][0], -1.0);  // |r| < 2^-7.9
+  // log1p(r) = r + r^2 (-1/2 + r q(r)), q = 1/3 - r/4 + r^2/5 - r^3/6 + r^4/7;
+  // the first omitted term r^8/8 is below 2^-66
+  double q = fma_(BODE_PK(2), r, BODE_PK(3));
+  q = fma_(q, r, BODE_PK(4));
+  q = fma_(q, r, BODE_PK(5));
+  q = fma_(q, r, BODE_PK(6));
+  // k ln2_hi is exact; for k != 0 it dominates log c, so Fast2Sum is exact
+  const double kl = mul((double)k, BODE_PK(14));
+  const double hi = add(kl, T.log_tab[i][1]);
+  const double hi_err = k != 0 ? sub(T.log_tab[i][1], sub(hi, kl)) : 0.0;
+  const double lo = add(fma_((double)k, BODE_PK(15), T.log_tab[i][2]), hi_err);
+  Lh = hi;
+  Ll = add(r, fma_(mul(r, r), fma_(r, q, BODE_PK(7)), lo));
+  return true;
+}
+
+// exp(e * (Lh + Ll)) within ~1 ulp; `x` (= exp(L)) is only used for the
+// libm fallback near overflow/underflow
+BODE_HD double fast_exp_mul(double e, double Lh, double Ll, double x, const PowTables& T) {
+  using namespace powimpl;
+  const double yh = mul(e, Lh);
+  const double yl = fma_(e, Ll, fma_(e, Lh, -yh));
+  if (!(yh < 700.0 && yh > -700.0)) return pow_fallback(x, e);
+  const double kd = rint(mul(yh, BODE_PK(18)));
+  const int64_t kf = (int64_t)kd;
+  const int j = (int)(kf & 127);
+  const int64_t ke = (kf - j) / 128;
+  const double r = add(fma_(-kd, BODE_PK(17), fma_(-kd, BODE_PK(16), yh)), yl);  // |r| < 2^-7.9
+  // exp(r) - 1 = r + r^2 (1/2 + r/6 + r^2/24 + r^3/120 + r^4/720); next term < 2^-67
+  double c = fma_(BODE_PK(9), r, BODE_PK(10));
+  c = fma_(c, r, BODE_PK(11));
+  c = fma_(c, r, BODE_PK(12));
+  c = fma_(c, r, BODE_PK(13));
+  const double p = fma_(mul(r, r), c, r);
+  const double th = T.exp_tab[j][0], tl = T.exp_tab[j][1];
+  const double res = add(th, fma_(th, p, tl));
+  return from_bits(bits(res) + (ke << 52));
+}
+
 // Correctly rounded (w.h.p.) x**e for x > 0 finite, e finite; everything
 // else -- and results near overflow/underflow -- goes to the libm pow.
 BODE_HD double cr_pow(double x, double e, const PowTables& T) {

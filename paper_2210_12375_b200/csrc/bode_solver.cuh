@@ -157,7 +157,7 @@ struct Lane {
     dt = P.final_dt[i];
     cursor = P.n_emitted[i];
     status = BODE_RUNNING;
-    L1.ok = cr_log(1.0, g_pow_tables, L1.h, L1.l);
+    L1.ok = cr_log(1.0, g_pow_tables, L1.h, L1.l);  // log(1) = 0 exactly (both modes)
   }
 
   // one iteration of step_once for this row (solver.py:208-282); returns
@@ -172,7 +172,7 @@ struct Lane {
     rk_step<T, F, O>(f, t, h, y, k, yn, err);
     const double norm = error_norm<D, O>(err, y, yn, atol, rtol);
     double dtn = h;
-    const bool accept = adapt_cached(P.ctrl, norm, n1, n2, L1, dtn, PT);
+    const bool accept = adapt_cached<O>(P.ctrl, norm, n1, n2, L1, dtn, PT);
     nsteps = j + 1;
     if (P.trace_cap > 0 && j < P.trace_cap) {
       const int64_t o = idx * P.trace_cap + j;

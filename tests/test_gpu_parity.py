@@ -75,10 +75,38 @@ def test_solve_matches_reference_golden(name):
                                        atol=T_TOL * span)
 
 
-@pytest.mark.parametrize("name", ["c1_vdp", "c2_vdp_pi42", "c3_lorenz", "c5_vdp_stiff"])
+@pytest.mark.parametrize("name", sorted(SCENARIOS))
 def test_fast_mode_within_tolerance(name):
-    """FMA-contracted mode: same step counts, ys within the same bar."""
+    """Fast mode (FMA-contracted arithmetic, ~1-ulp controller pow; the bench
+    headline mode): same statuses and step counts, ys within the same bar."""
     sc = SCENARIOS[name]
     g = G.load(name)
     sol = devspec.solve_scenario(sc, mode="fast")
     compare(sol, g, sc)
+
+
+def test_fast_mode_full_scale_c2():
+    """The headline workload (C2, 2^20 instances) in fast mode against the
+    pinned oracle: every status and step count identical, ys within 1e-10."""
+    import os
+    import sys
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                                    "oracle"))
+    import oracle as O
+    import paper_2210_12375_b200 as bode
+    import scenarios as S
+    mu, t_end = S.c2_inputs()
+    n = mu.shape[0]
+    y0 = np.tile([2.0, 0.0], (n, 1))
+    sol = bode.solve(bode.IvpBatch(y0, np.zeros(n), t_end, t_end[:, None]),
+                     bode.vdp_dynamics(bode.VdpParams(mu)), controller=bode.pid_controller("PI42"),
+                     cost_hint=mu * t_end, mode="fast")
+    ref = O.solve(y0, 0.0, t_end, [np.array([x]) for x in t_end], dict(name="vdp", inst=mu[:, None]),
+                  ctrl=dict(betas=S.PI42, safety=0.9, factor_min=0.2, factor_max=10.0, hist=True),
+                  nthreads=os.cpu_count())
+    assert np.array_equal(sol.status, ref["status"])
+    assert np.array_equal(sol.stats.n_steps, ref["n_steps"])
+    assert np.array_equal(sol.stats.n_accepted, ref["n_accepted"])
+    assert sol.stats.n_f_evals[0] == ref["n_f_evals"][0]
+    a, b = sol.ys_flat.reshape(n, -1), ref["ys"].reshape(n, -1)
+    assert np.max(np.abs(a - b).max(axis=1) / np.abs(b).max(axis=1)) <= YS_TOL

@@ -49,3 +49,24 @@ def test_special_values(crpow):
     assert crpow(2.0 ** -1060, 0.5) == math.pow(2.0 ** -1060, 0.5)   # subnormal input
     assert crpow(1e300, 0.9) == math.pow(1e300, 0.9)
     assert crpow(1e-300, 2.5) == math.pow(1e-300, 2.5)  # underflow edge -> libm
+
+
+@pytest.mark.parametrize("e", [-0.2, -0.12, 0.04, 1 / 6, -1 / 30, -1 / 90])
+def test_fast_mode_pow_within_1_ulp(e):
+    """BODE_MODE_FAST's controller pow (plain-double log/exp on the same
+    tables): within 1 ulp of the exact value over the controller's range."""
+    if not os.path.exists(LIB):
+        pytest.skip("host pow library not built")
+    lib = C.CDLL(LIB)
+    lib.bode_fast_pow_host.restype = C.c_double
+    lib.bode_fast_pow_host.argtypes = [C.c_double, C.c_double]
+    getcontext().prec = 50
+    rng = random.Random(7 + (hash(e) & 0xFF))
+    worst = 0
+    for _ in range(4000):
+        x = 10 ** rng.uniform(-10, 3)
+        ref = float((Decimal(e) * Decimal(x).ln()).exp())
+        got = lib.bode_fast_pow_host(x, e)
+        worst = max(worst, abs(got - ref) / math.ulp(ref))
+    assert worst <= 1, worst
+    assert lib.bode_fast_pow_host(1.0, e) == 1.0

@@ -49,6 +49,8 @@ def main():
                   ctrl=dict(betas=S.PI42, safety=0.9, factor_min=0.2, factor_max=10.0, hist=True))
     a, b = sol.ys_flat.reshape(n, -1), ref["ys"].reshape(n, -1)
     err = np.max(np.abs(a - b).max(axis=1) / np.abs(b).max(axis=1))
+    print(f"C2 instances with a different n_steps: {int(np.sum(sol.stats.n_steps != ref['n_steps']))}, "
+          f"n_accepted: {int(np.sum(sol.stats.n_accepted != ref['n_accepted']))}")
     print(f"\nC2 full scale (n={n}, vs oracle): status identical "
           f"{np.array_equal(sol.status, ref['status'])}, n_steps identical "
           f"{np.array_equal(sol.stats.n_steps, ref['n_steps'])}, n_accepted identical "
@@ -58,5 +60,43 @@ def main():
           f"{np.mean(sol.stats.final_dt == ref['final_dt']):.2%}")
 
 
-if __name__ == "__main__":
+if __name__ == "__main__" and "--extra" not in sys.argv:
     main()
+
+
+def full_scale_extra(mode):
+    """C5 (stiff VdP, 1M) and C3 (Lorenz tsit5 1e-8, 256K, 1000 points) at
+    full size vs the oracle: per-instance step-count mismatches, scaled ys."""
+    sys.path.insert(0, ROOT)
+    import bench
+    for name in ("c5", "c3"):
+        cfg = bench.make_config(name, 0)
+        n = cfg["n"]
+        te = cfg.get("te1d")
+        dyn = (bode.vdp_dynamics(bode.VdpParams(cfg["mu"])) if cfg["dyn"] == "vdp"
+               else bode.lorenz_dynamics())
+        tab = {"dopri5": bode.dopri5, "tsit5": bode.tsit5}[cfg["method"]]()
+        ctrl = bode.PidCoefficients(*cfg["ctrl"]["betas"])
+        sol = bode.solve(bode.IvpBatch(cfg["y0"], cfg["t_start"], cfg["t_end"],
+                                       te if te is not None else [np.empty(0)] * n),
+                         dyn, tableau=tab, tol=bode.Tolerances(cfg["tol"], cfg["tol"]),
+                         controller=ctrl, max_steps=cfg["max_steps"], mode=mode,
+                         cost_hint=cfg["cost"])
+        odyn = (dict(name="vdp", inst=cfg["mu"][:, None]) if cfg["dyn"] == "vdp"
+                else dict(name="lorenz", inst=None, shared=(10.0, 28.0, 8.0 / 3.0)))
+        ref = O.solve(cfg["y0"], cfg["t_start"], cfg["t_end"], te, odyn, method=cfg["method"],
+                      atol=cfg["tol"], rtol=cfg["tol"], ctrl=cfg["ctrl"], max_steps=cfg["max_steps"],
+                      nthreads=os.cpu_count())
+        ds = int(np.sum(sol.stats.n_steps != ref["n_steps"]))
+        da = int(np.sum(sol.stats.n_accepted != ref["n_accepted"]))
+        msg = ""
+        if te is not None:
+            a, b = sol.ys_flat.reshape(n, -1), ref["ys"].reshape(n, -1)
+            msg = f", max scaled ys err {np.max(np.abs(a - b).max(axis=1) / np.abs(b).max(axis=1)):.2e}"
+        print(f"{name} full scale (n={n}, mode={mode}, vs oracle): status identical "
+              f"{np.array_equal(sol.status, ref['status'])}, instances with different n_steps {ds}, "
+              f"n_accepted {da}, n_f_evals {sol.stats.n_f_evals[0]} vs {ref['n_f_evals'][0]}{msg}")
+
+
+if __name__ == "__main__" and "--extra" in sys.argv:
+    full_scale_extra(sys.argv[sys.argv.index("--extra") + 1])

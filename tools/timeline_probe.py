@@ -6,6 +6,7 @@ import numpy as np, torch
 import bench
 import paper_2210_12375_b200 as bode
 cfgname = sys.argv[1] if len(sys.argv) > 1 else "c2"
+mode = sys.argv[2] if len(sys.argv) > 2 else "exact"
 cfg = bench.make_config(cfgname, 0)
 dev = torch.device("cuda", 0)
 f64 = dict(dtype=torch.float64, device=dev)
@@ -16,7 +17,7 @@ cost = torch.tensor(cfg["cost"], **f64) if cfg["cost"] is not None else None
 ctrl = bode.PidCoefficients(*cfg["ctrl"]["betas"])
 def one():
     return bode.solve_device(y0, ts, tn, dyn, t_eval=te, method=cfg["method"], atol=cfg["tol"], rtol=cfg["tol"],
-                             controller=ctrl, max_steps=cfg["max_steps"], cost_hint=cost)
+                             controller=ctrl, max_steps=cfg["max_steps"], cost_hint=cost, mode=mode)
 for _ in range(3): one()
 torch.cuda.synchronize()
 t0 = time.perf_counter(); o = one(); t1 = time.perf_counter(); torch.cuda.synchronize(); t2 = time.perf_counter()
