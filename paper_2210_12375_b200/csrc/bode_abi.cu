@@ -7,6 +7,7 @@
 //   -> n_f_evals finalisation.
 // bode_solve_host adds the host<->device copies and, optionally, a chunked
 // pipeline that overlaps chunk k's solve with the neighbouring chunks' copies.
+#include <cmath>
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
@@ -67,6 +68,9 @@ CtrlParams make_ctrl(const bode_controller& c, int error_order) {
   p.fmin = c.factor_min;
   p.fmax = c.factor_max;
   p.hist = c.update_history_on_reject;
+  auto special = [](double e) { return e == 0.0 || e == 1.0 || e == -1.0 || e == 2.0 || e == 0.5; };
+  p.plain_pi = std::isfinite(p.e1) && std::isfinite(p.e2) && !special(p.e1) &&
+               (p.e2 == 0.0 || !special(p.e2)) && p.e3 == 0.0;
   return p;
 }
 

@@ -163,7 +163,7 @@ struct Lane {
   // one iteration of step_once for this row (solver.py:208-282); returns
   // true when the row just rejected and is still running (FSAL refresh at
   // the next iteration, solver.py:220-226)
-  __device__ __forceinline__ bool step(const SolveParams& P, const PowTables& PT) {
+  __device__ __forceinline__ bool step(const SolveParams& P, const PowTables& PT, bool tracing) {
     const int64_t j = nsteps;
     const double remaining = O::sub(t_end, t);
     const bool trunc = fabs(dt) >= fabs(remaining);
@@ -174,7 +174,7 @@ struct Lane {
     double dtn = h;
     const bool accept = adapt_cached<O>(P.ctrl, norm, n1, n2, L1, dtn, PT);
     nsteps = j + 1;
-    if (P.trace_cap > 0 && j < P.trace_cap) {
+    if (tracing && j < P.trace_cap) {
       const int64_t o = idx * P.trace_cap + j;
       if (P.trace_t) P.trace_t[o] = t;
       if (P.trace_dt) P.trace_dt[o] = h;
@@ -244,6 +244,7 @@ __global__ void __launch_bounds__(128, (F::D <= 2 ? BODE_BLOCKS_2D : 4)) bode_pe
   __syncthreads();
 
   Lane<M, F, O> L;
+  const bool tracing = P.trace_cap > 0;  // uniform: hoisted out of the step loop
   bool have = false, done = false;
   unsigned long long my_max = 0;
   const unsigned lt_mask = (1u << lane) - 1u;
@@ -274,7 +275,7 @@ __global__ void __launch_bounds__(128, (F::D <= 2 ? BODE_BLOCKS_2D : 4)) bode_pe
     }
     if (have) {
       const int64_t j = L.nsteps;
-      if (L.step(P, s_pow)) {
+      if (L.step(P, s_pow, tracing)) {
         const uint64_t bit = (uint64_t)j + 1;
         const uint32_t w = (uint32_t)(bit >> 5), msk = 1u << (bit & 31);
         if (P.smem_words > 0) {
