@@ -75,30 +75,39 @@ struct Lane {
   F f;
   double y[D];
   double k[S][D];  // k[0] is the FSAL cache f0
-  double t, dt, t_end, atol, rtol, n1, n2;
+  // Per-instance tolerances are re-derived from idx where used (scalar
+  // tolerances stay uniform) and counters are 32-bit, to keep the 2-D
+  // kernels at 5 blocks / SM with few spills.
+  double t, dt, t_end, n1, n2;
   LogCache L1;  // log(n1) for the PID history term (adapt_cached)
-  int64_t idx, nsteps, nacc, cursor, m;
+  int64_t idx;
+  int32_t nsteps, nacc, cursor, m;
+  int32_t status;
   const double* te;
   double* ys;
-  int32_t status;
+
+  __device__ __forceinline__ double atol_of(const SolveParams& P) const {
+    return P.atol_v ? P.atol_v[idx] : P.atol;
+  }
+  __device__ __forceinline__ double rtol_of(const SolveParams& P) const {
+    return P.rtol_v ? P.rtol_v[idx] : P.rtol;
+  }
 
   __device__ __forceinline__ void load_problem(const SolveParams& P, int64_t i) {
     idx = i;
     f.load(P.dyn, i);
     t = P.t_start[i];
     t_end = P.t_end[i];
-    atol = P.atol_v ? P.atol_v[i] : P.atol;
-    rtol = P.rtol_v ? P.rtol_v[i] : P.rtol;
 #pragma unroll
     for (int c = 0; c < D; c++) y[c] = P.y0[i * D + c];
     if (P.t_eval_offsets) {
       const int64_t off = P.t_eval_offsets[i];
       te = P.t_eval + off;
-      m = P.t_eval_offsets[i + 1] - off;
+      m = (int32_t)(P.t_eval_offsets[i + 1] - off);
       ys = P.ys ? P.ys + off * D : nullptr;
     } else {
       te = P.t_eval;
-      m = P.t_eval_len;
+      m = (int32_t)P.t_eval_len;
       ys = P.ys ? P.ys + i * P.t_eval_len * D : nullptr;
     }
     n1 = 1.0;
@@ -116,7 +125,7 @@ struct Lane {
     load_problem(P, i);
     const double direction = (t_end - t) > 0.0 ? 1.0 : -1.0;
     if (P.dt0_mode == BODE_DT0_HEURISTIC) {
-      dt = initial_step<F, O>(f, t, y, T::ORDER, atol, rtol, direction, k[0]);
+      dt = initial_step<F, O>(f, t, y, T::ORDER, atol_of(P), rtol_of(P), direction, k[0]);
     } else {
       dt = P.dt0_mode == BODE_DT0_SCALAR ? P.dt0 : P.dt0_v[i];
       f(t, y, k[0]);
@@ -155,7 +164,7 @@ struct Lane {
 #pragma unroll
     for (int c = 0; c < D; c++) k[0][c] = P.f0[i * D + c];
     dt = P.final_dt[i];
-    cursor = P.n_emitted[i];
+    cursor = (int32_t)P.n_emitted[i];
     status = BODE_RUNNING;
     L1.ok = cr_log(1.0, g_pow_tables, L1.h, L1.l);  // log(1) = 0 exactly (both modes)
   }
@@ -164,18 +173,18 @@ struct Lane {
   // true when the row just rejected and is still running (FSAL refresh at
   // the next iteration, solver.py:220-226)
   __device__ __forceinline__ bool step(const SolveParams& P, const PowTables& PT, bool tracing) {
-    const int64_t j = nsteps;
+    const int32_t j = nsteps;
     const double remaining = O::sub(t_end, t);
     const bool trunc = fabs(dt) >= fabs(remaining);
     const double h = trunc ? remaining : dt;
     double yn[D], err[D];
     rk_step<T, F, O>(f, t, h, y, k, yn, err);
-    const double norm = error_norm<D, O>(err, y, yn, atol, rtol);
+    const double norm = error_norm<D, O>(err, y, yn, atol_of(P), rtol_of(P));
     double dtn = h;
     const bool accept = adapt_cached<O>(P.ctrl, norm, n1, n2, L1, dtn, PT);
     nsteps = j + 1;
     if (tracing && j < P.trace_cap) {
-      const int64_t o = idx * P.trace_cap + j;
+      const int64_t o = idx * P.trace_cap + j;  // (trace only)
       if (P.trace_t) P.trace_t[o] = t;
       if (P.trace_dt) P.trace_dt[o] = h;
       if (P.trace_accept) P.trace_accept[o] = accept;
@@ -183,7 +192,7 @@ struct Lane {
     if (accept) {
       nacc++;
       const double t_old = t;
-      if (cursor < m && h != 0.0) emit(t_old, h);
+      if (cursor < m && h != 0.0) emit(P, t_old, h);
 #pragma unroll
       for (int c = 0; c < D; c++) y[c] = yn[c];
       t = trunc ? t_end : O::add(t_old, h);
@@ -201,7 +210,7 @@ struct Lane {
 
   // _emit, solver.py:284-322: every point with theta in (.., 1] is
   // interpolated from the pre-commit state (y is still y_old here)
-  __device__ __forceinline__ void emit(double t_old, double h) {
+  __device__ __forceinline__ void emit(const SolveParams& P, double t_old, double h) {
     while (cursor < m) {
       double theta = ddiv(O::sub(te[cursor], t_old), h);
       if (!(theta <= 1.0)) break;
