@@ -312,7 +312,8 @@ int bode_solve_host(const bode_solve_args* h) {
   if (h->order || h->trace_cap > 0 || h->dyn.kind == BODE_DYN_MLP) chunks = 1;
   if (chunks > n) chunks = (int)n;
   if (chunks > 64) chunks = 64;
-  const int64_t cmax = chunk_max(n, chunks);
+  // largest chunk (the middle ones when the first/last are half-size)
+  const int64_t cmax = chunks >= 3 ? (n + chunks - 2) / (chunks - 1) + 1 : chunk_max(n, chunks);
 
   // one device block for every array; per-instance arrays move in chunk
   // slices so chunk k can start as soon as its own rows landed.  Pinned
@@ -422,9 +423,18 @@ int bode_solve_host(const bode_solve_args* h) {
     cudaStreamWaitEvent(cout, ready, 0);
     if (st2 != st) cudaStreamWaitEvent(st2, ready, 0);
   }
+  // chunk boundaries: the first and last chunks are half-size, so the
+  // first solve starts (and the last download ends) sooner
+  int64_t bnd[65];
+  bnd[0] = 0;
+  for (int k = 1; k <= chunks; k++) {
+    const double units = chunks >= 3 ? 2.0 * (chunks - 1) : (double)chunks;  // in half-chunks
+    const double done = chunks >= 3 ? (k == chunks ? units : 2.0 * k - 1.0) : (double)k;
+    bnd[k] = k == chunks ? n : (int64_t)((double)n * done / units);
+  }
   auto rows = [&](int k, int64_t& lo, int64_t& hi) {
-    lo = (int64_t)k * cmax;
-    hi = lo + cmax < n ? lo + cmax : n;
+    lo = bnd[k];
+    hi = bnd[k + 1];
   };
   // byte range [o, o+b) of array x that belongs to chunk k; k == chunks
   // means "the whole-array outputs written by the finaliser"
@@ -435,13 +445,20 @@ int bode_solve_host(const bode_solve_args* h) {
       rows(k, lo, hi);
       o = (size_t)lo * x.row_bytes;
       b = (size_t)(hi - lo) * x.row_bytes;
-    } else if (x.out_field == (void**)&a.ys) {  // ys rows of this chunk's instances
+    } else if (x.out_field == (void**)&a.ys ||
+               (csr && x.in_field == (const void**)&a.t_eval)) {  // CSR rows of this chunk
       if (k == chunks) return false;
       rows(k, lo, hi);
       const int64_t r0 = csr ? h->t_eval_offsets[lo] : lo * h->t_eval_len;
       const int64_t r1 = csr ? h->t_eval_offsets[hi] : hi * h->t_eval_len;
-      o = (size_t)r0 * 8 * d;
-      b = (size_t)(r1 - r0) * 8 * d;
+      const size_t w = x.in_field ? 8 : 8 * (size_t)d;
+      o = (size_t)r0 * w;
+      b = (size_t)(r1 - r0) * w;
+    } else if (x.in_field == (const void**)&a.t_eval_offsets) {  // offsets [lo, hi]
+      if (k == chunks) return false;
+      rows(k, lo, hi);
+      o = (size_t)lo * 8;
+      b = (size_t)(hi - lo + 1) * 8;
     } else {  // whole arrays: inputs with chunk 0, outputs after the finaliser
       if (k != (x.in_field ? 0 : chunks)) return false;
       o = 0;

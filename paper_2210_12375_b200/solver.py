@@ -249,7 +249,7 @@ def _tol_arrays(tol: Tolerances, n: int):
 def solve(problem: IvpBatch, f, tableau=None, tol: Tolerances | None = None,
           controller: PidCoefficients | None = None, max_steps: int = DEFAULT_MAX_STEPS,
           dt0=None, record_trace: bool = False, *, mode: str = "exact", order=None,
-          cost_hint=None, pipeline_chunks: int = 4, with_refresh_map: bool = False,
+          cost_hint=None, pipeline_chunks: int = 3, with_refresh_map: bool = False,
           mlp_backend: str = "auto") -> Solution:
     """Integrate every instance independently with adaptive steps on the GPU
     (reference ``solve``, solver.py:352-369), host arrays in and out."""

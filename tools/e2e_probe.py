@@ -8,14 +8,14 @@ import paper_2210_12375_b200 as bode
 cfg = bench.make_config("c2", 0)
 n = cfg["n"]
 ctrl = bode.PidCoefficients(*cfg["ctrl"]["betas"])
-for pin in (False, True):
+for pin in (True, False):
     P = bode.pinned if pin else (lambda x: x)
     prob = bode.IvpBatch(P(cfg["y0"]), P(cfg["t_start"]), P(cfg["t_end"]), P(cfg["te2d"]))
     f = bode.vdp_dynamics(bode.VdpParams(P(cfg["mu"])))
     cost = P(cfg["cost"])
-    for chunks in (1, 2, 4, 8):
+    for chunks in (1, 2, 3, 4, 6, 8):
         kw = dict(tableau=bode.dopri5(), tol=bode.Tolerances(1e-6, 1e-6), controller=ctrl,
-                  max_steps=cfg["max_steps"], cost_hint=cost, pipeline_chunks=chunks)
+                  max_steps=cfg["max_steps"], cost_hint=cost, pipeline_chunks=chunks, mode="fast")
         bode.solve(prob, f, **kw)
         ts = []
         for _ in range(5):
