@@ -39,7 +39,10 @@ MLP_BACKENDS = {"auto": 0, "cuda_core": 1, "tcgen05": 2, "fused": 3}
 # the B200 box); below the minimum the pinned-allocator call costs more than
 # the copy it saves
 PIN_MIN_BYTES = 1 << 20
-PIN_MAX_BYTES = 1 << 30
+PIN_MAX_BYTES = 16 << 30
+# resident lanes of the persistent kernel (148 SMs x 5 blocks x 128): the
+# share of work one lane gets, used to decide whether chunking pays
+_LANES = 148 * 5 * 128
 
 
 def host_empty(shape, dtype=np.float64) -> np.ndarray:
@@ -249,7 +252,7 @@ def _tol_arrays(tol: Tolerances, n: int):
 def solve(problem: IvpBatch, f, tableau=None, tol: Tolerances | None = None,
           controller: PidCoefficients | None = None, max_steps: int = DEFAULT_MAX_STEPS,
           dt0=None, record_trace: bool = False, *, mode: str = "exact", order=None,
-          cost_hint=None, pipeline_chunks: int = 3, with_refresh_map: bool = False,
+          cost_hint=None, pipeline_chunks="auto", with_refresh_map: bool = False,
           mlp_backend: str = "auto") -> Solution:
     """Integrate every instance independently with adaptive steps on the GPU
     (reference ``solve``, solver.py:352-369), host arrays in and out."""
@@ -307,6 +310,16 @@ def solve(problem: IvpBatch, f, tableau=None, tol: Tolerances | None = None,
         ch = np.ascontiguousarray(np.broadcast_to(np.asarray(cost_hint, dtype=np.float64), (n,)))
         keep.append(ch)
         a.cost_hint = ch.ctypes.data
+    if pipeline_chunks == "auto":
+        # 3 chunks overlap uploads / downloads with the solve, but each chunk
+        # ends with its own tail: with a heavy-tailed cost hint (one instance
+        # costing more than a lane's share of a chunk) a single launch wins
+        pipeline_chunks = 3 if n >= 65536 else 1
+        if cost_hint is not None and pipeline_chunks > 1:
+            c = np.asarray(cost_hint, dtype=np.float64).reshape(-1)
+            smp = c[::max(1, c.size // 4096)]
+            if smp.max() > smp.mean() * n / (_LANES * pipeline_chunks):
+                pipeline_chunks = 1
     a.pipeline_chunks = int(pipeline_chunks) if n >= 65536 else 1
     a.mlp_backend = MLP_BACKENDS[mlp_backend]
     ys = host_empty((max(n_rows, 1), d))

@@ -1,7 +1,7 @@
-set -x
+# round verification: GPU tests, smoke, bench on every config, CPU reference arm
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv
 python -m pytest tests -m gpu -x -q 2>&1 | tail -15 > gpurun_out/pytest_gpu.log
 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1
 for c in c2 c1 c3 c4 c5; do timeout 600 python bench.py --config $c > gpurun_out/bench_$c.json 2> gpurun_out/bench_$c.err; done
 timeout 600 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err
-tail -3 gpurun_out/pytest_gpu.log; cat gpurun_out/smoke.log; cat gpurun_out/bench_*.json
+tail -3 gpurun_out/pytest_gpu.log; cat gpurun_out/smoke.log
