@@ -111,11 +111,31 @@ __device__ double pairwise_sum_rt(const double* a, int64_t n) {
 }
 
 // ------------------------------------------------------------ tableaus --
-// Coefficients live in the constant bank so FP64 instructions take them as
-// c[bank][offset] operands (immediates would cost two UMOVs per 64-bit
-// literal).  Layout per method: a[7][7] | b[7] | b_err[7] | c[7] | w[7][4].
-static __constant__ double c_tab[3][98] = {BODE_DOPRI5_FLAT_INIT, BODE_TSIT5_FLAT_INIT,
-                                           BODE_HEUN_FLAT_INIT};
+// Coefficients live in the constant bank and reach the FP64 instructions
+// through uniform registers (LDCU; immediates would cost two UMOVs per
+// 64-bit literal).  The generated flat layout a[7][7] | b[7] | b_err[7] |
+// c[7] | w[7][4] is remapped at compile time so that the coefficients an
+// instance reads together sit in aligned pairs (one LDCU.128 per two):
+// a rows padded to 8, b_i and b_err_i interleaved, w rows on even offsets.
+struct TabData {
+  double v[112];
+};
+constexpr TabData remap_tab(const double (&f)[98]) {
+  TabData t{};
+  for (int i = 0; i < 7; i++) {
+    for (int j = 0; j < 7; j++) t.v[8 * i + j] = f[i * 7 + j];  // a(i, j) -> 8 i + j
+    t.v[56 + 2 * i] = f[49 + i];                               // b(i)
+    t.v[57 + 2 * i] = f[56 + i];                               // b_err(i)
+    t.v[70 + i] = f[63 + i];                                   // c(i)
+    for (int j = 0; j < 4; j++) t.v[78 + 4 * i + j] = f[70 + i * 4 + j];  // w(i, j)
+  }
+  return t;
+}
+constexpr double k_dopri5_flat[98] = BODE_DOPRI5_FLAT_INIT;
+constexpr double k_tsit5_flat[98] = BODE_TSIT5_FLAT_INIT;
+constexpr double k_heun_flat[98] = BODE_HEUN_FLAT_INIT;
+static __constant__ TabData c_tab[3] = {remap_tab(k_dopri5_flat), remap_tab(k_tsit5_flat),
+                                        remap_tab(k_heun_flat)};
 
 template <int M> struct TabShape;
 // za/zb/ze/zw: the same coefficients as compile-time constants, used only to
@@ -147,11 +167,11 @@ template <> struct TabShape<BODE_METHOD_HEUN> {
 
 template <int M>
 struct Tab : TabShape<M> {
-  static __device__ __forceinline__ double a(int i, int j) { return c_tab[M][i * 7 + j]; }
-  static __device__ __forceinline__ double b(int i) { return c_tab[M][49 + i]; }
-  static __device__ __forceinline__ double e(int i) { return c_tab[M][56 + i]; }
-  static __device__ __forceinline__ double c(int i) { return c_tab[M][63 + i]; }
-  static __device__ __forceinline__ double w(int i, int j) { return c_tab[M][70 + i * 4 + j]; }
+  static __device__ __forceinline__ double a(int i, int j) { return c_tab[M].v[8 * i + j]; }
+  static __device__ __forceinline__ double b(int i) { return c_tab[M].v[56 + 2 * i]; }
+  static __device__ __forceinline__ double e(int i) { return c_tab[M].v[57 + 2 * i]; }
+  static __device__ __forceinline__ double c(int i) { return c_tab[M].v[70 + i]; }
+  static __device__ __forceinline__ double w(int i, int j) { return c_tab[M].v[78 + 4 * i + j]; }
 };
 
 // ------------------------------------------------------------ dynamics --
