@@ -75,16 +75,24 @@ struct Lane {
   F f;
   double y[D];
   double k[S][D];  // k[0] is the FSAL cache f0
-  // Per-instance tolerances are re-derived from idx where used (scalar
-  // tolerances stay uniform) and counters are 32-bit, to keep the 2-D
-  // kernels at 5 blocks / SM with few spills.
+  // Registers hold what every step touches: per-instance tolerances and the
+  // t_eval / ys bases are re-derived from idx where used (scalar tolerances
+  // stay uniform), the next output time is cached (te_next), counters are
+  // 32-bit -- the 2-D kernels stay at 5 blocks / SM with few spills.
   double t, dt, t_end, n1, n2;
+  double te_next;  // t_eval[cursor], cached: the per-step check needs no load
   LogCache L1;  // log(n1) for the PID history term (adapt_cached)
   int64_t idx;
   int32_t nsteps, nacc, cursor, m;
   int32_t status;
-  const double* te;
-  double* ys;
+
+  __device__ __forceinline__ const double* te_of(const SolveParams& P) const {
+    return P.t_eval_offsets ? P.t_eval + P.t_eval_offsets[idx] : P.t_eval;
+  }
+  __device__ __forceinline__ double* ys_of(const SolveParams& P) const {
+    if (!P.ys) return nullptr;
+    return P.t_eval_offsets ? P.ys + P.t_eval_offsets[idx] * D : P.ys + idx * P.t_eval_len * D;
+  }
 
   __device__ __forceinline__ double atol_of(const SolveParams& P) const {
     return P.atol_v ? P.atol_v[idx] : P.atol;
@@ -100,16 +108,7 @@ struct Lane {
     t_end = P.t_end[i];
 #pragma unroll
     for (int c = 0; c < D; c++) y[c] = P.y0[i * D + c];
-    if (P.t_eval_offsets) {
-      const int64_t off = P.t_eval_offsets[i];
-      te = P.t_eval + off;
-      m = (int32_t)(P.t_eval_offsets[i + 1] - off);
-      ys = P.ys ? P.ys + off * D : nullptr;
-    } else {
-      te = P.t_eval;
-      m = (int32_t)P.t_eval_len;
-      ys = P.ys ? P.ys + i * P.t_eval_len * D : nullptr;
-    }
+    m = (int32_t)(P.t_eval_offsets ? P.t_eval_offsets[i + 1] - P.t_eval_offsets[i] : P.t_eval_len);
     n1 = 1.0;
     n2 = 1.0;
     nsteps = 0;
@@ -140,6 +139,8 @@ struct Lane {
       dt = 0.0;
     }
     cursor = 0;
+    const double* te = te_of(P);
+    double* ys = ys_of(P);
     while (cursor < m && te[cursor] == t) {  // points at t_start: copies of y0
       if (ys) {
 #pragma unroll
@@ -165,6 +166,7 @@ struct Lane {
     for (int c = 0; c < D; c++) k[0][c] = P.f0[i * D + c];
     dt = P.final_dt[i];
     cursor = (int32_t)P.n_emitted[i];
+    te_next = cursor < m ? te_of(P)[cursor] : 0.0;
     status = BODE_RUNNING;
     L1.ok = cr_log(1.0, g_pow_tables, L1.h, L1.l);  // log(1) = 0 exactly (both modes)
   }
@@ -192,7 +194,13 @@ struct Lane {
     if (accept) {
       nacc++;
       const double t_old = t;
-      if (cursor < m && h != 0.0) emit(P, t_old, h);
+      if (cursor < m && h != 0.0) {
+        // theta = (t_eval[cursor] - t_old) / h is >= 0 (earlier points were
+        // emitted); |t_eval[cursor] - t_old| > 2|h| means theta > 2, so the
+        // exact division is only needed near a point
+        const double diff = O::sub(te_next, t_old);
+        if (!(fabs(diff) > 2.0 * fabs(h))) emit(P, t_old, h);
+      }
 #pragma unroll
       for (int c = 0; c < D; c++) y[c] = yn[c];
       t = trunc ? t_end : O::add(t_old, h);
@@ -211,8 +219,10 @@ struct Lane {
   // _emit, solver.py:284-322: every point with theta in (.., 1] is
   // interpolated from the pre-commit state (y is still y_old here)
   __device__ __forceinline__ void emit(const SolveParams& P, double t_old, double h) {
+    const double* te = te_of(P);
+    double* ys = ys_of(P);
     while (cursor < m) {
-      double theta = ddiv(O::sub(te[cursor], t_old), h);
+      double theta = ddiv(O::sub(te_next, t_old), h);
       if (!(theta <= 1.0)) break;
       theta = np_max(theta, 0.0);
       double out[D];
@@ -222,6 +232,7 @@ struct Lane {
         for (int c = 0; c < D; c++) ys[cursor * D + c] = out[c];
       }
       cursor++;
+      if (cursor < m) te_next = te[cursor];
     }
   }
 
