@@ -39,7 +39,7 @@
 extern "C" {
 #endif
 
-#define BODE_ABI_VERSION 2
+#define BODE_ABI_VERSION 3
 
 /* return codes */
 #define BODE_OK 0
@@ -183,7 +183,11 @@ typedef struct bode_solve_args {
    * chunk k's solve with chunk k+1's upload and chunk k-1's download
    * (0 or 1 = no pipelining).  n_f_evals stays batch-global. */
   int32_t pipeline_chunks;
-  int32_t _pad2;
+  /* 1: solve_joint (solver.py:372-427) -- the batch as ONE problem of size
+   * n*d with one error norm, step size and accept decision; requires the
+   * same t_start / t_end for every instance, a shared t_eval (offsets NULL)
+   * and scalar tolerances; statistics are replicated per instance */
+  int32_t joint;
   /* optional outputs for combining n_f_evals across shards (multi-GPU):
    * the largest n_steps of this solve and a byte per loop iteration j in
    * [0, max_steps + 2) that is 1 iff some instance rejected at iteration

@@ -143,7 +143,7 @@ def solve(y0, t_start, t_end, t_eval, dyn, method="dopri5", atol=1e-6, rtol=1e-6
     ts = _f64(np.broadcast_to(t_start, (n,)))
     tn = _f64(np.broadcast_to(t_end, (n,)))
     a = Args()
-    a.abi_version = 2
+    a.abi_version = 3
     a.method = METHODS[method]
     a.n, a.d = n, d
     a.dyn = make_dyn(dyn["name"], dyn.get("inst"), dyn.get("shared", ()), dyn.get("mlp"), keep)

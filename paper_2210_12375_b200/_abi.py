@@ -12,7 +12,7 @@ import os
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("BODE_LIB") or os.path.join(HERE, "_build", "libbode.so")
 
-ABI_VERSION = 2
+ABI_VERSION = 3
 OK, EINVAL, ECUDA, EUNSUPPORTED = 0, 1, 2, 3
 METHOD = {"dopri5": 0, "tsit5": 1, "heun": 2}
 MODE = {"exact": 0, "fast": 1}
@@ -57,7 +57,7 @@ class SolveArgs(C.Structure):
                 ("workspace", C.c_void_p), ("workspace_bytes", C.c_size_t),
                 ("stream", C.c_void_p), ("threads_per_block", C.c_int32),
                 ("blocks", C.c_int32), ("cost_hint", C.c_void_p),
-                ("pipeline_chunks", C.c_int32), ("_pad2", C.c_int32),
+                ("pipeline_chunks", C.c_int32), ("joint", C.c_int32),
                 ("max_iterations_out", C.c_void_p), ("refresh_map_out", C.c_void_p),
                 ("mlp_backend", C.c_int32), ("_pad3", C.c_int32),
                 ("prof_event_start", C.c_void_p), ("prof_event_stop", C.c_void_p),

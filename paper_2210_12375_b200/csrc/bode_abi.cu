@@ -18,6 +18,7 @@
 
 #include "bode_dispatch.cuh"
 #include "bode_hostio.cuh"
+#include "bode_joint.cuh"
 #include "bode_mlp.cuh"
 #include "bode_sched.cuh"
 #include "bode_units.cuh"
@@ -106,6 +107,12 @@ int validate(const bode_solve_args* a) {
       (!a->dyn.W1 || !a->dyn.b1 || !a->dyn.W2 || !a->dyn.b2 || a->dyn.hidden < 1))
     return fail(BODE_EINVAL, "MLP weights required");
   if (a->pipeline_chunks < 0) return fail(BODE_EINVAL, "pipeline_chunks must be >= 0");
+  if (a->joint) {  // solver.py:391-403
+    if (a->t_eval_offsets) return fail(BODE_EINVAL, "joint mode requires identical evaluation points");
+    if (a->atol_v || a->rtol_v) return fail(BODE_EINVAL, "joint mode supports scalar tolerances only");
+    if (a->dt0_mode == BODE_DT0_ARRAY) return fail(BODE_EINVAL, "joint mode takes a scalar dt0");
+    if (a->dyn.kind == BODE_DYN_MLP) return fail(BODE_EUNSUPPORTED, "joint mode: analytic dynamics only");
+  }
   return BODE_OK;
 }
 
@@ -126,6 +133,7 @@ Layout layout(const bode_solve_args* a, int64_t n_chunk, int slots) {
   L.lpt_slot = a->cost_hint && !a->order ? ((lpt_workspace_bytes(n_chunk) + 255) & ~(size_t)255) : 0;
   L.mlp = L.lpt + L.lpt_slot * slots;
   L.total = L.mlp + (a->dyn.kind == BODE_DYN_MLP ? mlp_workspace_bytes(a) : 0);
+  if (a->joint) L.total = L.f0 + joint_workspace_bytes(a->n, a->d, a->method);
   return L;
 }
 
@@ -201,6 +209,11 @@ int run_chunk(const bode_solve_args* a, int64_t lo, int64_t hi, const Layout& L,
     if (e != cudaSuccess) return cuda_fail(e, "LPT order");
     P.order = order;
   }
+  if (a->joint) {
+    g_launches += 1;
+    e = joint_solve(a->method, a->mode, a->dyn.kind, d, P, ws + L.f0, a->n_f_evals, st);
+    return e == cudaSuccess ? BODE_OK : cuda_fail(e, "joint solve");
+  }
   if (a->dyn.kind == BODE_DYN_MLP) {
     e = mlp_solve(a, P, ws + L.mlp, st, &g_launches);
     return e == cudaSuccess ? BODE_OK : cuda_fail(e, "mlp solve");
@@ -215,6 +228,7 @@ int run_chunk(const bode_solve_args* a, int64_t lo, int64_t hi, const Layout& L,
 }
 
 int finalize(const bode_solve_args* a, cudaStream_t st) {
+  if (a->joint) return BODE_OK;  // the joint kernel counts its own n_f_evals
   char* ws = (char*)a->workspace;
   g_launches += 1;
   bode_finalize_kernel<<<1, 256, 0, st>>>((unsigned long long*)(ws + 8),
@@ -309,7 +323,7 @@ int bode_solve_host(const bode_solve_args* h) {
   const int64_t ys_rows = csr ? n_te : n * h->t_eval_len;
   const int n_inst = __builtin_popcount(h->dyn.inst_mask);
   int chunks = h->pipeline_chunks > 1 ? h->pipeline_chunks : 1;
-  if (h->order || h->trace_cap > 0 || h->dyn.kind == BODE_DYN_MLP) chunks = 1;
+  if (h->order || h->trace_cap > 0 || h->dyn.kind == BODE_DYN_MLP || h->joint) chunks = 1;
   if (chunks > n) chunks = (int)n;
   if (chunks > 64) chunks = 64;
   // largest chunk (the middle ones when the first/last are half-size)

@@ -26,7 +26,7 @@ from .dynamics import DeviceDynamics, as_device_dynamics, build_struct
 from .tableau import method_of
 
 __all__ = ["DEFAULT_MAX_STEPS", "SolveStatus", "IvpBatch", "SolveStats", "Solution",
-           "solve", "solve_device", "pinned", "host_empty"]
+           "solve", "solve_joint", "solve_device", "pinned", "host_empty"]
 
 DEFAULT_MAX_STEPS = 10_000
 # MLP path: fused persistent tcgen05 kernel (auto when d == 64), lockstep
@@ -253,7 +253,7 @@ def solve(problem: IvpBatch, f, tableau=None, tol: Tolerances | None = None,
           controller: PidCoefficients | None = None, max_steps: int = DEFAULT_MAX_STEPS,
           dt0=None, record_trace: bool = False, *, mode: str = "exact", order=None,
           cost_hint=None, pipeline_chunks="auto", with_refresh_map: bool = False,
-          mlp_backend: str = "auto") -> Solution:
+          mlp_backend: str = "auto", _joint: bool = False) -> Solution:
     """Integrate every instance independently with adaptive steps on the GPU
     (reference ``solve``, solver.py:352-369), host arrays in and out."""
     if max_steps < 1:
@@ -322,6 +322,7 @@ def solve(problem: IvpBatch, f, tableau=None, tol: Tolerances | None = None,
                 pipeline_chunks = 1
     a.pipeline_chunks = int(pipeline_chunks) if n >= 65536 else 1
     a.mlp_backend = MLP_BACKENDS[mlp_backend]
+    a.joint = 1 if _joint else 0
     ys = host_empty((max(n_rows, 1), d))
     n_emitted = host_empty(n, np.int64)
     n_steps = host_empty(n, np.int64)
@@ -346,7 +347,11 @@ def solve(problem: IvpBatch, f, tableau=None, tol: Tolerances | None = None,
     if with_refresh_map:
         extra["max_iterations"] = int(max_it[0])
         extra["refresh_map"] = rmap
-    if record_trace:
+    if record_trace and _joint:  # one trajectory, replicated (solver.py:423)
+        extra["trace_t"] = [tt[0, :n_steps[0]].copy()] * n
+        extra["trace_dt"] = [tdt[0, :n_steps[0]].copy()] * n
+        extra["trace_accept"] = [tacc[0, :n_steps[0]].astype(bool)] * n
+    elif record_trace:
         extra["trace_t"] = [tt[i, :n_steps[i]].copy() for i in range(n)]
         extra["trace_dt"] = [tdt[i, :n_steps[i]].copy() for i in range(n)]
         extra["trace_accept"] = [tacc[i, :n_steps[i]].astype(bool) for i in range(n)]
@@ -357,6 +362,37 @@ def solve(problem: IvpBatch, f, tableau=None, tol: Tolerances | None = None,
         offs = None
     return Solution(ys[:n_rows], offs, te.size if problem.te_shared else 0, n_emitted, stats,
                     status, d)
+
+
+def solve_joint(problem: IvpBatch, f, tableau=None, tol: Tolerances | None = None,
+                controller: PidCoefficients | None = None, max_steps: int = DEFAULT_MAX_STEPS,
+                dt0=None, record_trace: bool = False, *, mode: str = "exact") -> Solution:
+    """Integrate the batch as one concatenated problem of size ``n * d``
+    (reference ``solve_joint``, solver.py:372-427): one RMS error norm over
+    all components, one shared step size and accept decision, statistics of
+    the shared trajectory replicated per instance -- the naive-batching
+    behaviour independent solving avoids.  Same validation as the reference;
+    one single-CTA kernel on the GPU (csrc/bode_joint.cu)."""
+    n = problem.batch_size
+    if np.any(problem.t_start != problem.t_start[0]) or np.any(
+            problem.t_end != problem.t_end[0]):
+        raise ValueError("joint mode requires identical integration bounds")
+    te0 = np.asarray(problem.t_eval[0], dtype=float)
+    if not problem.te_shared:
+        counts = problem.eval_counts()
+        if np.any(counts != te0.size):
+            raise ValueError("joint mode requires identical evaluation points")
+        vals = problem.te_values.reshape(n, te0.size) if te0.size else None
+        if vals is not None and np.any(vals != te0[None, :]):
+            raise ValueError("joint mode requires identical evaluation points")
+    if np.asarray(tol.atol if tol else 0.0).ndim > 0 or np.asarray(
+            tol.rtol if tol else 0.0).ndim > 0:
+        raise ValueError("joint mode supports scalar tolerances only")
+    if dt0 is not None and np.ndim(dt0) > 0:  # the flat problem has one row
+        dt0 = float(np.asarray(dt0, dtype=float).reshape(-1)[0])
+    flat = IvpBatch(problem.y0, problem.t_start, problem.t_end, te0)
+    return solve(flat, f, tableau, tol, controller, max_steps, dt0, record_trace, mode=mode,
+                 _joint=True)
 
 
 def solve_device(y0, t_start, t_end, f, *, t_eval=None, t_eval_offsets=None, method="dopri5",

@@ -227,7 +227,65 @@ def mlp_golden(n=64):
                 n_f_evals=sol.stats.n_f_evals)
 
 
+def run_joint(sc, problem=None):
+    """batchode.solve_joint on a scenario; stores inputs and outputs."""
+    n, d = sc["y0"].shape
+    if problem is None:
+        problem = bo.IvpBatch(y0=sc["y0"], t_start=sc["t_start"], t_end=sc["t_end"],
+                              t_eval=sc["t_eval"])
+    f = S.numpy_dynamics(sc["dyn"], n)
+    tol = bo.Tolerances(atol=sc["atol"], rtol=sc["rtol"])
+    sol = bo.solve_joint(problem, f, tableau=tableau(sc["method"]), tol=tol,
+                         controller=controller(sc["ctrl"]), max_steps=sc["max_steps"],
+                         dt0=sc["dt0"], record_trace=sc["trace"])
+    te0 = np.asarray(problem.t_eval[0], float)
+    ys = np.full((n, te0.size, d), np.nan)
+    n_emitted = np.zeros(n, dtype=np.int64)
+    for i in range(n):
+        ys[i, :sol.ys[i].shape[0]] = sol.ys[i]
+        n_emitted[i] = sol.ys[i].shape[0]
+    spec = sc["dyn"]
+    c = sc["ctrl"]
+    out = dict(
+        y0=problem.y0, t_start=problem.t_start, t_end=problem.t_end, te=te0,
+        dyn_name=np.array(spec["name"]),
+        dyn_inst=spec["inst"] if spec["inst"] is not None else np.zeros((0, 0)),
+        dyn_shared=np.array(spec["shared"], float), method=np.array(sc["method"]),
+        atol=np.asarray(sc["atol"], float), rtol=np.asarray(sc["rtol"], float),
+        betas=np.array(c["betas"], float), hist=np.array(c["hist"]),
+        max_steps=np.array(sc["max_steps"]), dt0=np.array(np.nan if sc["dt0"] is None else sc["dt0"]),
+        trace=np.array(sc["trace"]),
+        ys=ys, n_emitted=n_emitted, n_steps=sol.stats.n_steps, n_accepted=sol.stats.n_accepted,
+        n_f_evals=sol.stats.n_f_evals, final_dt=sol.stats.final_dt, status=sol.status,
+    )
+    if sc["trace"]:
+        for key in ("trace_t", "trace_dt", "trace_accept"):
+            out[key] = np.asarray(sol.stats.extra[key][0])
+    return out
+
+
+def joint_goldens():
+    os.makedirs(os.path.join(HERE, "joint"), exist_ok=True)
+    scs = list(S.joint_scenarios())
+    # the paper's pathology (tests/test_acceptance.py:103-113): 4 VdP on the
+    # mu = 25 limit cycle, tol 1e-5; inputs from the reference's vdp_batch
+    batch = bo.vdp_batch(4, 25.0)
+    path = S._scn("joint_pathology_vdp4_mu25", batch.y0, batch.t_start, batch.t_end,
+                  batch.t_eval, S.dyn("vdp", np.full(4, 25.0)), atol=1e-5, rtol=1e-5,
+                  max_steps=1_000_000)
+    for sc in scs + [path]:
+        out = run_joint(sc, batch if sc is path else None)
+        if sc is path:  # the independent solve, for the step ratio
+            ind = bo.solve(batch, S.numpy_dynamics(sc["dyn"], 4), tol=bo.Tolerances(1e-5, 1e-5),
+                           max_steps=1_000_000)
+            out["independent_n_steps"] = ind.stats.n_steps
+        np.savez_compressed(os.path.join(HERE, "joint", sc["name"] + ".npz"), **out)
+        print(f"{sc['name']:28s} n={sc['y0'].shape[0]:4d} steps={out['n_steps'][0]:6d} "
+              f"status={out['status'][0]} nfe={out['n_f_evals'][0]}")
+
+
 def main():
+    joint_goldens()
     os.makedirs(os.path.join(HERE, "solve"), exist_ok=True)
     for sc in S.all_solve_scenarios():
         out = run_scenario(sc)
@@ -247,4 +305,7 @@ def main():
 
 
 if __name__ == "__main__":
-    main()
+    if len(sys.argv) > 1 and sys.argv[1] == "joint":
+        joint_goldens()
+    else:
+        main()

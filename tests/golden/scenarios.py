@@ -301,3 +301,32 @@ def numpy_dynamics(spec, n):
     else:
         raise KeyError(name)
     return f
+
+
+# ------------------------------------------------ joint mode (solve_joint) --
+def joint_scenarios():
+    """solve_joint (solver.py:372-427) parity cases; the pathology case's
+    inputs come from the reference's vdp_batch and are stored in its fixture."""
+    rng = np.random.default_rng(5)
+    out = []
+    mu = rng.uniform(1.0, 10.0, 32)
+    out.append(_scn("joint_vdp32_I", np.tile([2.0, 0.0], (32, 1)), 0.0, 10.0,
+                    [np.linspace(0.0, 10.0, 20)] * 32, dyn("vdp", mu), max_steps=100_000))
+    y0 = 1.0 + 0.1 * rng.normal(size=(8, 3))
+    out.append(_scn("joint_lorenz_tsit5_trace", y0, 0.0, 2.0, [np.linspace(0.5, 2.0, 4)] * 8,
+                    dyn("lorenz", None, (10.0, 28.0, 8.0 / 3.0)), method="tsit5", atol=1e-8,
+                    rtol=1e-8, trace=True))
+    mu = rng.uniform(1.0, 5.0, 16)
+    out.append(_scn("joint_vdp16_pi42_dt0", np.tile([2.0, 0.0], (16, 1)), 0.0, 5.0,
+                    [np.array([2.5, 5.0])] * 16, dyn("vdp", mu), ctrl=_ctrl(PI42), dt0=0.01))
+    out.append(_scn("joint_single_linear", [[1.0, 2.0]], 0.0, 1.0, [np.array([0.5, 1.0])],
+                    dyn("linear", None, (-1.0,))))
+    out.append(_scn("joint_heun_harmonic", rng.normal(size=(8, 2)), 0.0, 3.0,
+                    [np.linspace(0.0, 3.0, 7)] * 8, dyn("harmonic"), method="heun", atol=1e-4,
+                    rtol=1e-4))
+    mu = rng.uniform(1.0, 3.0, 300)  # N = 600 > 128: multi-leaf pairwise tree
+    out.append(_scn("joint_vdp300_wide", np.tile([2.0, 0.0], (300, 1)), 0.0, 3.0, None,
+                    dyn("vdp", mu), atol=1e-7, rtol=1e-7))
+    out.append(_scn("joint_square_blowup", [[0.5], [1.0], [0.8]], 0.0, 2.0, [np.array([0.5])] * 3,
+                    dyn("square", None, (1e300,)), max_steps=100_000))
+    return out

@@ -101,3 +101,20 @@ def test_dynamics_packing_and_callables_rejected():
         bode.solve(bode.IvpBatch(np.ones((1, 1)), [0.0], [1.0], [np.empty(0)]), lambda t, y: y)
     with pytest.raises(TypeError):
         bode.vdp_dynamics(bode.VdpParams(2.0))(np.zeros(1), np.ones((1, 2)))
+
+
+def test_solve_joint_validation_matches_reference():
+    """solve_joint raises the reference's ValueErrors (solver.py:391-403)
+    before touching the device."""
+    import paper_2210_12375_b200 as bode
+    f = bode.vdp_dynamics(bode.VdpParams(np.array([1.0, 2.0])))
+    y0 = np.tile([2.0, 0.0], (2, 1))
+    with pytest.raises(ValueError, match="identical integration bounds"):
+        bode.solve_joint(bode.IvpBatch(y0, np.zeros(2), np.array([1.0, 2.0]),
+                                       [np.empty(0)] * 2), f)
+    with pytest.raises(ValueError, match="identical evaluation points"):
+        bode.solve_joint(bode.IvpBatch(y0, np.zeros(2), np.ones(2),
+                                       [np.array([0.5]), np.array([0.6])]), f)
+    with pytest.raises(ValueError, match="scalar tolerances"):
+        bode.solve_joint(bode.IvpBatch(y0, np.zeros(2), np.ones(2), [np.empty(0)] * 2), f,
+                         tol=bode.Tolerances(np.array([1e-6, 1e-6]), 1e-6))
