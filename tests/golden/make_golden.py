@@ -284,8 +284,38 @@ def joint_goldens():
               f"status={out['status'][0]} nfe={out['n_f_evals'][0]}")
 
 
+CLI_RUNS = {
+    # name: reference cli argv (output paths appended); compared by tests/test_gpu_cli.py
+    "vdp_ind": ["vdp-batching", "--n", "4", "--mu", "25"],
+    "vdp_joint": ["vdp-batching", "--n", "4", "--mu", "25", "--mode", "joint"],
+    "vdp_random_tsit5_pi42": ["vdp-batching", "--n", "6", "--mu", "5", "--random-phases", "--seed",
+                              "3", "--controller", "pid:PI42", "--method", "tsit5", "--n-eval", "0"],
+    "pid_sweep": ["pid-sweep", "--mu", "5,25"],
+}
+
+
+def cli_goldens():
+    """Run the reference CLI (cli.py) and keep its CSV output, plus the batch
+    builders' arrays (problems.py:53-143)."""
+    import batchode.cli as bcli
+    out_dir = os.path.join(HERE, "cli")
+    os.makedirs(out_dir, exist_ok=True)
+    for name, argv in CLI_RUNS.items():
+        extra = ["--out", os.path.join(out_dir, name + ".csv")]
+        if argv[0] == "vdp-batching":
+            extra += ["--trace-out", os.path.join(out_dir, name + "_trace.csv")]
+        rc = bcli.main(argv + extra)
+        print(f"cli {name}: rc={rc}")
+    anchor, period = bo.vdp_limit_cycle(25.0)
+    batch = bo.vdp_batch(4, 25.0, n_eval=5)
+    np.savez_compressed(os.path.join(out_dir, "problems.npz"), anchor=np.array(anchor),
+                        period=np.array(period), y0=batch.y0, t_end=batch.t_end,
+                        t_eval=np.array(batch.t_eval))
+
+
 def main():
     joint_goldens()
+    cli_goldens()
     os.makedirs(os.path.join(HERE, "solve"), exist_ok=True)
     for sc in S.all_solve_scenarios():
         out = run_scenario(sc)
@@ -307,5 +337,7 @@ def main():
 if __name__ == "__main__":
     if len(sys.argv) > 1 and sys.argv[1] == "joint":
         joint_goldens()
+    elif len(sys.argv) > 1 and sys.argv[1] == "cli":
+        cli_goldens()
     else:
         main()

@@ -118,3 +118,20 @@ def test_solve_joint_validation_matches_reference():
     with pytest.raises(ValueError, match="scalar tolerances"):
         bode.solve_joint(bode.IvpBatch(y0, np.zeros(2), np.ones(2), [np.empty(0)] * 2), f,
                          tol=bode.Tolerances(np.array([1e-6, 1e-6]), 1e-6))
+
+
+def test_cli_parser_mirrors_reference_flags():
+    """Flag validation of the experiment CLI (reference cli.py:242-288) runs
+    before any solve: bad values exit with argparse's code 2."""
+    from paper_2210_12375_b200 import cli
+    p = cli.build_parser()
+    a = p.parse_args(["vdp-batching", "--out", "x.csv"])
+    assert (a.n, a.mu, a.mode, a.method, a.n_eval, a.max_steps) == (4, 25.0, "independent",
+                                                                     "dopri5", 200, 100_000)
+    for bad in (["vdp-batching", "--n", "0", "--out", "x"],
+                ["vdp-batching", "--controller", "pid:nope", "--out", "x"],
+                ["looptime", "--steps", "-1", "--out", "x"]):
+        with pytest.raises(SystemExit) as e:
+            p.parse_args(bad)
+        assert e.value.code == 2
+    assert cli.main(["pid-sweep", "--presets", "nope", "--out", "/dev/null"]) == 2
