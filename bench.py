@@ -258,12 +258,18 @@ def run_bode(args, rank, world, local_rank):
     import paper_2210_12375_b200 as bode
     from paper_2210_12375_b200 import _abi
 
-    dev = torch.device("cuda", local_rank)
+    # BODE_BENCH_SHARED_GPU=1 (tests only): every rank on cuda:0 with gloo
+    # collectives, to exercise the multi-rank path on a one-GPU box
+    shared_gpu = os.environ.get("BODE_BENCH_SHARED_GPU") == "1"
+    dev = torch.device("cuda", 0 if shared_gpu else local_rank)
     torch.cuda.set_device(dev)
     dist = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=dev)
+        if shared_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
     lib = _abi.load()
     cfg = make_config(args.config, rank)
     cfg["_name"] = args.config
@@ -443,7 +449,7 @@ def run_bode(args, rank, world, local_rank):
                    sample=f"first {k} instances of the seeded batch, one solve "
                           f"({s:.2f} s wall, C oracle restating batchode, pthreads)")
 
-    clocks = clk.summary(local_rank)
+    clocks = clk.summary(dev.index)
     if rank == 0:
         line = dict(
             metric="accepted instance-steps/sec", value=value, unit="instance-steps/s",
