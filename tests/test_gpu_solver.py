@@ -257,6 +257,30 @@ def test_pipelined_host_path_matches_single_chunk():
         assert np.array_equal(a.status, b.status) and np.array_equal(a.n_emitted, b.n_emitted)
 
 
+def test_host_transfer_paths_are_equivalent(monkeypatch):
+    """Page-locked inputs (direct DMA), pageable inputs through the pinned
+    staging arena, and pageable inputs beyond the arena limit (driver-staged
+    copies) give bit-identical results (csrc/bode_hostio.cu)."""
+    rng = np.random.default_rng(22)
+    n = 70_001
+    mu = rng.uniform(1.0, 10.0, n)
+    t_end = rng.uniform(5.0, 20.0, n)
+    te = [np.sort(rng.uniform(0.0, x, rng.integers(0, 3))) for x in t_end]
+    y0 = np.tile([2.0, 0.0], (n, 1))
+    f = bode.vdp_dynamics(bode.VdpParams(mu))
+    a = bode.solve(bode.IvpBatch(y0, np.zeros(n), t_end, te), f, controller=PI42)
+    P = bode.pinned
+    b = bode.solve(bode.IvpBatch(P(y0), P(np.zeros(n)), P(t_end), te),
+                   bode.vdp_dynamics(bode.VdpParams(P(mu))), controller=PI42)
+    monkeypatch.setenv("BODE_STAGING_MAX", "4096")  # nothing fits: driver-staged copies
+    c = bode.solve(bode.IvpBatch(y0, np.zeros(n), t_end, te), f, controller=PI42)
+    for o in (b, c):
+        assert np.array_equal(a.ys_flat, o.ys_flat)
+        for k in ("n_steps", "n_accepted", "n_f_evals", "final_dt"):
+            assert np.array_equal(getattr(a.stats, k), getattr(o.stats, k)), k
+        assert np.array_equal(a.status, o.status) and np.array_equal(a.n_emitted, o.n_emitted)
+
+
 @pytest.mark.parametrize("backend", ["fused", "tcgen05", "cuda_core"])
 def test_mlp_neural_ode_vs_reference_fp32(backend):
     """C4 (neural ODE, D=64, H=256, tanh): the reference solve with a NumPy
