@@ -60,11 +60,28 @@ constexpr int kItemsMax = 16;     // weight items per stage (H / 16)
 // wider unit means fewer, more efficient MMAs (measured on B200: a
 // kind::tf32 M=128 MMA costs 46 / 54 / 66 cycles at N = 32 / 64 / 128 --
 // smem operand bandwidth -- for 1x / 2x / 4x the work).
+//
+// Where 64 more columns fit, the tanh outputs H_c (GEMM2's A operand, TF32
+// hi/lo for each group's 16 columns) are kept in TMEM as well
+// (tcgen05.mma with A in tensor memory): GEMM2 then reads only the weights
+// from shared memory, and the H stores never touch it.  For dopri5/tsit5
+// that holds for stages 1-5 (widths 128, 128, 64, 64, 32); stage 6 keeps H in
+// shared memory.
+__host__ __device__ __forceinline__ bool h_in_tmem(int s, int H, int* width) {
+  const int used = 64 * (s + 1);
+  for (int w = 128; w >= 32; w >>= 1)
+    if (H % w == 0 && used + 2 * w + 64 <= 512) {
+      *width = w;
+      return true;
+    }
+  const int free_cols = 512 - used;
+  *width = (free_cols >= 256 && H % 128 == 0) ? 128 : (free_cols >= 128 && H % 64 == 0) ? 64 : 32;
+  return false;
+}
 __host__ __device__ __forceinline__ int unit_width(int s, int H) {
-  const int free_cols = 512 - 64 * (s + 1);
-  if (free_cols >= 256 && H % 128 == 0) return 128;
-  if (free_cols >= 128 && H % 64 == 0) return 64;
-  return 32;
+  int w;
+  h_in_tmem(s, H, &w);
+  return w;
 }
 
 struct Smem {
@@ -296,8 +313,10 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_fused_kernel(const MlpFusedAr
         mbar_arrive(&sm.a_full);
         PROF_MARK(2)
         // ============ tanh epilogues of the hidden chunks
-        const int Wd = unit_width(s, A.H), spu = Wd / kHc;
-        const uint32_t acc1_base = 512 - 2 * Wd;
+        int Wd;
+        const bool htm = h_in_tmem(s, A.H, &Wd);
+        const int spu = Wd / kHc;
+        const uint32_t acc1_base = 512 - 2 * Wd, h_base = acc1_base - 64;
         for (int c = 0; c < nc; c++) {
           const int u = c / spu, b = u & 1;
           if (c % spu == 0) {
@@ -316,10 +335,22 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_fused_kernel(const MlpFusedAr
             mbar_wait(&sm.g2done[wg], (g2_base + c - 1) & 1);
           }
           PROF_MARK(5)
+          if (htm) {  // TF32 hi/lo into this group's TMEM columns (A of GEMM2)
+            float hi[16], lo[16];
 #pragma unroll
-          for (int q = 0; q < 4; q++)
-            store_hilo(sm.h[wg][0], sm.h[wg][1], cm_off(row, 4 * q, 16), v + 4 * q);
-          fence_async_smem();
+            for (int j = 0; j < 16; j++) {
+              hi[j] = tf32_hi(v[j]);
+              lo[j] = v[j] - hi[j];
+            }
+            tmem_st16(lrow + h_base + 32 * wg, hi);
+            tmem_st16(lrow + h_base + 32 * wg + 16, lo);
+            tmem_wait_st();
+          } else {
+#pragma unroll
+            for (int q = 0; q < 4; q++)
+              store_hilo(sm.h[wg][0], sm.h[wg][1], cm_off(row, 4 * q, 16), v + 4 * q);
+            fence_async_smem();
+          }
           fence_before();
           mbar_arrive(&sm.epidone[wg]);
           PROF_MARK(6)
@@ -357,9 +388,11 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_fused_kernel(const MlpFusedAr
         const uint64_t dA_hi = smem_desc(smem_u32(sm.a[0]), 2048);
         const uint64_t dA_lo = smem_desc(smem_u32(sm.a[1]), 2048);
         const uint64_t dW2 = smem_desc(smem_u32(sm.w[0]), 1024);
-        const int Wd = unit_width(s, A.H), spu = Wd / kHc, nu = A.H / Wd;
+        int Wd;
+        const bool htm = h_in_tmem(s, A.H, &Wd);
+        const int spu = Wd / kHc, nu = A.H / Wd;
         const int KS = 2048 / Wd;                     // K per 16 KB item
-        const uint32_t acc1_base = 512 - 2 * Wd;
+        const uint32_t acc1_base = 512 - 2 * Wd, h_base = acc1_base - 64;
         // GEMM1 unit u: acc1[u&1] (N = Wd) = Y_s W1[u Wd .. u Wd + Wd)^T,
         // K-step major, the three 3xTF32 products inner
         auto gemm1 = [&](int u) {
@@ -391,15 +424,26 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_fused_kernel(const MlpFusedAr
           const uint64_t wh = dW2 + (uint64_t)((sl * kWItem) >> 4), wl = wh + (kW2 >> 4);
           const uint64_t hh = smem_desc(smem_u32(sm.h[g][0]), 512), hl = smem_desc(smem_u32(sm.h[g][1]), 512);
           const uint32_t acc = tmem + 64 * s;
+          const uint32_t th = tmem + h_base + 32 * g, tl = th + 16;  // TMEM H (htm)
           PROF_MARK(20)
           if (elect_one()) {
             fence_after();
+            if (htm) {
 #pragma unroll
-            for (int kk = 0; kk < 2; kk++) {
-              const int k = 2 * g + kk;
-              mma_tf32(acc, hh + 16 * kk, wh + 16 * k, idesc(kD), (c | k) ? 1u : 0u);
-              mma_tf32(acc, hh + 16 * kk, wl + 16 * k, idesc(kD), 1u);
-              mma_tf32(acc, hl + 16 * kk, wh + 16 * k, idesc(kD), 1u);
+              for (int kk = 0; kk < 2; kk++) {
+                const int k = 2 * g + kk;
+                mma_tf32_ts(acc, th + 8 * kk, wh + 16 * k, idesc(kD), (c | k) ? 1u : 0u);
+                mma_tf32_ts(acc, th + 8 * kk, wl + 16 * k, idesc(kD), 1u);
+                mma_tf32_ts(acc, tl + 8 * kk, wh + 16 * k, idesc(kD), 1u);
+              }
+            } else {
+#pragma unroll
+              for (int kk = 0; kk < 2; kk++) {
+                const int k = 2 * g + kk;
+                mma_tf32(acc, hh + 16 * kk, wh + 16 * k, idesc(kD), (c | k) ? 1u : 0u);
+                mma_tf32(acc, hh + 16 * kk, wl + 16 * k, idesc(kD), 1u);
+                mma_tf32(acc, hl + 16 * kk, wh + 16 * k, idesc(kD), 1u);
+              }
             }
             mma_commit(&sm.g2done[g]);
             if (g == 1) {
