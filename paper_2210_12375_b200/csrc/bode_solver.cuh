@@ -245,6 +245,11 @@ struct Lane {
   }
 };
 
+#ifdef BODE_EXIT_PROF
+static __device__ unsigned long long g_exit_times[65536];
+static __device__ unsigned g_exit_count;
+#endif
+
 template <int M, class F, class O>
 // 2-D systems fit 5 blocks of 128 threads per SM (<= 102 registers); wider
 // ones keep 4 (<= 128 registers) to avoid spilling the stage vectors.
@@ -311,6 +316,14 @@ __global__ void __launch_bounds__(128, (F::D <= 2 ? BODE_BLOCKS_2D : 4)) bode_pe
       }
     }
   }
+#ifdef BODE_EXIT_PROF
+  if (lane == 0) {  // debug builds: when did each warp run out of work
+    unsigned long long ts;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ts));
+    const unsigned slot = atomicAdd(&g_exit_count, 1u);
+    if (slot < 65536) g_exit_times[slot] = ts;
+  }
+#endif
   // max n_steps: warp reduce then one atomic per warp
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
