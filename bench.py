@@ -293,10 +293,21 @@ def run_bode(args, rank, world, local_rank):
 
     is_mlp = cfg["dyn"] == "mlp"
 
+    from paper_2210_12375_b200 import distributed as bdist
+
     def one_step(prof=None):
-        return bode.solve_device(y0, ts, tn, dyn, method=cfg["method"], atol=cfg["tol"],
-                                 rtol=cfg["tol"], controller=ctrl, max_steps=cfg["max_steps"],
-                                 mode=args.mode, cost_hint=cost, prof_events=prof, **te_kw)
+        out = bode.solve_device(y0, ts, tn, dyn, method=cfg["method"], atol=cfg["tol"],
+                                rtol=cfg["tol"], controller=ctrl, max_steps=cfg["max_steps"],
+                                mode=args.mode, cost_hint=cost, prof_events=prof,
+                                with_refresh_map=world > 1, **te_kw)
+        if world > 1:
+            # the sharded batch's one real exchange: the batch-global n_f_evals
+            # (MAX all-reduce of iteration counts and refresh maps, NCCL)
+            out["n_f_evals"] = bdist.global_f_evals_device(
+                out, stages=2 if cfg["method"] == "heun" else 7, fsal=cfg["method"] != "heun")
+            if args.gather:  # optional: gather ys/stats to rank 0 over NVLink
+                bdist.gather_device(out, dst=0)
+        return out
 
     times, kern_times, accepted, attempted = [], [], 0, 0
     kern_ms = 0.0
@@ -487,6 +498,8 @@ def main():
     p.add_argument("--lpt", type=int, default=1, help="cost-sorted (LPT) instance queue")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
+    p.add_argument("--gather", action="store_true",
+                   help="N>1: also gather every shard's ys/stats to rank 0 inside the timed step")
     args = p.parse_args()
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))

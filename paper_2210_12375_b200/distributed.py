@@ -24,7 +24,8 @@ import numpy as np
 
 from .solver import IvpBatch, Solution, SolveStats
 
-__all__ = ["partition", "combine_f_evals", "subset_problem", "solve_sharded"]
+__all__ = ["partition", "combine_f_evals", "subset_problem", "solve_sharded",
+           "global_f_evals_device", "gather_device"]
 
 
 def partition(n: int, world: int, cost=None) -> list:
@@ -132,3 +133,55 @@ def solve_sharded(problem: IvpBatch, f, *, group=None, cost_hint=None, gather_to
     stats = SolveStats(n_steps=n_steps, n_accepted=n_acc,
                        n_f_evals=np.full(n, nfe, dtype=np.int64), final_dt=fdt)
     return Solution(flat, offs, 0, n_emit, stats, status, d)
+
+
+# ------------------------------------------------- device-side (NCCL) path --
+def global_f_evals_device(out, stages: int = 7, fsal: bool = True, group=None):
+    """The sharded solve's one real exchange, on device tensors: MAX
+    all-reduce of the shards' loop-iteration counts and refresh maps (a byte
+    per iteration, so MAX == OR), then n_f_evals = 1 + (S-1) max + #refresh
+    iterations in [1, max) (FSAL) -- the reference's batch-global count
+    (solver.py:184,224,239).  ``out`` is a ``solve_device(...,
+    with_refresh_map=True)`` result; returns a 0-d int64 device tensor, no
+    host sync."""
+    import torch
+    import torch.distributed as dist
+
+    mx = out["max_iterations"].clone()
+    rmap = out["refresh_map"].clone()
+    if dist.is_initialized() and dist.get_world_size(group) > 1:
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX, group=group)
+        dist.all_reduce(rmap, op=dist.ReduceOp.MAX, group=group)
+    if not fsal:
+        return 1 + stages * mx[0]
+    it = torch.arange(rmap.numel(), device=rmap.device)
+    refresh = ((rmap != 0) & (it >= 1) & (it < mx[0])).sum()
+    return 1 + (stages - 1) * mx[0] + refresh
+
+
+def gather_device(out, dst: int = 0, group=None, keys=("n_steps", "n_accepted", "final_dt",
+                                                        "status", "n_emitted", "ys")):
+    """Gather the shards' per-instance results to rank ``dst`` with device
+    collectives (NCCL over NVLink on the GPU box): returns a dict of
+    concatenated tensors in rank order on ``dst``, None elsewhere.  Shards
+    may differ in length (each rank's row count is exchanged first)."""
+    import torch
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    res = {} if rank == dst else None
+    for k in keys:
+        t = out[k].contiguous()
+        rows = torch.tensor([t.shape[0]], dtype=torch.int64, device=t.device)
+        sizes = [torch.zeros_like(rows) for _ in range(world)]
+        dist.all_gather(sizes, rows, group=group)
+        sizes = [int(x.item()) for x in sizes]
+        mrow = max(sizes)
+        pad = torch.zeros((mrow,) + tuple(t.shape[1:]), dtype=t.dtype, device=t.device)
+        pad[:t.shape[0]] = t
+        bufs = [torch.empty_like(pad) for _ in range(world)] if rank == dst else None
+        dist.gather(pad, bufs, dst=dst, group=group)
+        if rank == dst:
+            res[k] = torch.cat([b[:s_] for b, s_ in zip(bufs, sizes)])
+    return res

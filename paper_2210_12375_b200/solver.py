@@ -400,7 +400,7 @@ def solve_device(y0, t_start, t_end, f, *, t_eval=None, t_eval_offsets=None, met
                  max_steps: int = DEFAULT_MAX_STEPS, dt0=None, order=None, cost_hint=None,
                  mode: str = "exact", record_trace: bool = False, stream=None,
                  threads_per_block: int = 0, blocks: int = 0, mlp_backend: str = "auto",
-                 prof_events=None):
+                 prof_events=None, with_refresh_map: bool = False):
     """Device-resident solve on torch CUDA tensors; asynchronous (no host
     sync).  ``t_eval``: None, a 1-D tensor shared by all instances, a 2-D
     (n, m) tensor, or CSR values with ``t_eval_offsets`` (n+1).  ``atol`` /
@@ -495,6 +495,11 @@ def solve_device(y0, t_start, t_end, f, *, t_eval=None, t_eval_offsets=None, met
         out["trace_accept"] = torch.zeros((n, cap), dtype=torch.uint8, device=dev)
         a.trace_t, a.trace_dt = out["trace_t"].data_ptr(), out["trace_dt"].data_ptr()
         a.trace_accept, a.trace_cap = out["trace_accept"].data_ptr(), cap
+    if with_refresh_map:  # for the cross-shard n_f_evals (distributed.global_f_evals_device)
+        out["max_iterations"] = torch.zeros(1, dtype=torch.int64, device=dev)
+        out["refresh_map"] = torch.zeros(int(max_steps) + 2, dtype=torch.uint8, device=dev)
+        a.max_iterations_out = out["max_iterations"].data_ptr()
+        a.refresh_map_out = out["refresh_map"].data_ptr()
     a.threads_per_block, a.blocks = int(threads_per_block), int(blocks)
     a.mlp_backend = MLP_BACKENDS[mlp_backend]
     if prof_events is not None:  # (torch.cuda.Event, torch.cuda.Event) around the integrator
