@@ -444,7 +444,7 @@ def run_bode(args, rank, world, local_rank):
                + (cfg["mu"].nbytes if cfg["mu"] is not None else 0)
                + (sum(w.nbytes for w in cfg["mlp"]) if cfg.get("mlp") else 0)
                + (8 * n if args.lpt and cfg["cost"] is not None else 0))
-        d2h = 8 * pts * d + n * (8 + 8 + 8 + 8 + 4) + 8
+        d2h = 8 * pts * d + n * (8 + 8 + 8 + 8 + 8) + 8  # ys + 5 int64/f64 stats + n_f_evals
         e2e = dict(value=e2e_acc / tot, unit="instance-steps/s", h2d_bytes_per_step=int(h2d),
                    d2h_bytes_per_step=int(d2h), ms_per_step=1e3 * tot / len(e2e_t),
                    path="paper_2210_12375_b200.solve -> bode_solve_host (NumPy arrays in "
