@@ -552,7 +552,11 @@ __device__ __forceinline__ void rk_step(const F& f, double t, double h, const do
     for (int i = 1; i < S; i++) {
       if (T::zb(i) != 0.0) s = O::mad(T::b(i), k[i][c], s);
       if (T::ze(i) != 0.0) e = O::mad(T::e(i), k[i][c], e);
-      if (T::zb(i) == 0.0 || T::ze(i) == 0.0) skipped_nonfinite |= !isfinite(k[i][c]);
+      // (exact mode only: in fast mode a non-finite stage already makes err
+      // non-finite through the following stages, so the step is rejected and
+      // y_next is never observed)
+      if (!O::kFast && (T::zb(i) == 0.0 || T::ze(i) == 0.0))
+        skipped_nonfinite |= !isfinite(k[i][c]);
     }
     y_next[c] = O::mad(h, s, y[c]);
     err[c] = O::mul(h, e);
