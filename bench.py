@@ -375,6 +375,11 @@ def run_bode(args, rank, world, local_rank):
         traffic = tj["dram_read_bytes"] + tj["dram_write_bytes"]
     except Exception:
         pass
+    ncu_pipes = None  # pipe utilisation of the same kernel from the committed ncu capture
+    try:
+        ncu_pipes = json.load(open(os.path.join(ROOT, "profiles", "ncu_pipes.json")))[args.config]
+    except Exception:
+        pass
     if is_mlp:
         # tensor-pipe bound: algorithmic MLP GEMM flops (4*D*H per f-eval, 6 FSAL
         # stages per attempted step) of the fused persistent kernel (the init
@@ -390,7 +395,7 @@ def run_bode(args, rank, world, local_rank):
                          "tensor-pipe work = 3 x achieved) / fused-kernel time (CUDA events "
                          "around its launch); peak = tcgen05 kind::tf32 M=128 N=256 throughput "
                          "measured in-run by bode_probe_tf32",
-                    mma_issue_frac=3 * achieved / peak, kernel_ms=kern_ms)
+                    mma_issue_frac=3 * achieved / peak, kernel_ms=kern_ms, ncu=ncu_pipes)
     else:
         peak_fp64 = fp64_peak(torch, lib, dev)
         flops_launch = flops_per_step(cfg["dyn"], d) * att_launch + flops_per_point(d) * pts
@@ -401,8 +406,9 @@ def run_bode(args, rank, world, local_rank):
                          "15d+51 per point; pow, div, sqrt not counted) / persistent-kernel time "
                          "(CUDA events around its launch); peak = DFMA throughput measured in-run "
                          "by bode_probe_fp64 (2 flops/DFMA); traffic = ncu dram bytes/launch "
-                         "(profiles/traffic.json); ncu FP64-pipe utilisation in profiles/",
-                    kernel_ms=kern_ms)
+                         "(profiles/traffic.json); ncu = FP64-pipe / issue utilisation of the "
+                         "same kernel (profiles/ncu_pipes.json)",
+                    kernel_ms=kern_ms, ncu=ncu_pipes)
 
     # ---- end to end through the reference-facing solve() with host buffers
     e2e = None
