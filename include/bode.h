@@ -39,7 +39,7 @@
 extern "C" {
 #endif
 
-#define BODE_ABI_VERSION 3
+#define BODE_ABI_VERSION 4
 
 /* return codes */
 #define BODE_OK 0
@@ -209,7 +209,37 @@ typedef struct bode_solve_args {
   void* prof_event_stop;
   /* optional HOST pointer: number of kernels this call launched */
   int64_t* launch_count_out;
+  /* optional (gradients, bode_solve_adjoint): record every accepted step.
+   * Row traj_offsets[i] + k (k < n_accepted[i]) receives the k-th accepted
+   * step of instance i as BODE_TRAJ_EXTRA + d doubles: t_old, h, the t_eval
+   * cursor before the step, y_old[d].  traj_offsets (n+1) is the exclusive
+   * prefix sum of n_accepted from an earlier identical solve (the solve is
+   * deterministic).  Analytic dynamics only; not with joint. */
+  double* traj;
+  const int64_t* traj_offsets;
 } bode_solve_args;
+
+#define BODE_TRAJ_EXTRA 3
+
+/* Reverse-mode gradients of a solve ("AutoDiffAdjoint" backward; the
+ * reference has no gradients, SPEC.md:13 / SURVEY.md 8(f) row 1).
+ * Discretise-then-optimise through the recorded accepted steps: every RK
+ * stage, the solution update and the Horner dense output are differentiated
+ * exactly; the step sizes, accept decisions and interpolation positions
+ * theta are held fixed (no gradient through the step-size controller). */
+typedef struct bode_adjoint_args {
+  const double* traj;          /* recorded by bode_solve (fwd->traj) */
+  const int64_t* traj_offsets; /* (n+1,) */
+  const int64_t* n_emitted;    /* (n,) from the forward solve */
+  const double* grad_ys;       /* dL/dys, same layout as the forward ys */
+  double* grad_y0;             /* (n, d) out: dL/dy0 */
+  double* grad_params;         /* (n, 8) out or NULL: dL/dp_k of instance i
+                                  (slot k of bode_dynamics; a shared slot's
+                                  gradient is the column sum) */
+  void* workspace;             /* bode_adjoint_workspace_size bytes, device */
+  size_t workspace_bytes;
+  int64_t* launch_count_out;   /* optional HOST pointer */
+} bode_adjoint_args;
 
 #define BODE_MLP_AUTO 0
 #define BODE_MLP_CUDA_CORE 1
@@ -228,6 +258,13 @@ int bode_solve(const bode_solve_args* args);
 /* Same, but every pointer in args is a HOST pointer: copies inputs to the
  * device, solves, copies outputs back and synchronises (end-to-end path). */
 int bode_solve_host(const bode_solve_args* args);
+
+size_t bode_adjoint_workspace_size(const bode_solve_args* fwd);
+
+/* dL/dy0 and dL/dparams for the solve described by fwd (the same
+ * arguments as the recording bode_solve: method, dynamics, t_eval layout,
+ * stream); device buffers, asynchronous on fwd->stream. */
+int bode_solve_adjoint(const bode_solve_args* fwd, const bode_adjoint_args* adj);
 
 /* One embedded RK trial step on the full batch (Stepper.step):
  * k0 = f0 for FSAL methods, else f(t, y).  k: (stages, n, d). */

@@ -66,7 +66,8 @@ class Args(C.Structure):
                 ("max_iterations_out", C.c_void_p), ("refresh_map_out", C.c_void_p),
                 ("mlp_backend", C.c_int32), ("_pad3", C.c_int32),
                 ("prof_event_start", C.c_void_p), ("prof_event_stop", C.c_void_p),
-                ("launch_count_out", C.c_void_p)]
+                ("launch_count_out", C.c_void_p),
+                ("traj", C.c_void_p), ("traj_offsets", C.c_void_p)]
 
 
 _lib = None
@@ -143,7 +144,7 @@ def solve(y0, t_start, t_end, t_eval, dyn, method="dopri5", atol=1e-6, rtol=1e-6
     ts = _f64(np.broadcast_to(t_start, (n,)))
     tn = _f64(np.broadcast_to(t_end, (n,)))
     a = Args()
-    a.abi_version = 3
+    a.abi_version = 4
     a.method = METHODS[method]
     a.n, a.d = n, d
     a.dyn = make_dyn(dyn["name"], dyn.get("inst"), dyn.get("shared", ()), dyn.get("mlp"), keep)

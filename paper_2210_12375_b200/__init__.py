@@ -13,7 +13,7 @@ from .dynamics import (AnalyticProblem, DeviceDynamics, VdpParams, analytic_prob
                        lorenz_dynamics, mlp_dynamics, relaxation_dynamics,
                        sin_plus_t_dynamics, square_dynamics, vdp_dynamics, zero_dynamics)
 from .solver import (DEFAULT_MAX_STEPS, IvpBatch, Solution, SolveStats, SolveStatus, host_empty,
-                     pinned, solve, solve_device, solve_joint)
+                     pinned, solve, solve_device, solve_joint, adjoint_device)
 from .tableau import ButcherTableau, dopri5, heun, tsit5
 
 __version__ = "0.1.0"
@@ -25,5 +25,5 @@ __all__ = [
     "linear_dynamics", "logistic_dynamics", "lorenz_dynamics", "mlp_dynamics",
     "relaxation_dynamics", "sin_plus_t_dynamics", "square_dynamics", "vdp_dynamics",
     "zero_dynamics", "DEFAULT_MAX_STEPS", "IvpBatch", "Solution", "SolveStats", "SolveStatus",
-    "solve", "solve_joint", "solve_device", "pinned", "host_empty", "ButcherTableau", "dopri5", "heun", "tsit5",
+    "solve", "solve_joint", "solve_device", "adjoint_device", "pinned", "host_empty", "ButcherTableau", "dopri5", "heun", "tsit5",
 ]

@@ -12,7 +12,8 @@ import os
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("BODE_LIB") or os.path.join(HERE, "_build", "libbode.so")
 
-ABI_VERSION = 3
+ABI_VERSION = 4
+TRAJ_EXTRA = 3
 OK, EINVAL, ECUDA, EUNSUPPORTED = 0, 1, 2, 3
 METHOD = {"dopri5": 0, "tsit5": 1, "heun": 2}
 MODE = {"exact": 0, "fast": 1}
@@ -61,6 +62,15 @@ class SolveArgs(C.Structure):
                 ("max_iterations_out", C.c_void_p), ("refresh_map_out", C.c_void_p),
                 ("mlp_backend", C.c_int32), ("_pad3", C.c_int32),
                 ("prof_event_start", C.c_void_p), ("prof_event_stop", C.c_void_p),
+                ("launch_count_out", C.c_void_p),
+                ("traj", C.c_void_p), ("traj_offsets", C.c_void_p)]
+
+
+class AdjointArgs(C.Structure):
+    _fields_ = [("traj", C.c_void_p), ("traj_offsets", C.c_void_p),
+                ("n_emitted", C.c_void_p), ("grad_ys", C.c_void_p),
+                ("grad_y0", C.c_void_p), ("grad_params", C.c_void_p),
+                ("workspace", C.c_void_p), ("workspace_bytes", C.c_size_t),
                 ("launch_count_out", C.c_void_p)]
 
 
@@ -73,6 +83,8 @@ SIGNATURES = {
     "bode_workspace_size": ([C.POINTER(SolveArgs)], _SZ),
     "bode_solve": ([C.POINTER(SolveArgs)], C.c_int),
     "bode_solve_host": ([C.POINTER(SolveArgs)], C.c_int),
+    "bode_adjoint_workspace_size": ([C.POINTER(SolveArgs)], _SZ),
+    "bode_solve_adjoint": ([C.POINTER(SolveArgs), C.POINTER(AdjointArgs)], C.c_int),
     "bode_rk_step": ([_I32, _I32, _P, _I64, _I64, _P, _P, _P, _P, _P, _P, _P, _P], C.c_int),
     "bode_interpolate": ([_I32, _I32, _I64, _I64, _P, _P, _P, _P, _P, _P], C.c_int),
     "bode_error_norm": ([_I64, _I64, _P, _P, _P, _P, _P, _D, _D, _P, _P], C.c_int),

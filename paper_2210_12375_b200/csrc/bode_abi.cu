@@ -16,6 +16,7 @@
 #include <string>
 #include <vector>
 
+#include "bode_adjoint.cuh"
 #include "bode_dispatch.cuh"
 #include "bode_hostio.cuh"
 #include "bode_joint.cuh"
@@ -107,6 +108,9 @@ int validate(const bode_solve_args* a) {
       (!a->dyn.W1 || !a->dyn.b1 || !a->dyn.W2 || !a->dyn.b2 || a->dyn.hidden < 1))
     return fail(BODE_EINVAL, "MLP weights required");
   if (a->pipeline_chunks < 0) return fail(BODE_EINVAL, "pipeline_chunks must be >= 0");
+  if (a->traj && !a->traj_offsets) return fail(BODE_EINVAL, "traj needs traj_offsets");
+  if (a->traj && (a->dyn.kind == BODE_DYN_MLP || a->joint))
+    return fail(BODE_EUNSUPPORTED, "trajectory recording: analytic dynamics, independent solve only");
   if (a->joint) {  // solver.py:391-403
     if (a->t_eval_offsets) return fail(BODE_EINVAL, "joint mode requires identical evaluation points");
     if (a->atol_v || a->rtol_v) return fail(BODE_EINVAL, "joint mode supports scalar tolerances only");
@@ -191,6 +195,8 @@ int run_chunk(const bode_solve_args* a, int64_t lo, int64_t hi, const Layout& L,
   P.trace_t = a->trace_t ? a->trace_t + lo * a->trace_cap : nullptr;
   P.trace_dt = a->trace_dt ? a->trace_dt + lo * a->trace_cap : nullptr;
   P.trace_accept = a->trace_accept ? a->trace_accept + lo * a->trace_cap : nullptr;
+  P.traj = a->traj;
+  P.traj_offsets = a->traj_offsets ? a->traj_offsets + lo : nullptr;
   P.queue = (unsigned long long*)(ws + qoff);
   P.max_n = (unsigned long long*)(ws + 8);
   P.refresh = (uint32_t*)(ws + Workspace::kHeader);
@@ -312,9 +318,47 @@ int bode_solve(const bode_solve_args* a) {
   return rc;
 }
 
+size_t bode_adjoint_workspace_size(const bode_solve_args* a) {
+  if (validate(a) != BODE_OK) return 0;
+  return adjoint_workspace_bytes(a->n);
+}
+
+int bode_solve_adjoint(const bode_solve_args* a, const bode_adjoint_args* g) {
+  int rc = validate(a);
+  if (rc != BODE_OK) return rc;
+  if (!g) return fail(BODE_EINVAL, "null adjoint args");
+  if (a->dyn.kind == BODE_DYN_MLP || a->joint)
+    return fail(BODE_EUNSUPPORTED, "gradients: analytic dynamics, independent solve only");
+  if (!g->traj || !g->traj_offsets || !g->n_emitted || !g->grad_y0)
+    return fail(BODE_EINVAL, "adjoint needs traj, traj_offsets, n_emitted and grad_y0");
+  if ((a->t_eval_offsets || a->t_eval_len > 0) && !g->grad_ys)
+    return fail(BODE_EINVAL, "adjoint needs grad_ys");
+  if (!g->workspace || g->workspace_bytes < adjoint_workspace_bytes(a->n))
+    return fail(BODE_EINVAL, "workspace too small (see bode_adjoint_workspace_size)");
+  AdjParams A;
+  memset(&A, 0, sizeof(A));
+  A.n = a->n;
+  A.dyn = make_dyn(a->dyn);
+  A.t_eval = a->t_eval;
+  A.t_eval_offsets = a->t_eval_offsets;
+  A.t_eval_len = a->t_eval_offsets ? 0 : a->t_eval_len;
+  A.traj = g->traj;
+  A.traj_offsets = g->traj_offsets;
+  A.n_emitted = g->n_emitted;
+  A.grad_ys = g->grad_ys;
+  A.grad_y0 = g->grad_y0;
+  A.grad_params = g->grad_params;
+  int64_t launches = 0;
+  cudaError_t e = adjoint_launch(a->method, a->d, A, g->workspace, (cudaStream_t)a->stream,
+                                 &launches);
+  if (g->launch_count_out) *g->launch_count_out = launches;
+  return e == cudaSuccess ? BODE_OK : cuda_fail(e, "adjoint launch");
+}
+
 int bode_solve_host(const bode_solve_args* h) {
   int rc = validate(h);
   if (rc != BODE_OK) return rc;
+  if (h->traj) return fail(BODE_EUNSUPPORTED, "trajectory recording: device buffers (bode_solve) only");
   g_launches = 0;
   retain_pool();
   const int64_t n = h->n, d = h->d;

@@ -1,0 +1,34 @@
+// bode_adjoint.cuh -- reverse-mode gradients of a batched solve (bode_adjoint.cu).
+#pragma once
+#include <cstddef>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "bode_device.cuh"
+
+namespace bode {
+
+struct AdjParams {
+  int64_t n;
+  DynParams dyn;
+  const double* t_eval;
+  const int64_t* t_eval_offsets;  // CSR rows, or NULL: one shared array of t_eval_len
+  int64_t t_eval_len;
+  const double* traj;             // (rows, kTrajExtra + D), see SolveParams::traj
+  const int64_t* traj_offsets;    // (n+1,)
+  const int64_t* n_emitted;
+  const double* grad_ys;          // ys layout
+  double* grad_y0;                // (n, D)
+  double* grad_params;            // (n, 8) or NULL
+  const int64_t* order;           // queue order (longest first) or NULL
+  unsigned long long* queue;
+};
+
+size_t adjoint_workspace_bytes(int64_t n);
+// Builds the longest-first queue from the trajectory lengths, then launches
+// the persistent backward kernel; returns the number of kernels launched
+// through *launches.
+cudaError_t adjoint_launch(int method, int64_t d, AdjParams A, void* ws, cudaStream_t st,
+                           int64_t* launches);
+
+}  // namespace bode

@@ -208,6 +208,14 @@ struct VdP {  // problems.py:45-48: (v, mu*(1-x*x)*v - x)
     f[0] = v;
     f[1] = O::sub(O::mul(O::mul(mu, O::sub(1.0, O::mul(x, x))), v), x);
   }
+  // adjoint (bode_adjoint.cu): yb = J^T g, pb[slot] += (df/dp)^T g
+  __device__ __forceinline__ void vjp(double, const double* y, const double* g, double* yb,
+                                      double* pb) const {
+    const double x = y[0], v = y[1], q = 1.0 - x * x;
+    yb[0] = g[1] * (-2.0 * mu * x * v - 1.0);
+    yb[1] = g[0] + g[1] * mu * q;
+    pb[0] += g[1] * q * v;
+  }
 };
 
 template <class O>
@@ -231,6 +239,16 @@ struct Lorenz {  // (s*(y-x), x*(r-z)-y, x*y - b*z)
       f[2] = O::sub(O::mul(x, yy), O::mul(b, z));
     }
   }
+  __device__ __forceinline__ void vjp(double, const double* y, const double* g, double* yb,
+                                      double* pb) const {
+    const double x = y[0], yy = y[1], z = y[2];
+    yb[0] = -s * g[0] + (r - z) * g[1] + yy * g[2];
+    yb[1] = s * g[0] - g[1] + x * g[2];
+    yb[2] = -x * g[1] - b * g[2];
+    pb[0] += (yy - x) * g[0];
+    pb[1] += x * g[1];
+    pb[2] += -z * g[2];
+  }
 };
 
 template <class O>
@@ -241,6 +259,11 @@ struct Harmonic {  // problems.py:169-170
     f[0] = y[1];
     f[1] = -y[0];
   }
+  __device__ __forceinline__ void vjp(double, const double*, const double* g, double* yb,
+                                      double*) const {
+    yb[0] = -g[1];
+    yb[1] = g[0];
+  }
 };
 
 template <class O>
@@ -250,6 +273,11 @@ struct Damped {  // (y1, -y0 - 0.1*y1*|y1|)
   __device__ __forceinline__ void operator()(double, const double* y, double* f) const {
     f[0] = y[1];
     f[1] = O::sub(-y[0], O::mul(O::mul(0.1, y[1]), fabs(y[1])));
+  }
+  __device__ __forceinline__ void vjp(double, const double* y, const double* g, double* yb,
+                                      double*) const {
+    yb[0] = -g[1];
+    yb[1] = g[0] - 0.2 * fabs(y[1]) * g[1];  // d(y|y|)/dy = 2|y|
   }
 };
 
@@ -311,6 +339,69 @@ struct Elementwise {
       default:
 #pragma unroll
         for (int j = 0; j < D; j++) f[j] = __longlong_as_double(0x7ff8000000000000LL);
+    }
+  }
+  __device__ __forceinline__ void vjp(double t, const double* y, const double* g, double* yb,
+                                      double* pb) const {
+    double sg = 0.0;  // sum of g over components (shared-term gradients)
+#pragma unroll
+    for (int j = 0; j < D; j++) sg += g[j];
+    switch (kind) {
+      case BODE_DYN_ZERO:
+#pragma unroll
+        for (int j = 0; j < D; j++) yb[j] = 0.0;
+        break;
+      case BODE_DYN_CONST:
+#pragma unroll
+        for (int j = 0; j < D; j++) yb[j] = 0.0;
+        pb[0] += sg;
+        break;
+      case BODE_DYN_LINEAR:
+      case BODE_DYN_LINEAR_COS:
+      case BODE_DYN_LINEAR_SIN:
+#pragma unroll
+        for (int j = 0; j < D; j++) {
+          yb[j] = p[0] * g[j];
+          pb[0] += y[j] * g[j];
+        }
+        if (kind == BODE_DYN_LINEAR_COS) {
+          double sn, cs;
+          sincos(p[2] * t, &sn, &cs);
+          pb[1] += cs * sg;
+          pb[2] -= p[1] * sn * t * sg;
+        } else if (kind == BODE_DYN_LINEAR_SIN) {
+          double sn, cs;
+          sincos(p[2] * t, &sn, &cs);
+          pb[1] += sn * sg;
+          pb[2] += p[1] * cs * t * sg;
+        }
+        break;
+      case BODE_DYN_RELAX_COS: {
+        double sn, cs;
+        sincos(p[1] * t, &sn, &cs);
+#pragma unroll
+        for (int j = 0; j < D; j++) {
+          yb[j] = p[0] * g[j];
+          pb[0] += (y[j] - cs) * g[j];
+        }
+        pb[1] += p[0] * sn * t * sg;
+        break;
+      }
+      case BODE_DYN_SQUARE:
+#pragma unroll
+        for (int j = 0; j < D; j++) yb[j] = 2.0 * y[j] * g[j];
+        break;
+      case BODE_DYN_LOGISTIC:
+#pragma unroll
+        for (int j = 0; j < D; j++) yb[j] = (1.0 - 2.0 * y[j]) * g[j];
+        break;
+      case BODE_DYN_SIN_PLUS_T:
+#pragma unroll
+        for (int j = 0; j < D; j++) yb[j] = cos(y[j]) * g[j];
+        break;
+      default:
+#pragma unroll
+        for (int j = 0; j < D; j++) yb[j] = __longlong_as_double(0x7ff8000000000000LL);
     }
   }
 };

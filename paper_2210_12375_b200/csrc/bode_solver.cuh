@@ -48,6 +48,11 @@ struct SolveParams {
   double* trace_dt;
   uint8_t* trace_accept;
   int64_t trace_cap;
+  // optional accepted-step trajectory for the adjoint (bode_adjoint.cu):
+  // row traj_offsets[i] + k = the k-th accepted step of instance i, laid out
+  // as [t_old, h, cursor before the step, y_old[D]] (kTrajExtra + D doubles)
+  double* traj;
+  const int64_t* traj_offsets;
   // workspace
   unsigned long long* queue;   // next instance position
   unsigned long long* max_n;   // max n_steps over the batch
@@ -57,6 +62,8 @@ struct SolveParams {
   void* ev_start;              // host side only: optional cudaEvent_t around
   void* ev_stop;               // the persistent launch (bench roofline)
 };
+
+constexpr int kTrajExtra = 3;
 
 struct Workspace {
   static constexpr size_t kHeader = 64;
@@ -174,7 +181,8 @@ struct Lane {
   // one iteration of step_once for this row (solver.py:208-282); returns
   // true when the row just rejected and is still running (FSAL refresh at
   // the next iteration, solver.py:220-226)
-  __device__ __forceinline__ bool step(const SolveParams& P, const PowTables& PT, bool tracing) {
+  __device__ __forceinline__ bool step(const SolveParams& P, const PowTables& PT, bool tracing,
+                                       bool recording) {
     const int32_t j = nsteps;
     const double remaining = O::sub(t_end, t);
     const bool trunc = fabs(dt) >= fabs(remaining);
@@ -192,6 +200,14 @@ struct Lane {
       if (P.trace_accept) P.trace_accept[o] = accept;
     }
     if (accept) {
+      if (recording) {  // (adjoint only) the pre-commit state of this step
+        double* r = P.traj + (P.traj_offsets[idx] + nacc) * (kTrajExtra + D);
+        r[0] = t;
+        r[1] = h;
+        r[2] = (double)cursor;
+#pragma unroll
+        for (int c = 0; c < D; c++) r[kTrajExtra + c] = y[c];
+      }
       nacc++;
       const double t_old = t;
       if (cursor < m && h != 0.0) {
@@ -270,6 +286,7 @@ __global__ void __launch_bounds__(128, (F::D <= 2 ? BODE_BLOCKS_2D : 4)) bode_pe
 
   Lane<M, F, O> L;
   const bool tracing = P.trace_cap > 0;  // uniform: hoisted out of the step loop
+  const bool recording = P.traj != nullptr;
   bool have = false, done = false;
   unsigned long long my_max = 0;
   const unsigned lt_mask = (1u << lane) - 1u;
@@ -300,7 +317,7 @@ __global__ void __launch_bounds__(128, (F::D <= 2 ? BODE_BLOCKS_2D : 4)) bode_pe
     }
     if (have) {
       const int64_t j = L.nsteps;
-      if (L.step(P, s_pow, tracing)) {
+      if (L.step(P, s_pow, tracing, recording)) {
         const uint64_t bit = (uint64_t)j + 1;
         const uint32_t w = (uint32_t)(bit >> 5), msk = 1u << (bit & 31);
         if (P.smem_words > 0) {

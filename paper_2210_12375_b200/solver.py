@@ -26,7 +26,7 @@ from .dynamics import DeviceDynamics, as_device_dynamics, build_struct
 from .tableau import method_of
 
 __all__ = ["DEFAULT_MAX_STEPS", "SolveStatus", "IvpBatch", "SolveStats", "Solution",
-           "solve", "solve_joint", "solve_device", "pinned", "host_empty"]
+           "solve", "solve_joint", "solve_device", "adjoint_device", "pinned", "host_empty"]
 
 DEFAULT_MAX_STEPS = 10_000
 # MLP path: fused persistent tcgen05 kernel (auto when d == 64), lockstep
@@ -400,13 +400,17 @@ def solve_device(y0, t_start, t_end, f, *, t_eval=None, t_eval_offsets=None, met
                  max_steps: int = DEFAULT_MAX_STEPS, dt0=None, order=None, cost_hint=None,
                  mode: str = "exact", record_trace: bool = False, stream=None,
                  threads_per_block: int = 0, blocks: int = 0, mlp_backend: str = "auto",
-                 prof_events=None, with_refresh_map: bool = False):
+                 prof_events=None, with_refresh_map: bool = False,
+                 record_trajectory: bool = False):
     """Device-resident solve on torch CUDA tensors; asynchronous (no host
     sync).  ``t_eval``: None, a 1-D tensor shared by all instances, a 2-D
     (n, m) tensor, or CSR values with ``t_eval_offsets`` (n+1).  ``atol`` /
     ``rtol`` / ``dt0``: Python floats or (n,) tensors.  Returns a dict of
     device tensors: ys, n_emitted, n_steps, n_accepted, final_dt, status,
-    n_f_evals (+ trace_* when ``record_trace``)."""
+    n_f_evals (+ trace_* when ``record_trace``).  ``record_trajectory``:
+    also record every accepted step for :func:`adjoint_device` (a second,
+    recording pass of the same deterministic solve, sized from the first
+    pass's n_accepted -- one host sync)."""
     import torch
 
     lib = _abi.load()
@@ -516,6 +520,16 @@ def solve_device(y0, t_start, t_end, f, *, t_eval=None, t_eval_offsets=None, met
     nlaunch = _abi.C.c_int64(0)
     a.launch_count_out = _abi.C.addressof(nlaunch)
     _abi.check(lib.bode_solve(_abi.C.byref(a)))
+    if record_trajectory:
+        toff = torch.zeros(n + 1, dtype=torch.int64, device=dev)
+        torch.cumsum(out["n_accepted"], 0, out=toff[1:])
+        rows = int(toff[-1])
+        traj = torch.empty((max(rows, 1), _abi.TRAJ_EXTRA + d), **f64)
+        keep += [toff, traj]
+        a.traj, a.traj_offsets = traj.data_ptr(), toff.data_ptr()
+        _abi.check(lib.bode_solve(_abi.C.byref(a)))
+        out["traj"], out["traj_offsets"] = traj[:rows], toff
+        out["_args"], out["_keep"] = a, keep
     # keep inputs alive until the stream has consumed them
     for t in keep:
         if isinstance(t, torch.Tensor):
@@ -525,3 +539,47 @@ def solve_device(y0, t_start, t_end, f, *, t_eval=None, t_eval_offsets=None, met
     out["offsets"] = offsets
     out["shared_len"] = shared_len
     return out
+
+
+def adjoint_device(fwd: dict, grad_ys):
+    """Reverse-mode gradients of a recorded device solve
+    (``solve_device(..., record_trajectory=True)``): returns
+    ``(grad_y0 (n, d), grad_params (n, 8))`` for ``grad_ys`` = dL/dys in
+    the forward ys layout.  Column k of grad_params is dL/dp_k per instance
+    for parameter slot k of the dynamics (``dynamics.SLOTS`` order); for a
+    parameter shared by the batch its gradient is the column sum.  Step
+    sizes and accept decisions are constants (no gradient through the
+    step-size controller); see include/bode.h ``bode_solve_adjoint``."""
+    import torch
+
+    lib = _abi.load()
+    if "_args" not in fwd:
+        raise ValueError("the forward solve was not recorded (record_trajectory=True)")
+    a = fwd["_args"]
+    n, d = int(a.n), int(a.d)
+    dev = fwd["n_emitted"].device
+    g = _abi.AdjointArgs()
+    keep = []
+    g.traj, g.traj_offsets = fwd["traj"].data_ptr(), fwd["traj_offsets"].data_ptr()
+    g.n_emitted = fwd["n_emitted"].data_ptr()
+    if fwd["ys"].numel():
+        gy = grad_ys.to(dtype=torch.float64, device=dev).reshape(fwd["ys"].shape).contiguous()
+        keep.append(gy)
+        g.grad_ys = gy.data_ptr()
+    grad_y0 = torch.empty((n, d), dtype=torch.float64, device=dev)
+    grad_params = torch.empty((n, 8), dtype=torch.float64, device=dev)
+    g.grad_y0, g.grad_params = grad_y0.data_ptr(), grad_params.data_ptr()
+    wsb = lib.bode_adjoint_workspace_size(_abi.C.byref(a))
+    if wsb == 0:
+        _abi.check(_abi.EINVAL)
+    ws = torch.empty(wsb, dtype=torch.uint8, device=dev)
+    keep.append(ws)
+    g.workspace, g.workspace_bytes = ws.data_ptr(), wsb
+    nlaunch = _abi.C.c_int64(0)
+    g.launch_count_out = _abi.C.addressof(nlaunch)
+    _abi.check(lib.bode_solve_adjoint(_abi.C.byref(a), _abi.C.byref(g)))
+    st = torch.cuda.current_stream(dev)
+    for t in keep:
+        t.record_stream(st)
+    fwd["adjoint_launches"] = int(nlaunch.value)
+    return grad_y0, grad_params

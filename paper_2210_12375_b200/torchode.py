@@ -15,16 +15,24 @@ onto the reference's semantics (SURVEY.md §8(b) mapping table):
 
 Everything is torch CUDA tensors and stays on the device (no host sync in
 ``solve``).  ``f`` must be a registered device functor
-(:mod:`paper_2210_12375_b200.dynamics`); gradients through the solve are not
-part of the reference and are not provided.
+(:mod:`paper_2210_12375_b200.dynamics`).
+
+Gradients (the reference has none): when
+``y0`` or a dynamics parameter given as a tensor requires grad,
+``AutoDiffAdjoint.solve`` records the accepted steps and ``ys`` becomes
+differentiable; ``backward`` runs the sm_100a adjoint kernel
+(``bode_solve_adjoint``, csrc/bode_adjoint.cu): exact reverse mode through
+every RK stage, solution update and dense-output interpolant, with the
+step sizes and accept decisions held fixed (discretise-then-optimise, no
+gradient through the step-size controller).  Analytic dynamics only.
 """
 
 from dataclasses import dataclass
 
 from . import _abi  # noqa: F401  (fails loudly without the CUDA library)
 from .controller import PID_PRESETS, PidCoefficients
-from .dynamics import DeviceDynamics, as_device_dynamics
-from .solver import DEFAULT_MAX_STEPS, SolveStatus, solve_device
+from .dynamics import SLOTS, DeviceDynamics, _is_tensor, as_device_dynamics
+from .solver import DEFAULT_MAX_STEPS, SolveStatus, adjoint_device, solve_device
 
 __all__ = ["ODETerm", "InitialValueProblem", "Dopri5", "Tsit5", "Heun", "IntegralController",
            "PIDController", "AutoDiffAdjoint", "Solution", "Status"]
@@ -148,7 +156,8 @@ class Solution:
 
 class AutoDiffAdjoint:
     """Solver facade (torchode's name).  ``solve`` runs the batch through the
-    persistent sm_100a integrator; it is forward only."""
+    persistent sm_100a integrator; when y0 or a parameter tensor requires
+    grad, ys is differentiable (adjoint kernel, see the module docstring)."""
 
     def __init__(self, step_method: _StepMethod, step_size_controller: IntegralController,
                  max_steps: int | None = None, mode: str = "exact"):
@@ -166,19 +175,64 @@ class AutoDiffAdjoint:
             raise ValueError("no ODETerm given")
         n = problem.batch_size
         te = problem.t_eval
-        out = solve_device(problem.y0, problem.t_start, problem.t_end, term.f, t_eval=te,
-                           method=self.step_method.method, atol=self.controller.atol,
-                           rtol=self.controller.rtol, controller=self.controller.coeffs,
-                           max_steps=self.max_steps, dt0=dt0, cost_hint=cost_hint,
-                           mode=self.mode)
+        kw = dict(t_eval=te, method=self.step_method.method, atol=self.controller.atol,
+                  rtol=self.controller.rtol, controller=self.controller.coeffs,
+                  max_steps=self.max_steps, dt0=dt0, cost_hint=cost_hint, mode=self.mode)
+        dyn = term.f
+        grads = [(name, v) for name, v in dyn.params.items()
+                 if _is_tensor(v) and v.requires_grad]
+        if torch.is_grad_enabled() and (problem.y0.requires_grad or grads):
+            spec = dict(problem=problem, dyn=dyn, kw=kw,
+                        slots=[SLOTS[dyn.kind].index(name) for name, _ in grads])
+            ys_flat = _AdjointSolve.apply(spec, problem.y0, *[v for _, v in grads])
+            out = spec["out"]
+        else:
+            out = solve_device(problem.y0, problem.t_start, problem.t_end, dyn, **kw)
+            ys_flat = out["ys"]
         d = problem.y0.shape[1]
         if te is None:
-            ys = out["ys"].new_empty((n, 0, d))
+            ys = ys_flat.new_empty((n, 0, d))
         else:
             m = te.shape[-1]
-            ys = out["ys"].reshape(n, m, d)
+            ys = ys_flat.reshape(n, m, d)
             reached = torch.arange(m, device=ys.device)[None, :] < out["n_emitted"][:, None]
             ys = torch.where(reached[:, :, None], ys, torch.full_like(ys, float("nan")))
         stats = {k: out[k] for k in ("n_steps", "n_accepted", "final_dt", "n_emitted")}
         stats["n_f_evals"] = out["n_f_evals"].expand(n)
         return Solution(ts=te, ys=ys, status=out["status"].to(torch.int64), stats=stats)
+
+
+class _AdjointSolve:
+    """torch.autograd.Function: ys = solve(y0, params); backward = the
+    sm_100a adjoint kernel over the recorded trajectory."""
+
+    @staticmethod
+    def apply(spec, y0, *params):
+        import torch
+
+        class Fn(torch.autograd.Function):
+            @staticmethod
+            def forward(ctx, y0_, *params_):
+                p = spec["problem"]
+                dyn = spec["dyn"]
+                plain = {k: (v.detach() if _is_tensor(v) else v) for k, v in dyn.params.items()}
+                dyn0 = DeviceDynamics(dyn.kind, plain, dyn.mlp)
+                out = solve_device(y0_.detach(), p.t_start, p.t_end, dyn0,
+                                   record_trajectory=True, **spec["kw"])
+                spec["out"] = out
+                ctx.fwd, ctx.y0_dtype = out, y0_.dtype
+                ctx.shapes = [q.shape for q in params_]
+                return out["ys"]
+
+            @staticmethod
+            def backward(ctx, g):
+                gy0, gp = adjoint_device(ctx.fwd, g)
+                pg = []
+                for slot, shape in zip(spec["slots"], ctx.shapes):
+                    col = gp[:, slot]
+                    pg.append(col.sum().reshape(shape) if len(shape) == 0 or
+                              (len(shape) == 1 and shape[0] == 1 and gp.shape[0] != 1)
+                              else col.reshape(shape))
+                return (gy0.to(ctx.y0_dtype), *pg)
+
+        return Fn.apply(y0, *params)
