@@ -211,8 +211,9 @@ typedef struct bode_solve_args {
   int64_t* launch_count_out;
   /* optional (gradients, bode_solve_adjoint): record every accepted step.
    * Row traj_offsets[i] + k (k < n_accepted[i]) receives the k-th accepted
-   * step of instance i as BODE_TRAJ_EXTRA + d doubles: t_old, h, the t_eval
-   * cursor before the step, y_old[d].  traj_offsets (n+1) is the exclusive
+   * step of instance i: t_old, h, the t_eval cursor before the step,
+   * y_old[d], padded to BODE_TRAJ_STRIDE(d) doubles (whole 32-byte sectors,
+   * so the scattered per-instance row writes never partially fill one).  traj_offsets (n+1) is the exclusive
    * prefix sum of n_accepted from an earlier identical solve (the solve is
    * deterministic).  Analytic dynamics only; not with joint. */
   double* traj;
@@ -220,6 +221,7 @@ typedef struct bode_solve_args {
 } bode_solve_args;
 
 #define BODE_TRAJ_EXTRA 3
+#define BODE_TRAJ_STRIDE(d) ((((d) + BODE_TRAJ_EXTRA) + 3) / 4 * 4)
 
 /* Reverse-mode gradients of a solve ("AutoDiffAdjoint" backward; the
  * reference has no gradients, SPEC.md:13 / SURVEY.md 8(f) row 1).

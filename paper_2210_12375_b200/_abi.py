@@ -14,6 +14,11 @@ LIB_PATH = os.environ.get("BODE_LIB") or os.path.join(HERE, "_build", "libbode.s
 
 ABI_VERSION = 4
 TRAJ_EXTRA = 3
+
+
+def traj_stride(d: int) -> int:
+    """BODE_TRAJ_STRIDE(d): doubles per recorded accepted step."""
+    return (d + TRAJ_EXTRA + 3) // 4 * 4
 OK, EINVAL, ECUDA, EUNSUPPORTED = 0, 1, 2, 3
 METHOD = {"dopri5": 0, "tsit5": 1, "heun": 2}
 MODE = {"exact": 0, "fast": 1}

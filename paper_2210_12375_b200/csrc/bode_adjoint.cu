@@ -33,7 +33,7 @@ namespace {
 template <int M, class F>
 __device__ __forceinline__ void adjoint_instance(const AdjParams& A, int64_t i) {
   using T = Tab<M>;
-  constexpr int D = F::D, S = T::S, NI = T::NI, W = kTrajExtra + D;
+  constexpr int D = F::D, S = T::S, NI = T::NI, W = kTrajStride<D>;
   F f;
   f.load(A.dyn, i);
   const double* te = A.t_eval_offsets ? A.t_eval + A.t_eval_offsets[i] : A.t_eval;
@@ -47,7 +47,12 @@ __device__ __forceinline__ void adjoint_instance(const AdjParams& A, int64_t i) 
   for (int c = 0; c < D; c++) ab[c] = 0.0;
 
   for (int64_t r = nrec - 1; r >= 0; r--) {
-    const double* rec = A.traj + (r0 + r) * W;
+    double rec[W];
+#pragma unroll
+    for (int q = 0; q < W; q += 4)  // whole sectors, one 256-bit load each
+      asm volatile("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];"
+                   : "=d"(rec[q]), "=d"(rec[q + 1]), "=d"(rec[q + 2]), "=d"(rec[q + 3])
+                   : "l"(A.traj + (r0 + r) * W + q));
     const double t = rec[0], h = rec[1];
     const int64_t lo = (int64_t)rec[2];
     double y[D];
@@ -140,7 +145,6 @@ __device__ __forceinline__ void adjoint_instance(const AdjParams& A, int64_t i) 
 template <int M, class F>
 __global__ void __launch_bounds__(128) bode_adjoint_kernel(const AdjParams A) {
   const int lane = threadIdx.x & 31;
-  const unsigned lt = (1u << lane) - 1u;
   // one queue claim per warp and round: instances are independent, the
   // longest trajectories go first, a lane that finishes takes the next one
   while (true) {
@@ -149,7 +153,6 @@ __global__ void __launch_bounds__(128) bode_adjoint_kernel(const AdjParams A) {
     base = __shfl_sync(0xffffffffu, base, 0);
     if (base >= (unsigned long long)A.n) break;
     const unsigned long long pos = base + lane;
-    (void)lt;
     if (pos < (unsigned long long)A.n) {
       const int64_t i = A.order ? A.order[pos] : (int64_t)pos;
       adjoint_instance<M, F>(A, i);

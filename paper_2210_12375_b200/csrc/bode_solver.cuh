@@ -50,7 +50,7 @@ struct SolveParams {
   int64_t trace_cap;
   // optional accepted-step trajectory for the adjoint (bode_adjoint.cu):
   // row traj_offsets[i] + k = the k-th accepted step of instance i, laid out
-  // as [t_old, h, cursor before the step, y_old[D]] (kTrajExtra + D doubles)
+  // as [t_old, h, cursor before the step, y_old[D], pad] (kTrajStride<D>)
   double* traj;
   const int64_t* traj_offsets;
   // workspace
@@ -63,7 +63,9 @@ struct SolveParams {
   void* ev_stop;               // the persistent launch (bench roofline)
 };
 
-constexpr int kTrajExtra = 3;
+constexpr int kTrajExtra = BODE_TRAJ_EXTRA;
+template <int D>
+constexpr int kTrajStride = BODE_TRAJ_STRIDE(D);
 
 struct Workspace {
   static constexpr size_t kHeader = 64;
@@ -181,8 +183,10 @@ struct Lane {
   // one iteration of step_once for this row (solver.py:208-282); returns
   // true when the row just rejected and is still running (FSAL refresh at
   // the next iteration, solver.py:220-226)
+  // trec (recording only): shared-memory slot holding this lane's
+  // trajectory row base, set at resume -- no per-step global load
   __device__ __forceinline__ bool step(const SolveParams& P, const PowTables& PT, bool tracing,
-                                       bool recording) {
+                                       double* const* trec) {
     const int32_t j = nsteps;
     const double remaining = O::sub(t_end, t);
     const bool trunc = fabs(dt) >= fabs(remaining);
@@ -200,13 +204,16 @@ struct Lane {
       if (P.trace_accept) P.trace_accept[o] = accept;
     }
     if (accept) {
-      if (recording) {  // (adjoint only) the pre-commit state of this step
-        double* r = P.traj + (P.traj_offsets[idx] + nacc) * (kTrajExtra + D);
-        r[0] = t;
-        r[1] = h;
-        r[2] = (double)cursor;
+      if (trec) {  // (adjoint only) the pre-commit state of this step,
+        // written as whole 32-byte sectors, one 256-bit store each
+        double rec[kTrajStride<D>] = {t, h, (double)cursor};
 #pragma unroll
-        for (int c = 0; c < D; c++) r[kTrajExtra + c] = y[c];
+        for (int c = 0; c < D; c++) rec[kTrajExtra + c] = y[c];
+        double* r = *trec + (int64_t)nacc * kTrajStride<D>;
+#pragma unroll
+        for (int q = 0; q < kTrajStride<D>; q += 4)
+          asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(r + q), "d"(rec[q]),
+                       "d"(rec[q + 1]), "d"(rec[q + 2]), "d"(rec[q + 3]) : "memory");
       }
       nacc++;
       const double t_old = t;
@@ -266,13 +273,15 @@ static __device__ unsigned long long g_exit_times[65536];
 static __device__ unsigned g_exit_count;
 #endif
 
-template <int M, class F, class O>
 // 2-D systems fit 5 blocks of 128 threads per SM (<= 102 registers); wider
-// ones keep 4 (<= 128 registers) to avoid spilling the stage vectors.
+// ones keep 4 (<= 128 registers) to avoid spilling the stage vectors.  The
+// trajectory-recording instantiation (REC, gradients only) keeps 4: its
+// row stores need registers the 5-block budget would spill.
 #ifndef BODE_BLOCKS_2D
 #define BODE_BLOCKS_2D 5
 #endif
-__global__ void __launch_bounds__(128, (F::D <= 2 ? BODE_BLOCKS_2D : 4)) bode_persistent_kernel(const SolveParams P) {
+template <int M, class F, class O, bool REC>
+__global__ void __launch_bounds__(128, (F::D <= 2 && !REC ? BODE_BLOCKS_2D : 4)) bode_persistent_kernel(const SolveParams P) {
   extern __shared__ uint32_t s_refresh[];
   __shared__ PowTables s_pow;  // pow tables: divergent lookups, so shared not constant
   const int lane = threadIdx.x & 31;
@@ -286,7 +295,8 @@ __global__ void __launch_bounds__(128, (F::D <= 2 ? BODE_BLOCKS_2D : 4)) bode_pe
 
   Lane<M, F, O> L;
   const bool tracing = P.trace_cap > 0;  // uniform: hoisted out of the step loop
-  const bool recording = P.traj != nullptr;
+  __shared__ double* s_trec[REC ? 128 : 1];  // per-lane trajectory row base
+  double* const* trec = REC ? &s_trec[threadIdx.x] : nullptr;
   bool have = false, done = false;
   unsigned long long my_max = 0;
   const unsigned lt_mask = (1u << lane) - 1u;
@@ -306,6 +316,7 @@ __global__ void __launch_bounds__(128, (F::D <= 2 ? BODE_BLOCKS_2D : 4)) bode_pe
           const int64_t i = P.order ? P.order[pos] : (int64_t)pos;
           if (P.status[i] == BODE_RUNNING) {  // else finalised by the init pass
             L.resume(P, i);
+            if constexpr (REC) s_trec[threadIdx.x] = P.traj + P.traj_offsets[i] * kTrajStride<F::D>;
             have = true;
           }
         }
@@ -317,7 +328,7 @@ __global__ void __launch_bounds__(128, (F::D <= 2 ? BODE_BLOCKS_2D : 4)) bode_pe
     }
     if (have) {
       const int64_t j = L.nsteps;
-      if (L.step(P, s_pow, tracing, recording)) {
+      if (L.step(P, s_pow, tracing, trec)) {
         const uint64_t bit = (uint64_t)j + 1;
         const uint32_t w = (uint32_t)(bit >> 5), msk = 1u << (bit & 31);
         if (P.smem_words > 0) {
@@ -369,7 +380,7 @@ __global__ void bode_finalize_kernel(const unsigned long long* max_n, const uint
 
 template <int M, class F, class O>
 cudaError_t launch_persistent(const SolveParams& P, int threads, int blocks, cudaStream_t st) {
-  auto kern = bode_persistent_kernel<M, F, O>;
+  auto kern = P.traj ? bode_persistent_kernel<M, F, O, true> : bode_persistent_kernel<M, F, O, false>;
   const size_t smem = (size_t)P.smem_words * 4;
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

@@ -524,7 +524,7 @@ def solve_device(y0, t_start, t_end, f, *, t_eval=None, t_eval_offsets=None, met
         toff = torch.zeros(n + 1, dtype=torch.int64, device=dev)
         torch.cumsum(out["n_accepted"], 0, out=toff[1:])
         rows = int(toff[-1])
-        traj = torch.empty((max(rows, 1), _abi.TRAJ_EXTRA + d), **f64)
+        traj = torch.empty((max(rows, 1), _abi.traj_stride(d)), **f64)
         keep += [toff, traj]
         a.traj, a.traj_offsets = traj.data_ptr(), toff.data_ptr()
         _abi.check(lib.bode_solve(_abi.C.byref(a)))
