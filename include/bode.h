@@ -18,6 +18,9 @@
  *   bode_error_norm               <- error_norm         controller.py:120-142
  *   bode_adapt_step               <- adapt_step         controller.py:200-238
  *   bode_initial_step             <- initial_step       controller.py:145-197
+ *   bode_solve_adjoint            <- (no reference counterpart: gradients,
+ *                                    torchode's AutoDiffAdjoint backward;
+ *                                    SURVEY.md 8(f) row 1)
  *
  * Error behaviour mirrors the reference: invalid arguments (the cases where
  * batchode raises ValueError) return BODE_EINVAL with a message in
