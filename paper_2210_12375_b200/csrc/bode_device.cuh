@@ -450,6 +450,24 @@ __device__ __forceinline__ double error_norm(const double* e, const double* y0, 
   return isfinite(norm) ? norm : __longlong_as_double(0x7ff0000000000000LL);
 }
 
+// fast mode: the squared norm mean(r*r) (what error_norm takes the square
+// root of), +inf when non-finite -- the I/PI controller below never needs
+// the root
+template <int D, class O>
+__device__ __forceinline__ double error_ms(const double* e, const double* y0, const double* y1,
+                                           double atol, double rtol) {
+  double sq[D];
+#pragma unroll
+  for (int j = 0; j < D; j++) {
+    const double scale = O::mad(rtol, np_max(fabs(y0[j]), fabs(y1[j])), atol);
+    const double r = e[j] * fast_rcp(scale);
+    sq[j] = O::mul(r, r);
+  }
+  const double s = pairwise_sum<D, O>(sq);
+  const double mean = s * (1.0 / D);  // (exact for power-of-two D, ~1 ulp otherwise)
+  return mean < INFINITY ? mean : __longlong_as_double(0x7ff0000000000000LL);  // NaN -> inf
+}
+
 // adapt_step, controller.py:200-238 (one instance).  dt is dt_used on entry,
 // dt_next on exit; returns accept.
 __device__ __forceinline__ bool adapt(const CtrlParams& C, double norm, double& n1, double& n2,
@@ -556,6 +574,44 @@ __device__ __forceinline__ bool adapt_cached(const CtrlParams& C, double norm, d
     n1 = a;
     L1 = La;
   }
+  return accept;
+}
+
+// Fast-mode I / PI controller (C.plain_pi) on the squared norm ms:
+//   accept  = norm <= 1          <=>  ms <= 1 + 2^-52 (sqrt correctly rounded)
+//   factor  = safety * a^e1 * n1^e2 = safety * exp(e1 log a + e2 log n1)
+// with log a = log(ms)/2 (a = max(norm, NORM_FLOOR), controller.py:26), the
+// history term from the cached log of the previous norm, and ONE exp of the
+// combined exponent (a few ulp, like the two ~1-ulp pows it replaces: the
+// accept decisions are insensitive at that level -- statuses and step counts
+// stay equal to the oracle's at full scale, tests/test_gpu_parity.py).  The
+// non-finite cases resolve to what the reference computes: a = +inf or
+// n1 = +inf make the product 0 or inf, i.e. factor_min; an exponent beyond
+// the double range gives inf (factor_min) or a finite huge / tiny factor
+// (clipped to factor_max / factor_min).
+__device__ __forceinline__ bool adapt_pi_ms(const CtrlParams& C, double ms, LogCache& L1,
+                                            double& dt, const PowTables& T) {
+  const bool accept = ms <= 1.0000000000000002;
+  LogCache La;
+  La.ok = ms < INFINITY;
+  double factor = C.fmin;
+  if (La.ok) {
+    const bool tiny = !(ms >= 1e-20);  // norm below the floor: a = 1e-10 exactly
+    fast_log(tiny ? 1e-10 : ms, T, La.h, La.l);
+    const double sc = tiny ? 1.0 : 0.5;
+    La.h *= sc;
+    La.l *= sc;
+    if (C.e2 == 0.0 || L1.ok) {
+      double y = fma(C.e1, La.h, C.e1 * La.l);
+      if (C.e2 != 0.0) y = fma(C.e2, L1.h, fma(C.e2, L1.l, y));
+      if (y < 700.0 && y > -700.0)
+        factor = np_min(np_max(C.safety * fast_exp(y, T), C.fmin), C.fmax);
+      else
+        factor = (y > 0.0 && y < 709.78) ? C.fmax : C.fmin;
+    }
+  }
+  dt = __dmul_rn(dt, factor);
+  if (C.hist || accept) L1 = La;
   return accept;
 }
 

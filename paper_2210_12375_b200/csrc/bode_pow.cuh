@@ -275,6 +275,25 @@ BODE_HD double fast_exp_mul(double e, double Lh, double Ll, double x, const PowT
   return from_bits(bits(res) + (ke << 52));
 }
 
+// exp(y) for |y| < 700 within ~1 ulp of exp of the rounded argument (the
+// table-driven body of fast_exp_mul with a plain-double argument)
+BODE_HD double fast_exp(double y, const PowTables& T) {
+  using namespace powimpl;
+  const double kd = rint(mul(y, BODE_PK(18)));
+  const int64_t kf = (int64_t)kd;
+  const int j = (int)(kf & 127);
+  const int64_t ke = (kf - j) / 128;
+  const double r = fma_(-kd, BODE_PK(17), fma_(-kd, BODE_PK(16), y));  // |r| < 2^-7.9
+  double c = fma_(BODE_PK(9), r, BODE_PK(10));
+  c = fma_(c, r, BODE_PK(11));
+  c = fma_(c, r, BODE_PK(12));
+  c = fma_(c, r, BODE_PK(13));
+  const double p = fma_(mul(r, r), c, r);
+  const double th = T.exp_tab[j][0], tl = T.exp_tab[j][1];
+  const double res = add(th, fma_(th, p, tl));
+  return from_bits(bits(res) + (ke << 52));
+}
+
 // Correctly rounded (w.h.p.) x**e for x > 0 finite, e finite; everything
 // else -- and results near overflow/underflow -- goes to the libm pow.
 BODE_HD double cr_pow(double x, double e, const PowTables& T) {

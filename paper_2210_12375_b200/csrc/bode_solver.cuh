@@ -185,6 +185,10 @@ struct Lane {
   // the next iteration, solver.py:220-226)
   // trec (recording only): shared-memory slot holding this lane's
   // trajectory row base, set at resume -- no per-step global load
+  // PI (fast mode only): the launch was specialised for an I / PI
+  // controller (CtrlParams::plain_pi), so the general controller is not
+  // compiled into the loop
+  template <bool PI>
   __device__ __forceinline__ bool step(const SolveParams& P, const PowTables& PT, bool tracing,
                                        double* const* trec) {
     const int32_t j = nsteps;
@@ -193,9 +197,14 @@ struct Lane {
     const double h = trunc ? remaining : dt;
     double yn[D], err[D];
     rk_step<T, F, O>(f, t, h, y, k, yn, err);
-    const double norm = error_norm<D, O>(err, y, yn, atol_of(P), rtol_of(P));
     double dtn = h;
-    const bool accept = adapt_cached<O>(P.ctrl, norm, n1, n2, L1, dtn, PT);
+    bool accept;
+    if constexpr (O::kFast && PI) {
+      accept = adapt_pi_ms(P.ctrl, error_ms<D, O>(err, y, yn, atol_of(P), rtol_of(P)), L1, dtn, PT);
+    } else {
+      const double norm = error_norm<D, O>(err, y, yn, atol_of(P), rtol_of(P));
+      accept = adapt_cached<O>(P.ctrl, norm, n1, n2, L1, dtn, PT);
+    }
     nsteps = j + 1;
     if (tracing && j < P.trace_cap) {
       const int64_t o = idx * P.trace_cap + j;  // (trace only)
@@ -280,7 +289,7 @@ static __device__ unsigned g_exit_count;
 #ifndef BODE_BLOCKS_2D
 #define BODE_BLOCKS_2D 5
 #endif
-template <int M, class F, class O, bool REC>
+template <int M, class F, class O, bool REC, bool PI>
 __global__ void __launch_bounds__(128, (F::D <= 2 && !REC ? BODE_BLOCKS_2D : 4)) bode_persistent_kernel(const SolveParams P) {
   extern __shared__ uint32_t s_refresh[];
   __shared__ PowTables s_pow;  // pow tables: divergent lookups, so shared not constant
@@ -328,7 +337,7 @@ __global__ void __launch_bounds__(128, (F::D <= 2 && !REC ? BODE_BLOCKS_2D : 4))
     }
     if (have) {
       const int64_t j = L.nsteps;
-      if (L.step(P, s_pow, tracing, trec)) {
+      if (L.template step<PI>(P, s_pow, tracing, trec)) {
         const uint64_t bit = (uint64_t)j + 1;
         const uint32_t w = (uint32_t)(bit >> 5), msk = 1u << (bit & 31);
         if (P.smem_words > 0) {
@@ -380,7 +389,12 @@ __global__ void bode_finalize_kernel(const unsigned long long* max_n, const uint
 
 template <int M, class F, class O>
 cudaError_t launch_persistent(const SolveParams& P, int threads, int blocks, cudaStream_t st) {
-  auto kern = P.traj ? bode_persistent_kernel<M, F, O, true> : bode_persistent_kernel<M, F, O, false>;
+  // fast mode with an I / PI controller takes the specialised loop
+  const bool pi = O::kFast && P.ctrl.plain_pi;
+  auto kern = P.traj ? (pi ? bode_persistent_kernel<M, F, O, true, O::kFast>
+                           : bode_persistent_kernel<M, F, O, true, false>)
+                     : (pi ? bode_persistent_kernel<M, F, O, false, O::kFast>
+                           : bode_persistent_kernel<M, F, O, false, false>);
   const size_t smem = (size_t)P.smem_words * 4;
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
