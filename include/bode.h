@@ -244,6 +244,12 @@ typedef struct bode_adjoint_args {
   void* workspace;             /* bode_adjoint_workspace_size bytes, device */
   size_t workspace_bytes;
   int64_t* launch_count_out;   /* optional HOST pointer */
+  /* MLP dynamics: dL/dW1 (H,d), dL/db1 (H,), dL/dW2 (d,H), dL/db2 (d,),
+   * fp32 device buffers summed over the batch, each optional (NULL) */
+  float* grad_W1;
+  float* grad_b1;
+  float* grad_W2;
+  float* grad_b2;
 } bode_adjoint_args;
 
 #define BODE_MLP_AUTO 0

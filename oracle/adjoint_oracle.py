@@ -181,3 +181,41 @@ def replay_ys(method: str, dyn_name: str, params: dict, y0: np.ndarray, t_start,
                               float(t0[i]), accepted_steps(ref, i),
                               np.asarray(t_eval[i], dtype=np.float64)).numpy())
     return res
+
+
+def mlp_dynamics(W1, b1, W2, b2):
+    """f(y) = W2 tanh(W1 y + b1) + b2 in fp32 on the fp64 state (the C4
+    oracle's NumPy fp32 MLP), as a torch function."""
+
+    def f(t, y, p):
+        z = p["W1"] @ y.to(torch.float32) + p["b1"]
+        return (p["W2"] @ torch.tanh(z) + p["b2"]).to(torch.float64)
+
+    return f
+
+
+def gradients_mlp(method: str, weights, y0: np.ndarray, t_start, steps: list, t_eval: list,
+                  grad_ys: list):
+    """dL/dy0 (n, d) and the batch-summed dL/dW1, db1, dW2, db2 for
+    L = sum_i <grad_ys[i], ys_i>, replaying the given accepted steps
+    (``steps[i]`` = list of (t_old, h)) with the fp32 MLP."""
+    f = mlp_dynamics(*weights)
+    y0 = np.atleast_2d(y0)
+    n, d = y0.shape
+    t0 = np.broadcast_to(np.asarray(t_start, dtype=np.float64), (n,))
+    p = {k: torch.tensor(np.asarray(v, dtype=np.float32), requires_grad=True)
+         for k, v in zip(("W1", "b1", "W2", "b2"), weights)}
+    gy0 = np.zeros((n, d))
+    total = None
+    for i in range(n):
+        yi = torch.tensor(y0[i], dtype=torch.float64, requires_grad=True)
+        ys = replay(method, f, p, yi, float(t0[i]), steps[i], np.asarray(t_eval[i], np.float64))
+        g = torch.as_tensor(np.asarray(grad_ys[i])[:ys.shape[0]], dtype=torch.float64)
+        loss = (ys * g).sum()
+        (gyi,) = torch.autograd.grad(loss, [yi], retain_graph=True) if loss.requires_grad else (None,)
+        if gyi is not None:
+            gy0[i] = gyi.numpy()
+        total = loss if total is None else total + loss
+    gw = torch.autograd.grad(total, list(p.values()), allow_unused=True)
+    return gy0, {k: (g.numpy() if g is not None else np.zeros_like(v.detach().numpy()))
+                 for (k, v), g in zip(p.items(), gw)}

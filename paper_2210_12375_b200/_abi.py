@@ -76,7 +76,8 @@ class AdjointArgs(C.Structure):
                 ("n_emitted", C.c_void_p), ("grad_ys", C.c_void_p),
                 ("grad_y0", C.c_void_p), ("grad_params", C.c_void_p),
                 ("workspace", C.c_void_p), ("workspace_bytes", C.c_size_t),
-                ("launch_count_out", C.c_void_p)]
+                ("launch_count_out", C.c_void_p), ("grad_W1", C.c_void_p),
+                ("grad_b1", C.c_void_p), ("grad_W2", C.c_void_p), ("grad_b2", C.c_void_p)]
 
 
 # every symbol include/bode.h declares, with its ctypes signature

@@ -109,8 +109,8 @@ int validate(const bode_solve_args* a) {
     return fail(BODE_EINVAL, "MLP weights required");
   if (a->pipeline_chunks < 0) return fail(BODE_EINVAL, "pipeline_chunks must be >= 0");
   if (a->traj && !a->traj_offsets) return fail(BODE_EINVAL, "traj needs traj_offsets");
-  if (a->traj && (a->dyn.kind == BODE_DYN_MLP || a->joint))
-    return fail(BODE_EUNSUPPORTED, "trajectory recording: analytic dynamics, independent solve only");
+  if (a->traj && a->joint)
+    return fail(BODE_EUNSUPPORTED, "trajectory recording: independent solve only");
   if (a->joint) {  // solver.py:391-403
     if (a->t_eval_offsets) return fail(BODE_EINVAL, "joint mode requires identical evaluation points");
     if (a->atol_v || a->rtol_v) return fail(BODE_EINVAL, "joint mode supports scalar tolerances only");
@@ -320,20 +320,23 @@ int bode_solve(const bode_solve_args* a) {
 
 size_t bode_adjoint_workspace_size(const bode_solve_args* a) {
   if (validate(a) != BODE_OK) return 0;
-  return adjoint_workspace_bytes(a->n);
+  return adjoint_workspace_bytes(a->n, a->d, a->dyn.kind, a->dyn.hidden);
 }
 
 int bode_solve_adjoint(const bode_solve_args* a, const bode_adjoint_args* g) {
   int rc = validate(a);
   if (rc != BODE_OK) return rc;
   if (!g) return fail(BODE_EINVAL, "null adjoint args");
-  if (a->dyn.kind == BODE_DYN_MLP || a->joint)
-    return fail(BODE_EUNSUPPORTED, "gradients: analytic dynamics, independent solve only");
+  if (a->joint) return fail(BODE_EUNSUPPORTED, "gradients: independent solve only");
+  if (a->dyn.kind == BODE_DYN_MLP &&
+      !((a->d == 4 || a->d == 8 || a->d == 16 || a->d == 32 || a->d == 64) && a->dyn.hidden <= 256))
+    return fail(BODE_EUNSUPPORTED, "MLP gradients: d in {4, 8, 16, 32, 64}, hidden <= 256");
   if (!g->traj || !g->traj_offsets || !g->n_emitted || !g->grad_y0)
     return fail(BODE_EINVAL, "adjoint needs traj, traj_offsets, n_emitted and grad_y0");
   if ((a->t_eval_offsets || a->t_eval_len > 0) && !g->grad_ys)
     return fail(BODE_EINVAL, "adjoint needs grad_ys");
-  if (!g->workspace || g->workspace_bytes < adjoint_workspace_bytes(a->n))
+  if (!g->workspace ||
+      g->workspace_bytes < adjoint_workspace_bytes(a->n, a->d, a->dyn.kind, a->dyn.hidden))
     return fail(BODE_EINVAL, "workspace too small (see bode_adjoint_workspace_size)");
   AdjParams A;
   memset(&A, 0, sizeof(A));
@@ -348,6 +351,17 @@ int bode_solve_adjoint(const bode_solve_args* a, const bode_adjoint_args* g) {
   A.grad_ys = g->grad_ys;
   A.grad_y0 = g->grad_y0;
   A.grad_params = g->grad_params;
+  if (a->dyn.kind == BODE_DYN_MLP) {
+    A.H = a->dyn.hidden;
+    A.W1 = a->dyn.W1;
+    A.b1 = a->dyn.b1;
+    A.W2 = a->dyn.W2;
+    A.b2 = a->dyn.b2;
+    A.gW1 = g->grad_W1;
+    A.gb1 = g->grad_b1;
+    A.gW2 = g->grad_W2;
+    A.gb2 = g->grad_b2;
+  }
   int64_t launches = 0;
   cudaError_t e = adjoint_launch(a->method, a->d, A, g->workspace, (cudaStream_t)a->stream,
                                  &launches);

@@ -211,9 +211,13 @@ cudaError_t dispatch_adjoint(int kind, int64_t d, const AdjParams& A, cudaStream
 
 }  // namespace
 
-// workspace: [queue counter | cost (n doubles) | LPT scratch]
-size_t adjoint_workspace_bytes(int64_t n) {
-  return 256 + ((8 * (size_t)n + 255) & ~(size_t)255) + lpt_workspace_bytes(n);
+static size_t adjoint_lpt_end(int64_t n) {
+  return 256 + ((8 * (size_t)n + 255) & ~(size_t)255) + ((lpt_workspace_bytes(n) + 255) & ~(size_t)255);
+}
+
+// workspace: [queue counter | cost (n doubles) | LPT scratch | MLP partials]
+size_t adjoint_workspace_bytes(int64_t n, int64_t d, int kind, int64_t H) {
+  return adjoint_lpt_end(n) + (kind == BODE_DYN_MLP ? mlp_adjoint_part_bytes(d, H) : 0);
 }
 
 cudaError_t adjoint_launch(int method, int64_t d, AdjParams A, void* ws, cudaStream_t st,
@@ -230,7 +234,12 @@ cudaError_t adjoint_launch(int method, int64_t d, AdjParams A, void* ws, cudaStr
   e = lpt_order(cost, A.n, w + 256 + ((8 * (size_t)A.n + 255) & ~(size_t)255), &order, st);
   if (e != cudaSuccess) return e;
   A.order = order;
-  *launches += 5;  // cost + 3 LPT passes + the backward kernel
+  *launches += 4;  // cost + 3 LPT passes
+  if (A.dyn.kind == BODE_DYN_MLP) {
+    A.mlp_part = (float*)(w + adjoint_lpt_end(A.n));
+    return mlp_adjoint_run(method, d, A, st, launches);
+  }
+  *launches += 1;
   switch (method) {
     case BODE_METHOD_DOPRI5: return dispatch_adjoint<BODE_METHOD_DOPRI5>(A.dyn.kind, d, A, st);
     case BODE_METHOD_TSIT5: return dispatch_adjoint<BODE_METHOD_TSIT5>(A.dyn.kind, d, A, st);

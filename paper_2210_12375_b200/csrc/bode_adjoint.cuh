@@ -22,9 +22,18 @@ struct AdjParams {
   double* grad_params;            // (n, 8) or NULL
   const int64_t* order;           // queue order (longest first) or NULL
   unsigned long long* queue;
+  // MLP dynamics (bode_mlp_adjoint.cu): weights, batch-summed weight
+  // gradients (fp32, NULL = not wanted) and per-CTA partials (workspace)
+  int64_t H;
+  const float *W1, *b1, *W2, *b2;
+  float *gW1, *gb1, *gW2, *gb2;
+  float* mlp_part;
 };
 
-size_t adjoint_workspace_bytes(int64_t n);
+// workspace: [queue | LPT cost | LPT scratch | MLP partials (MLP only)]
+size_t adjoint_workspace_bytes(int64_t n, int64_t d, int kind, int64_t H);
+size_t mlp_adjoint_part_bytes(int64_t d, int64_t H);
+cudaError_t mlp_adjoint_run(int method, int64_t d, AdjParams A, cudaStream_t st, int64_t* launches);
 // Builds the longest-first queue from the trajectory lengths, then launches
 // the persistent backward kernel; returns the number of kernels launched
 // through *launches.

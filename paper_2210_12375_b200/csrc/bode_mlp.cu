@@ -24,6 +24,7 @@ namespace bode {
 namespace {
 
 constexpr int kMaxD = 128;
+constexpr int kTrajRowExtra = BODE_TRAJ_EXTRA;
 constexpr int kTile = 32;  // instances per block in the CUDA-core MLP
 
 struct MlpWs {
@@ -177,6 +178,9 @@ struct CtrlArgs {
   int64_t max_steps;
   unsigned long long* max_n;
   uint32_t* refresh;
+  // optional accepted-step trajectory (gradients; SolveParams::traj layout)
+  double* traj;
+  const int64_t* traj_offsets;
 };
 
 __device__ __forceinline__ void te_of(const CtrlArgs& A, int64_t i, int D, const double*& te,
@@ -206,6 +210,7 @@ __global__ void __launch_bounds__(128) mlp_control_kernel(MlpWs W, CtrlArgs A, i
   const double h = W.h[i], y_t = W.t[i], t_end = A.t_end[i];
   const double atol = A.atol_v ? A.atol_v[i] : A.atol, rtol = A.rtol_v ? A.rtol_v[i] : A.rtol;
   const int nslot = (D + 31) / 32;
+  const int64_t nacc_before = A.n_accepted[i];  // (read before lane 0 updates it)
   double yv[4], yn[4];
   for (int s = 0; s < nslot; s++) {
     const int c = lane + 32 * s;
@@ -244,6 +249,19 @@ __global__ void __launch_bounds__(128) mlp_control_kernel(MlpWs W, CtrlArgs A, i
   int64_t cursor = A.n_emitted[i];
   int status = BODE_RUNNING;
   double t_new = y_t;
+  if (acc_i && A.traj) {  // record (t_old, h, cursor, y_old) for the adjoint
+    const int W = BODE_TRAJ_STRIDE(D);
+    double* rec = A.traj + (A.traj_offsets[i] + nacc_before) * W;
+    if (lane == 0) {
+      rec[0] = y_t;
+      rec[1] = h;
+      rec[2] = (double)cursor;
+    }
+    for (int s = 0; s < nslot; s++) {
+      const int c = lane + 32 * s;
+      if (c < D) rec[kTrajRowExtra + c] = yv[s];
+    }
+  }
   if (acc_i) {
     // dense output (solver.py:284-322) from the pre-commit state
     const double* te;
@@ -517,7 +535,11 @@ static cudaError_t mlp_solve_m(const bode_solve_args* a, const SolveParams& P, c
   if (a->mlp_backend == BODE_MLP_TCGEN05 && !tc_ok) return cudaErrorNotSupported;
   if (a->mlp_backend == BODE_MLP_FUSED && !fused_ok) return cudaErrorNotSupported;
   const bool use_tc = tc_ok && a->mlp_backend != BODE_MLP_CUDA_CORE;
-  const bool use_fused = fused_ok && (a->mlp_backend == BODE_MLP_AUTO || a->mlp_backend == BODE_MLP_FUSED);
+  // a recording pass (gradients) runs the lockstep tensor-core path, which is
+  // bit-identical to the fused kernel (tests/test_gpu_solver.py), so the
+  // trajectory is that of the solve being differentiated
+  const bool use_fused = fused_ok && !a->traj &&
+                         (a->mlp_backend == BODE_MLP_AUTO || a->mlp_backend == BODE_MLP_FUSED);
   if (use_tc && (e = mlp_tc_prep(W1, W2, H, W.wprep, st)) != cudaSuccess) return e;
   int64_t nl = use_tc ? 1 : 0;  // kernels launched
   const int max_tiles = (int)((n + 127) / 128);
@@ -555,7 +577,7 @@ static cudaError_t mlp_solve_m(const bode_solve_args* a, const SolveParams& P, c
   CtrlArgs A{P.ctrl, a->t_end, a->atol_v, a->rtol_v, a->atol, a->rtol, a->t_eval,
              a->t_eval_offsets, a->t_eval_offsets ? 0 : a->t_eval_len, a->ys, a->n_emitted,
              a->n_steps, a->n_accepted, a->final_dt, a->status, a->max_steps, P.max_n,
-             P.refresh};
+             P.refresh, a->traj, a->traj_offsets};
   mlp_init_a_kernel<<<grid_for(n * D), 256, 0, st>>>(W, I, n, D);
   eval(W.k);  // f0 = f(t0, y0)
   const bool heur = a->dt0_mode == BODE_DT0_HEURISTIC;

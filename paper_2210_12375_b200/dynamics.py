@@ -193,8 +193,14 @@ def damped_dynamics() -> DeviceDynamics:
 
 def mlp_dynamics(W1, b1, W2, b2) -> DeviceDynamics:
     """Neural-ODE dynamics W2 tanh(W1 y + b1) + b2 evaluated in fp32 on the
-    tensor cores; the state stays fp64."""
-    W1, b1, W2, b2 = (np.ascontiguousarray(np.asarray(x, dtype=np.float32)) for x in (W1, b1, W2, b2))
+    tensor cores; the state stays fp64.  Weights as
+    NumPy arrays, or CUDA tensors (for the device path; tensors that
+    require grad receive gradients through torchode.AutoDiffAdjoint)."""
+    if any(_is_tensor(x) for x in (W1, b1, W2, b2)):  # device tensors (may require grad)
+        W1, b1, W2, b2 = (x.float().contiguous() for x in (W1, b1, W2, b2))
+    else:
+        W1, b1, W2, b2 = (np.ascontiguousarray(np.asarray(x, dtype=np.float32))
+                          for x in (W1, b1, W2, b2))
     H, D = W1.shape
     if b1.shape != (H,) or W2.shape != (D, H) or b2.shape != (D,):
         raise ValueError("MLP weights must be W1 (H,D), b1 (H,), W2 (D,H), b2 (D,)")

@@ -547,7 +547,9 @@ def adjoint_device(fwd: dict, grad_ys):
     ``(grad_y0 (n, d), grad_params (n, 8))`` for ``grad_ys`` = dL/dys in
     the forward ys layout.  Column k of grad_params is dL/dp_k per instance
     for parameter slot k of the dynamics (``dynamics.SLOTS`` order); for a
-    parameter shared by the batch its gradient is the column sum.  Step
+    parameter shared by the batch its gradient is the column sum.  For MLP
+    dynamics grad_params is instead a dict of the batch-summed fp32 weight
+    gradients {W1, b1, W2, b2}.  Step
     sizes and accept decisions are constants (no gradient through the
     step-size controller); see include/bode.h ``bode_solve_adjoint``."""
     import torch
@@ -569,6 +571,13 @@ def adjoint_device(fwd: dict, grad_ys):
     grad_y0 = torch.empty((n, d), dtype=torch.float64, device=dev)
     grad_params = torch.empty((n, 8), dtype=torch.float64, device=dev)
     g.grad_y0, g.grad_params = grad_y0.data_ptr(), grad_params.data_ptr()
+    if a.dyn.kind == _abi.DYN["mlp"]:  # batch-summed weight gradients (fp32)
+        H = int(a.dyn.hidden)
+        f32 = dict(dtype=torch.float32, device=dev)
+        grad_params = dict(W1=torch.empty((H, d), **f32), b1=torch.empty(H, **f32),
+                           W2=torch.empty((d, H), **f32), b2=torch.empty(d, **f32))
+        g.grad_W1, g.grad_b1 = grad_params["W1"].data_ptr(), grad_params["b1"].data_ptr()
+        g.grad_W2, g.grad_b2 = grad_params["W2"].data_ptr(), grad_params["b2"].data_ptr()
     wsb = lib.bode_adjoint_workspace_size(_abi.C.byref(a))
     if wsb == 0:
         _abi.check(_abi.EINVAL)

@@ -24,7 +24,10 @@ differentiable; ``backward`` runs the sm_100a adjoint kernel
 (``bode_solve_adjoint``, csrc/bode_adjoint.cu): exact reverse mode through
 every RK stage, solution update and dense-output interpolant, with the
 step sizes and accept decisions held fixed (discretise-then-optimise, no
-gradient through the step-size controller).  Analytic dynamics only.
+gradient through the step-size controller).  Analytic dynamics get
+dL/dy0 and dL/d(parameter tensors); MLP dynamics (csrc/bode_mlp_adjoint.cu)
+dL/dy0 and dL/d(W1, b1, W2, b2) when the weights are tensors requiring
+grad.
 """
 
 from dataclasses import dataclass
@@ -179,11 +182,12 @@ class AutoDiffAdjoint:
                   rtol=self.controller.rtol, controller=self.controller.coeffs,
                   max_steps=self.max_steps, dt0=dt0, cost_hint=cost_hint, mode=self.mode)
         dyn = term.f
-        grads = [(name, v) for name, v in dyn.params.items()
+        grads = [(("param", SLOTS[dyn.kind].index(name)), v) for name, v in dyn.params.items()
                  if _is_tensor(v) and v.requires_grad]
+        grads += [(("mlp", k), v) for k, v in enumerate(dyn.mlp or ())
+                  if _is_tensor(v) and v.requires_grad]
         if torch.is_grad_enabled() and (problem.y0.requires_grad or grads):
-            spec = dict(problem=problem, dyn=dyn, kw=kw,
-                        slots=[SLOTS[dyn.kind].index(name) for name, _ in grads])
+            spec = dict(problem=problem, dyn=dyn, kw=kw, leaves=[key for key, _ in grads])
             ys_flat = _AdjointSolve.apply(spec, problem.y0, *[v for _, v in grads])
             out = spec["out"]
         else:
@@ -216,7 +220,8 @@ class _AdjointSolve:
                 p = spec["problem"]
                 dyn = spec["dyn"]
                 plain = {k: (v.detach() if _is_tensor(v) else v) for k, v in dyn.params.items()}
-                dyn0 = DeviceDynamics(dyn.kind, plain, dyn.mlp)
+                mlp = tuple(v.detach() if _is_tensor(v) else v for v in dyn.mlp) if dyn.mlp else None
+                dyn0 = DeviceDynamics(dyn.kind, plain, mlp)
                 out = solve_device(y0_.detach(), p.t_start, p.t_end, dyn0,
                                    record_trajectory=True, **spec["kw"])
                 spec["out"] = out
@@ -228,8 +233,11 @@ class _AdjointSolve:
             def backward(ctx, g):
                 gy0, gp = adjoint_device(ctx.fwd, g)
                 pg = []
-                for slot, shape in zip(spec["slots"], ctx.shapes):
-                    col = gp[:, slot]
+                for (kind, key), shape in zip(spec["leaves"], ctx.shapes):
+                    if kind == "mlp":  # batch-summed fp32 weight gradients
+                        pg.append(gp[("W1", "b1", "W2", "b2")[key]].reshape(shape))
+                        continue
+                    col = gp[:, key]
                     pg.append(col.sum().reshape(shape) if len(shape) == 0 or
                               (len(shape) == 1 and shape[0] == 1 and gp.shape[0] != 1)
                               else col.reshape(shape))
