@@ -518,6 +518,7 @@ def solve_device(y0, t_start, t_end, f, *, t_eval=None, t_eval_offsets=None, met
     st = stream if stream is not None else torch.cuda.current_stream(dev)
     a.stream = st.cuda_stream
     nlaunch = _abi.C.c_int64(0)
+    keep.append(nlaunch)  # a.launch_count_out must stay valid while `a` is reused
     a.launch_count_out = _abi.C.addressof(nlaunch)
     _abi.check(lib.bode_solve(_abi.C.byref(a)))
     if record_trajectory:
@@ -569,9 +570,11 @@ def adjoint_device(fwd: dict, grad_ys):
         keep.append(gy)
         g.grad_ys = gy.data_ptr()
     grad_y0 = torch.empty((n, d), dtype=torch.float64, device=dev)
-    grad_params = torch.empty((n, 8), dtype=torch.float64, device=dev)
-    g.grad_y0, g.grad_params = grad_y0.data_ptr(), grad_params.data_ptr()
-    if a.dyn.kind == _abi.DYN["mlp"]:  # batch-summed weight gradients (fp32)
+    g.grad_y0 = grad_y0.data_ptr()
+    if a.dyn.kind != _abi.DYN["mlp"]:  # per-instance parameter-slot gradients
+        grad_params = torch.empty((n, 8), dtype=torch.float64, device=dev)
+        g.grad_params = grad_params.data_ptr()
+    else:  # batch-summed weight gradients (fp32)
         H = int(a.dyn.hidden)
         f32 = dict(dtype=torch.float32, device=dev)
         grad_params = dict(W1=torch.empty((H, d), **f32), b1=torch.empty(H, **f32),

@@ -30,7 +30,10 @@ def main():
     ap.add_argument("--n", type=int, default=2 ** 20)
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--mode", default="fast")
+    ap.add_argument("--config", default="c2", choices=["c2", "c4"])
     args = ap.parse_args()
+    if args.config == "c4":
+        return main_c4(args)
     cfg = bench.make_config("c2", 0, n_override=args.n)
     dev = torch.device("cuda:0")
     n = cfg["n"]
@@ -104,6 +107,67 @@ def main():
         linearity_rel_err=lin, subsample_max_scaled_err=float(err),
         subsample_counts_equal=bool(np.array_equal(out["n_accepted"].cpu().numpy()[idx],
                                                    ref["n_accepted"])))))
+
+
+def main_c4(args):
+    """Neural ODE (C4: 64K instances, D=64, H=256, dopri5, t in [0,10]):
+    recording forward, adjoint (dL/dy0 + weight gradients), subsample
+    parity of dL/dy0 vs the autograd replay of the GPU's own steps."""
+    import torch
+
+    import bench
+    import paper_2210_12375_b200 as bode
+    from paper_2210_12375_b200 import _abi
+
+    cfg = bench.make_config("c4", 0, n_override=None if args.n == 2 ** 20 else args.n)
+    dev = torch.device("cuda:0")
+    n, D = cfg["n"], cfg["d"]
+    W = [torch.tensor(w, device=dev) for w in cfg["mlp"]]
+    dyn = bode.mlp_dynamics(*W)
+    kw = dict(t_eval=torch.tensor(cfg["te2d"], device=dev), method="dopri5", atol=cfg["tol"],
+              rtol=cfg["tol"], max_steps=cfg["max_steps"])
+    y0 = torch.tensor(cfg["y0"], device=dev)
+    out = bode.solve_device(y0, 0.0, 10.0, dyn, record_trajectory=True, **kw)
+    lib = _abi.load()
+    a = out["_args"]
+    gy = torch.ones_like(out["ys"])
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
+    t_plain, t_rec, t_adj = [], [], []
+    rec_traj = a.traj
+    for _ in range(args.reps):
+        torch.cuda.synchronize()
+        a.traj = None
+        ev[0].record()
+        _abi.check(lib.bode_solve(_abi.C.byref(a)))
+        ev[1].record()
+        a.traj = rec_traj
+        _abi.check(lib.bode_solve(_abi.C.byref(a)))
+        ev[2].record()
+        g0, gw = bode.adjoint_device(out, gy)
+        ev[3].record()
+        torch.cuda.synchronize()
+        t_plain.append(ev[0].elapsed_time(ev[1]))
+        t_rec.append(ev[1].elapsed_time(ev[2]))
+        t_adj.append(ev[2].elapsed_time(ev[3]))
+    acc = int(out["n_accepted"].sum())
+    print("timed", t_plain, t_rec, t_adj, file=sys.stderr, flush=True)
+    import adjoint_oracle as AO
+
+    idx = np.sort(np.random.default_rng(5).choice(n, 4, replace=False))
+    traj = out["traj"].cpu().numpy()
+    toff = out["traj_offsets"].cpu().numpy()
+    steps = [[tuple(r) for r in traj[toff[i]:toff[i + 1], :2]] for i in idx]
+    gy0_ref, _ = AO.gradients_mlp("dopri5", cfg["mlp"], cfg["y0"][idx], 0.0, steps,
+                                  [cfg["te2d"][i] for i in idx], [np.ones((1, D))] * len(idx))
+    err = float(np.abs(g0.cpu().numpy()[idx] - gy0_ref).max() / np.abs(gy0_ref).max())
+    med = lambda v: float(np.median(v))  # noqa: E731
+    print(json.dumps(dict(
+        workload=cfg["workload"] + "_gradient", n=n, accepted_steps=acc,
+        traj_bytes=int(toff[-1]) * _abi.traj_stride(D) * 8,
+        forward_ms=med(t_plain), recording_forward_ms=med(t_rec), adjoint_ms=med(t_adj),
+        gradient_instance_steps_per_s=acc / ((med(t_rec) + med(t_adj)) / 1e3),
+        adjoint_launches=out.get("adjoint_launches"), subsample_rel_err_dy0=err,
+        weight_grad_norms={k: float(v.norm()) for k, v in gw.items()})))
 
 
 if __name__ == "__main__":
