@@ -8,8 +8,11 @@
 // output -- with step sizes and accept decisions held fixed.  Outputs
 // dL/dy0 per instance and dL/dW1, db1, dW2, db2 summed over the batch.
 //
-// One CTA (256 threads) owns one instance at a time and walks its steps
-// backwards; thread j owns hidden unit j, thread c < D state component c.
+// One CTA (256 threads) reverses kRows instances at a time in lockstep
+// (consecutive entries of the longest-first queue, so their trajectory
+// lengths match); thread j owns hidden unit j for all rows, thread
+// (r, c) < kRows*D row r's state component c.  Every weight read from
+// shared memory serves the kRows rows.
 // Both weight matrices sit in shared memory with padded rows (conflict-free
 // for row- and column-wise access), the seven stages' fp32 inputs and
 // hidden activations of the step being reversed are kept in shared memory,
@@ -27,35 +30,42 @@ namespace bode {
 namespace {
 
 constexpr int kThreads = 256;
+constexpr int kRows = 4;  // instances reversed together by one CTA
 
 template <int D>
 constexpr size_t mlp_adj_smem(int S) {
-  return 4 * ((size_t)kThreads * (D + 1) + (size_t)D * (kThreads + 1) + (size_t)S * kThreads +
-              (size_t)S * D + 4 * 64 + 64 + kThreads) +
-         8 * ((size_t)2 * S * D + 3 * D) + 64;
+  return 8 * ((size_t)2 * S * kRows * D + 3 * kRows * D + 4 * kRows) +
+         4 * ((size_t)kThreads * (D + 1) + (size_t)D * (kThreads + 1) +
+              (size_t)S * kRows * kThreads + (size_t)S * kRows * D + kRows * 4 * 64 +
+              kRows * 64 + kRows * kThreads) + 64;
 }
 
+// Rows r < kRows of a CTA are kRows consecutive instances of the
+// longest-first queue, reversed in lockstep (iteration `it` reverses each
+// row's (nrec - 1 - it)-th step; a row whose trajectory is exhausted is
+// inactive and contributes exactly zero: its stage adjoints are zero).
 template <int M, int D>
 __global__ void __launch_bounds__(kThreads, 1) mlp_adjoint_kernel(const AdjParams A) {
   using T = Tab<M>;
-  constexpr int S = T::S, NI = T::NI, W = BODE_TRAJ_STRIDE(D);
+  constexpr int S = T::S, NI = T::NI, W = BODE_TRAJ_STRIDE(D), R = kRows;
   const int H = A.H;
   const int tid = threadIdx.x;
   extern __shared__ __align__(16) unsigned char smraw[];
-  double* kk = reinterpret_cast<double*>(smraw);  // [S][D] stage derivatives
-  double* kb = kk + S * D;                           // [S][D] their adjoints
-  double* yv = kb + S * D;                           // [D] y_old
-  double* yb = yv + D;                               // [D] running dL/dy_old
-  double* ab = yb + D;                               // [D] dL/dy_next
-  float* W1p = reinterpret_cast<float*>(ab + D);    // [H][D+1]
+  double* kk = reinterpret_cast<double*>(smraw);  // [S][R][D] stage derivatives
+  double* kb = kk + S * R * D;                       // [S][R][D] their adjoints
+  double* yv = kb + S * R * D;                       // [R][D] y_old
+  double* yb = yv + R * D;                           // [R][D] running dL/dy_old
+  double* ab = yb + R * D;                           // [R][D] dL/dy_next
+  double* rs = ab + R * D;                           // [R][4] t_old, h, lo, active
+  float* W1p = reinterpret_cast<float*>(rs + 4 * R);  // [H][D+1]
   float* W2p = W1p + kThreads * (D + 1);             // [D][H+1]
-  float* Hs = W2p + D * (kThreads + 1);              // [S][256] tanh activations
-  float* Yf = Hs + S * kThreads;                     // [S][D] fp32 stage inputs
-  float* Pp = Yf + S * D;                            // [4][64] partial sums
-  float* gf = Pp + 4 * 64;                           // [64] fp32 stage adjoint
-  float* Vs = gf + 64;                               // [256] tanh' * W2^T g
-  __shared__ int64_t s_inst;
-  __shared__ double s_rec[3];
+  float* Hs = W2p + D * (kThreads + 1);              // [S][R][256] tanh activations
+  float* Yf = Hs + S * R * kThreads;                 // [S][R][D] fp32 stage inputs
+  float* Pp = Yf + S * R * D;                        // [R][4][64] partial sums
+  float* gf = Pp + R * 4 * 64;                       // [R][64] fp32 stage adjoint
+  float* Vs = gf + R * 64;                           // [R][256]
+  __shared__ int64_t s_inst[R], s_nrec[R], s_r0[R], s_hi[R];
+  __shared__ int64_t s_it;
 
   for (int e = tid; e < H * D; e += kThreads) {
     const int j = e / D, c = e % D;
@@ -63,9 +73,11 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_adjoint_kernel(const AdjParam
     const int o = e / H, jj = e % H;
     W2p[o * (kThreads + 1) + jj] = A.W2[e];
   }
-  const bool own_j = tid < H, own_c = tid < D;
+  const bool own_j = tid < H;
+  const int er = tid / D, ec = tid % D;  // (row, component) of this thread
+  const bool own_e = tid < R * D;
   const float b1j = own_j ? A.b1[tid] : 0.0f;
-  const float b2c = own_c ? A.b2[tid] : 0.0f;
+  const float b2c = own_e ? A.b2[ec] : 0.0f;
   float gW1[D], gW2[D], gb1 = 0.0f, gb2 = 0.0f;
 #pragma unroll
   for (int c = 0; c < D; c++) gW1[c] = gW2[c] = 0.0f;
@@ -75,132 +87,201 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_adjoint_kernel(const AdjParam
 
   while (true) {
     if (tid == 0) {
-      const unsigned long long q = atomicAdd(A.queue, 1ull);
-      s_inst = q < (unsigned long long)A.n ? (A.order ? A.order[q] : (int64_t)q) : -1;
+      const unsigned long long q = atomicAdd(A.queue, (unsigned long long)R);
+      int64_t mx = -1;
+      for (int r = 0; r < R; r++) {
+        const int64_t i = q + r < (unsigned long long)A.n ? (A.order ? A.order[q + r] : (int64_t)(q + r)) : -1;
+        s_inst[r] = i;
+        s_r0[r] = i >= 0 ? A.traj_offsets[i] : 0;
+        s_nrec[r] = i >= 0 ? A.traj_offsets[i + 1] - s_r0[r] : -1;
+        s_hi[r] = i >= 0 ? A.n_emitted[i] : 0;
+        mx = s_nrec[r] > mx ? s_nrec[r] : mx;
+      }
+      s_it = q < (unsigned long long)A.n ? mx : -1;
     }
     __syncthreads();
-    const int64_t i = s_inst;
-    if (i < 0) break;
-    const double* te = A.t_eval_offsets ? A.t_eval + A.t_eval_offsets[i] : A.t_eval;
-    const double* gy = A.t_eval_offsets ? A.grad_ys + A.t_eval_offsets[i] * D
-                                        : A.grad_ys + i * A.t_eval_len * D;
-    const int64_t r0 = A.traj_offsets[i], nrec = A.traj_offsets[i + 1] - r0;
-    int64_t hi = A.n_emitted[i];
-    if (own_c) ab[tid] = 0.0;
-    for (int64_t r = nrec - 1; r >= 0; r--) {
-      const double* rec = A.traj + (r0 + r) * W;
-      if (tid < 3) s_rec[tid] = rec[tid];
-      if (own_c) yv[tid] = rec[kTrajExtra + tid];
+    const int64_t iters = s_it;
+    if (iters < 0) break;
+    if (own_e) ab[tid] = 0.0;
+    for (int64_t it = 0; it < iters; it++) {
+      // ---- load this iteration's record of every active row
+      if (tid < R) {
+        const int64_t k = s_nrec[tid] - 1 - it;
+        double* q = rs + 4 * tid;
+        if (k >= 0) {
+          const double* rec = A.traj + (s_r0[tid] + k) * W;
+          q[0] = rec[0];
+          q[1] = rec[1];
+          q[2] = rec[2];
+          q[3] = 1.0;
+        } else {
+          q[0] = q[1] = q[2] = 0.0;
+          q[3] = 0.0;
+        }
+      }
       __syncthreads();
-      const double t = s_rec[0], h = s_rec[1];
-      const int64_t lo = (int64_t)s_rec[2];
-      (void)t;  // autonomous dynamics
-      // ---- forward recompute of the step: Yf[s], Hs[s], kk[s]
+      const bool act_e = own_e && rs[4 * er + 3] != 0.0;
+      const double h_e = own_e ? rs[4 * er + 1] : 0.0;
+      if (own_e)
+        yv[tid] = act_e ? A.traj[(s_r0[er] + s_nrec[er] - 1 - it) * W + kTrajExtra + ec] : 0.0;
+      __syncthreads();
+      // ---- forward recompute: Yf[s], Hs[s], kk[s] for all rows
       for (int s = 0; s < S; s++) {
-        if (own_c) {
+        if (own_e) {
           double acc = 0.0;
           if (s > 0) {
             acc = T::a(s, 0) * kk[tid];
-            for (int j = 1; j < s; j++) acc = fma(T::a(s, j), kk[j * D + tid], acc);
+            for (int j = 1; j < s; j++) acc = fma(T::a(s, j), kk[(j * R) * D + tid], acc);
           }
-          Yf[s * D + tid] = (float)(s > 0 ? fma(h, acc, yv[tid]) : yv[tid]);
+          Yf[(s * R) * D + tid] = (float)(s > 0 ? fma(h_e, acc, yv[tid]) : yv[tid]);
         }
         __syncthreads();
         if (own_j) {
-          float z = b1j;
+          float z[R];
+#pragma unroll
+          for (int r = 0; r < R; r++) z[r] = b1j;
           const float* w = W1p + tid * (D + 1);
-          const float* yf = Yf + s * D;
-#pragma unroll 16
-          for (int c = 0; c < D; c++) z = fmaf(w[c], yf[c], z);
-          Hs[s * kThreads + tid] = tanhf(z);
+          const float* yf = Yf + (s * R) * D;
+#pragma unroll 8
+          for (int c = 0; c < D; c++) {
+            const float wc = w[c];
+#pragma unroll
+            for (int r = 0; r < R; r++) z[r] = fmaf(wc, yf[r * D + c], z[r]);
+          }
+#pragma unroll
+          for (int r = 0; r < R; r++) Hs[(s * R + r) * kThreads + tid] = tanhf(z[r]);
         }
         __syncthreads();
         if (po < D) {
-          float acc = 0.0f;
+          float acc[R];
+#pragma unroll
+          for (int r = 0; r < R; r++) acc[r] = 0.0f;
           const float* w = W2p + po * (kThreads + 1);
-          const float* hs = Hs + s * kThreads;
-          for (int j = j_lo; j < j_hi; j++) acc = fmaf(w[j], hs[j], acc);
-          Pp[part * 64 + po] = acc;
+          const float* hs = Hs + (s * R) * kThreads;
+          for (int j = j_lo; j < j_hi; j++) {
+            const float wj = w[j];
+#pragma unroll
+            for (int r = 0; r < R; r++) acc[r] = fmaf(wj, hs[r * kThreads + j], acc[r]);
+          }
+#pragma unroll
+          for (int r = 0; r < R; r++) Pp[(r * 4 + part) * 64 + po] = acc[r];
         }
         __syncthreads();
-        if (own_c)
-          kk[s * D + tid] = (double)(((Pp[tid] + Pp[64 + tid]) + (Pp[128 + tid] + Pp[192 + tid])) + b2c);
+        if (own_e) {
+          const float* pp = Pp + er * 256 + ec;
+          kk[(s * R) * D + tid] = (double)(((pp[0] + pp[64]) + (pp[128] + pp[192])) + b2c);
+        }
         __syncthreads();
       }
       // ---- seeds: y_next = y + h sum b_s k_s and the points of this step
-      if (own_c) {
-        const double a0 = ab[tid];
+      if (own_e) {
+        const double a0 = act_e ? ab[tid] : 0.0;
         double y_b = a0;
 #pragma unroll
-        for (int s = 0; s < S; s++) kb[s * D + tid] = (h * T::b(s)) * a0;
-        for (int64_t p = lo; p < hi; p++) {
-          double theta = ddiv(te[p] - s_rec[0], h);
-          theta = np_max(theta, 0.0);
-          const double g = gy[p * D + tid];
-          y_b += g;
+        for (int s = 0; s < S; s++) kb[(s * R) * D + tid] = (h_e * T::b(s)) * a0;
+        if (act_e) {
+          const int64_t i = s_inst[er];
+          const double* te = A.t_eval_offsets ? A.t_eval + A.t_eval_offsets[i] : A.t_eval;
+          const double* gy = A.t_eval_offsets ? A.grad_ys + A.t_eval_offsets[i] * D
+                                              : A.grad_ys + i * A.t_eval_len * D;
+          const double t_old = rs[4 * er];
+          const int64_t lo = (int64_t)rs[4 * er + 2];
+          for (int64_t p = lo; p < s_hi[er]; p++) {
+            double theta = ddiv(te[p] - t_old, h_e);
+            theta = np_max(theta, 0.0);
+            const double g = gy[p * D + ec];
+            y_b += g;
 #pragma unroll
-          for (int s = 0; s < S; s++) {
-            double v = T::w(s, NI - 1);
+            for (int s = 0; s < S; s++) {
+              double v = T::w(s, NI - 1);
 #pragma unroll
-            for (int j = NI - 2; j >= 0; j--) v = fma(v, theta, T::w(s, j));
-            kb[s * D + tid] = fma(h * (v * theta), g, kb[s * D + tid]);
+              for (int j = NI - 2; j >= 0; j--) v = fma(v, theta, T::w(s, j));
+              kb[(s * R) * D + tid] = fma(h_e * (v * theta), g, kb[(s * R) * D + tid]);
+            }
           }
         }
         yb[tid] = y_b;
       }
-      hi = lo;
       __syncthreads();
+      if (tid < R && rs[4 * tid + 3] != 0.0) s_hi[tid] = (int64_t)rs[4 * tid + 2];
       // ---- reverse sweep through the stages
       for (int s = S - 1; s >= 0; s--) {
-        if (own_c) {
-          const float g = (float)kb[s * D + tid];
-          gf[tid] = g;
+        if (own_e) {
+          const float g = (float)kb[(s * R) * D + tid];
+          gf[er * 64 + ec] = g;
           gb2 += g;
         }
         __syncthreads();
         if (own_j) {
-          float u = 0.0f;
+          float u[R];
+#pragma unroll
+          for (int r = 0; r < R; r++) u[r] = 0.0f;
           const float* w = W2p + tid;
-#pragma unroll 16
-          for (int o = 0; o < D; o++) u = fmaf(w[o * (kThreads + 1)], gf[o], u);
-          const float hj = Hs[s * kThreads + tid];
-          const float v = u * (1.0f - hj * hj);
-          Vs[tid] = v;
-          gb1 += v;
-          const float* yf = Yf + s * D;
+#pragma unroll 8
+          for (int o = 0; o < D; o++) {
+            const float wo = w[o * (kThreads + 1)];
+#pragma unroll
+            for (int r = 0; r < R; r++) u[r] = fmaf(wo, gf[r * 64 + o], u[r]);
+          }
+          float v[R], hj[R];
+#pragma unroll
+          for (int r = 0; r < R; r++) {
+            hj[r] = Hs[(s * R + r) * kThreads + tid];
+            v[r] = u[r] * (1.0f - hj[r] * hj[r]);
+            Vs[r * kThreads + tid] = v[r];
+            gb1 += v[r];
+          }
+          const float* yf = Yf + (s * R) * D;
 #pragma unroll
           for (int c = 0; c < D; c++) {
-            gW1[c] = fmaf(v, yf[c], gW1[c]);
-            gW2[c] = fmaf(gf[c], hj, gW2[c]);
+#pragma unroll
+            for (int r = 0; r < R; r++) {
+              gW1[c] = fmaf(v[r], yf[r * D + c], gW1[c]);
+              gW2[c] = fmaf(gf[r * 64 + c], hj[r], gW2[c]);
+            }
           }
         }
         __syncthreads();
         if (po < D) {
-          float acc = 0.0f;
-          for (int j = j_lo; j < j_hi; j++) acc = fmaf(W1p[j * (D + 1) + po], Vs[j], acc);
-          Pp[part * 64 + po] = acc;
+          float acc[R];
+#pragma unroll
+          for (int r = 0; r < R; r++) acc[r] = 0.0f;
+          for (int j = j_lo; j < j_hi; j++) {
+            const float wj = W1p[j * (D + 1) + po];
+#pragma unroll
+            for (int r = 0; r < R; r++) acc[r] = fmaf(wj, Vs[r * kThreads + j], acc[r]);
+          }
+#pragma unroll
+          for (int r = 0; r < R; r++) Pp[(r * 4 + part) * 64 + po] = acc[r];
         }
         __syncthreads();
-        if (own_c) {
-          const double Yb = (double)((Pp[tid] + Pp[64 + tid]) + (Pp[128 + tid] + Pp[192 + tid]));
+        if (own_e) {
+          const float* pp = Pp + er * 256 + ec;
+          const double Yb = (double)((pp[0] + pp[64]) + (pp[128] + pp[192]));
           yb[tid] += Yb;
           for (int j = 0; j < s; j++)
-            if (T::za(s, j) != 0.0) kb[j * D + tid] = fma(h * T::a(s, j), Yb, kb[j * D + tid]);
+            if (T::za(s, j) != 0.0) kb[(j * R) * D + tid] = fma(h_e * T::a(s, j), Yb, kb[(j * R) * D + tid]);
         }
         __syncthreads();
       }
-      if (own_c) ab[tid] = yb[tid];
+      if (act_e) ab[tid] = yb[tid];
       __syncthreads();
     }
-    if (own_c) {
+    if (own_e && s_inst[er] >= 0) {
+      const int64_t i = s_inst[er];
+      const double* gy = A.t_eval_offsets ? A.grad_ys + A.t_eval_offsets[i] * D
+                                          : A.grad_ys + i * A.t_eval_len * D;
       double a0 = ab[tid];
-      for (int64_t p = 0; p < hi; p++) a0 += gy[p * D + tid];  // points at t_start
-      A.grad_y0[i * D + tid] = a0;
+      for (int64_t p = 0; p < s_hi[er]; p++) a0 += gy[p * D + ec];  // points at t_start
+      A.grad_y0[i * D + ec] = a0;
     }
-    if (A.grad_params && tid < 8) A.grad_params[i * 8 + tid] = 0.0;
     __syncthreads();
   }
   // per-CTA partial weight gradients: [dW1 (H,D) | dW2 (D,H) | db1 (H) | db2 (D)]
+  // (gb2 partials of the R row-threads of a component are summed through smem)
+  float* red = Pp;
+  if (own_e) red[tid] = gb2;
+  __syncthreads();
   float* out = A.mlp_part + (size_t)blockIdx.x * (2 * D * H + H + D);
   if (own_j) {
 #pragma unroll
@@ -210,7 +291,11 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_adjoint_kernel(const AdjParam
     }
     out[2 * D * H + tid] = gb1;
   }
-  if (own_c) out[2 * D * H + H + tid] = gb2;
+  if (tid < D) {
+    float sb = 0.0f;
+    for (int r = 0; r < R; r++) sb += red[r * D + tid];
+    out[2 * D * H + H + tid] = sb;
+  }
 }
 
 __global__ void mlp_grad_reduce_kernel(const float* part, int blocks, int D, int H, float* gW1,
