@@ -120,20 +120,21 @@ int validate(const bode_solve_args* a) {
   return BODE_OK;
 }
 
-// Workspace: [header | iteration bitmap | f0 (n x d) | LPT scratch x slots | MLP scratch]
+// Workspace: [header | iteration bitmap | f0 (n x d) | te_next (n) | LPT scratch x slots | MLP scratch]
 // Header: queue counter of slot 0 at +0, max n_steps at +8, queue counter of
 // slot 1 at +16.  Pipelined host solves run consecutive chunks on two
 // streams (slots 0/1), so a chunk's solve can fill the SMs the previous
 // chunk's tail leaves idle; each slot has its own queue and LPT scratch, and
 // f0 rows are indexed by absolute instance.
 struct Layout {
-  size_t f0, lpt, lpt_slot, mlp, total;
+  size_t f0, tn, lpt, lpt_slot, mlp, total;
 };
 
 Layout layout(const bode_solve_args* a, int64_t n_chunk, int slots) {
   Layout L;
   L.f0 = Workspace::f0_offset(a->max_steps);
-  L.lpt = L.f0 + ((8 * (size_t)a->n * (size_t)a->d + 255) & ~(size_t)255);
+  L.tn = L.f0 + ((8 * (size_t)a->n * (size_t)a->d + 255) & ~(size_t)255);
+  L.lpt = L.tn + ((8 * (size_t)a->n + 255) & ~(size_t)255);
   L.lpt_slot = a->cost_hint && !a->order ? ((lpt_workspace_bytes(n_chunk) + 255) & ~(size_t)255) : 0;
   L.mlp = L.lpt + L.lpt_slot * slots;
   L.total = L.mlp + (a->dyn.kind == BODE_DYN_MLP ? mlp_workspace_bytes(a) : 0);
@@ -203,6 +204,7 @@ int run_chunk(const bode_solve_args* a, int64_t lo, int64_t hi, const Layout& L,
   const size_t words = Workspace::bitmap_words(a->max_steps);
   P.smem_words = words * 4 <= 32 * 1024 ? (int32_t)words : 0;  // per-block shared bitmap
   P.f0 = (double*)(ws + L.f0) + lo * d;
+  P.te_next = (double*)(ws + L.tn) + lo;
   P.ev_start = a->prof_event_start;
   P.ev_stop = a->prof_event_stop;
   if (a->order) {

@@ -59,6 +59,7 @@ struct SolveParams {
   uint32_t* refresh;           // global bitmap over iterations
   int32_t smem_words;          // >0: per-block shared bitmap of this many words
   double* f0;                  // (n, D) FSAL seeds from the init pass
+  double* te_next;             // (n) first pending output time from the init pass
   void* ev_start;              // host side only: optional cudaEvent_t around
   void* ev_stop;               // the persistent launch (bench roofline)
 };
@@ -160,6 +161,7 @@ struct Lane {
     if (status == BODE_RUNNING) {
 #pragma unroll
       for (int c = 0; c < D; c++) P.f0[i * D + c] = k[0][c];
+      P.te_next[i] = cursor < m ? te[cursor] : 0.0;
       P.final_dt[i] = dt;
       P.n_emitted[i] = cursor;
       P.status[i] = BODE_RUNNING;
@@ -175,7 +177,7 @@ struct Lane {
     for (int c = 0; c < D; c++) k[0][c] = P.f0[i * D + c];
     dt = P.final_dt[i];
     cursor = (int32_t)P.n_emitted[i];
-    te_next = cursor < m ? te_of(P)[cursor] : 0.0;
+    te_next = P.te_next[i];  // no load dependent on cursor
     status = BODE_RUNNING;
     L1.ok = cr_log(1.0, g_pow_tables, L1.h, L1.l);  // log(1) = 0 exactly (both modes)
   }
@@ -323,8 +325,11 @@ __global__ void __launch_bounds__(128, (F::D <= 2 && !REC ? BODE_BLOCKS_2D : 4))
           done = true;
         } else {
           const int64_t i = P.order ? P.order[pos] : (int64_t)pos;
-          if (P.status[i] == BODE_RUNNING) {  // else finalised by the init pass
-            L.resume(P, i);
+          // every load of the refill issues at once (one round trip after
+          // the order lookup); a row the init pass finalised is dropped
+          const int64_t st = P.status[i];
+          L.resume(P, i);
+          if (st == BODE_RUNNING) {
             if constexpr (REC) s_trec[threadIdx.x] = P.traj + P.traj_offsets[i] * kTrajStride<F::D>;
             have = true;
           }
