@@ -78,6 +78,14 @@ struct Workspace {
   }
 };
 
+// per-lane output bases (t_eval row, ys row) kept in shared memory from
+// the refill on, so a lane emitting a point does not stall its warp on a
+// dependent offsets load
+struct EmitBase {
+  const double* te;
+  double* ys;
+};
+
 template <int M, class F, class O>
 struct Lane {
   using T = Tab<M>;
@@ -192,7 +200,7 @@ struct Lane {
   // compiled into the loop
   template <bool PI>
   __device__ __forceinline__ bool step(const SolveParams& P, const PowTables& PT, bool tracing,
-                                       double* const* trec) {
+                                       double* const* trec, const EmitBase& eb) {
     const int32_t j = nsteps;
     const double remaining = O::sub(t_end, t);
     const bool trunc = fabs(dt) >= fabs(remaining);
@@ -233,7 +241,7 @@ struct Lane {
         // emitted); |t_eval[cursor] - t_old| > 2|h| means theta > 2, so the
         // exact division is only needed near a point
         const double diff = O::sub(te_next, t_old);
-        if (!(fabs(diff) > 2.0 * fabs(h))) emit(P, t_old, h);
+        if (!(fabs(diff) > 2.0 * fabs(h))) emit(eb, t_old, h);
       }
 #pragma unroll
       for (int c = 0; c < D; c++) y[c] = yn[c];
@@ -252,9 +260,9 @@ struct Lane {
 
   // _emit, solver.py:284-322: every point with theta in (.., 1] is
   // interpolated from the pre-commit state (y is still y_old here)
-  __device__ __forceinline__ void emit(const SolveParams& P, double t_old, double h) {
-    const double* te = te_of(P);
-    double* ys = ys_of(P);
+  __device__ __forceinline__ void emit(const EmitBase& eb, double t_old, double h) {
+    const double* te = eb.te;
+    double* ys = eb.ys;
     while (cursor < m) {
       double theta = ddiv(O::sub(te_next, t_old), h);
       if (!(theta <= 1.0)) break;
@@ -308,6 +316,7 @@ __global__ void __launch_bounds__(128, (F::D <= 2 && !REC ? BODE_BLOCKS_2D : 4))
   const bool tracing = P.trace_cap > 0;  // uniform: hoisted out of the step loop
   __shared__ double* s_trec[REC ? 128 : 1];  // per-lane trajectory row base
   double* const* trec = REC ? &s_trec[threadIdx.x] : nullptr;
+  __shared__ EmitBase s_eb[128];
   bool have = false, done = false;
   unsigned long long my_max = 0;
   const unsigned lt_mask = (1u << lane) - 1u;
@@ -329,6 +338,7 @@ __global__ void __launch_bounds__(128, (F::D <= 2 && !REC ? BODE_BLOCKS_2D : 4))
           // the order lookup); a row the init pass finalised is dropped
           const int64_t st = P.status[i];
           L.resume(P, i);
+          s_eb[threadIdx.x] = EmitBase{L.te_of(P), L.ys_of(P)};
           if (st == BODE_RUNNING) {
             if constexpr (REC) s_trec[threadIdx.x] = P.traj + P.traj_offsets[i] * kTrajStride<F::D>;
             have = true;
@@ -342,7 +352,7 @@ __global__ void __launch_bounds__(128, (F::D <= 2 && !REC ? BODE_BLOCKS_2D : 4))
     }
     if (have) {
       const int64_t j = L.nsteps;
-      if (L.template step<PI>(P, s_pow, tracing, trec)) {
+      if (L.template step<PI>(P, s_pow, tracing, trec, s_eb[threadIdx.x])) {
         const uint64_t bit = (uint64_t)j + 1;
         const uint32_t w = (uint32_t)(bit >> 5), msk = 1u << (bit & 31);
         if (P.smem_words > 0) {
