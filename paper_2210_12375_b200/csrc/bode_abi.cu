@@ -331,8 +331,9 @@ int bode_solve_adjoint(const bode_solve_args* a, const bode_adjoint_args* g) {
   if (!g) return fail(BODE_EINVAL, "null adjoint args");
   if (a->joint) return fail(BODE_EUNSUPPORTED, "gradients: independent solve only");
   if (a->dyn.kind == BODE_DYN_MLP &&
-      !((a->d == 4 || a->d == 8 || a->d == 16 || a->d == 32 || a->d == 64) && a->dyn.hidden <= 256))
-    return fail(BODE_EUNSUPPORTED, "MLP gradients: d in {4, 8, 16, 32, 64}, hidden <= 256");
+      !((a->d == 4 || a->d == 8 || a->d == 16 || a->d == 32 || a->d == 64) &&
+        a->dyn.hidden <= 256 && a->dyn.hidden % 16 == 0))
+    return fail(BODE_EUNSUPPORTED, "MLP gradients: d in {4, 8, 16, 32, 64}, hidden <= 256, multiple of 16");
   if (!g->traj || !g->traj_offsets || !g->n_emitted || !g->grad_y0)
     return fail(BODE_EINVAL, "adjoint needs traj, traj_offsets, n_emitted and grad_y0");
   if ((a->t_eval_offsets || a->t_eval_len > 0) && !g->grad_ys)

@@ -32,10 +32,15 @@ namespace {
 constexpr int kThreads = 256;
 constexpr int kRows = 4;  // instances reversed together by one CTA
 
+// weight rows padded by 4 floats: 16-byte aligned rows for float4 reads
+// along a row, and conflict-free (row stride = 4 banks) for both row- and
+// column-wise access
+constexpr int kPad = 4;
+
 template <int D>
 constexpr size_t mlp_adj_smem(int S) {
   return 8 * ((size_t)2 * S * kRows * D + 3 * kRows * D + 4 * kRows) +
-         4 * ((size_t)kThreads * (D + 1) + (size_t)D * (kThreads + 1) +
+         4 * ((size_t)kThreads * (D + kPad) + (size_t)D * (kThreads + kPad) +
               (size_t)S * kRows * kThreads + (size_t)S * kRows * D + kRows * 4 * 64 +
               kRows * 64 + kRows * kThreads) + 64;
 }
@@ -57,9 +62,10 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_adjoint_kernel(const AdjParam
   double* yb = yv + R * D;                           // [R][D] running dL/dy_old
   double* ab = yb + R * D;                           // [R][D] dL/dy_next
   double* rs = ab + R * D;                           // [R][4] t_old, h, lo, active
-  float* W1p = reinterpret_cast<float*>(rs + 4 * R);  // [H][D+1]
-  float* W2p = W1p + kThreads * (D + 1);             // [D][H+1]
-  float* Hs = W2p + D * (kThreads + 1);              // [S][R][256] tanh activations
+  constexpr int L1 = D + kPad, L2 = kThreads + kPad;  // padded row lengths
+  float* W1p = reinterpret_cast<float*>(rs + 4 * R);  // [H][L1]
+  float* W2p = W1p + kThreads * L1;                  // [D][L2]
+  float* Hs = W2p + D * L2;                          // [S][R][256] tanh activations
   float* Yf = Hs + S * R * kThreads;                 // [S][R][D] fp32 stage inputs
   float* Pp = Yf + S * R * D;                        // [R][4][64] partial sums
   float* gf = Pp + R * 4 * 64;                       // [R][64] fp32 stage adjoint
@@ -69,9 +75,9 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_adjoint_kernel(const AdjParam
 
   for (int e = tid; e < H * D; e += kThreads) {
     const int j = e / D, c = e % D;
-    W1p[j * (D + 1) + c] = A.W1[e];
+    W1p[j * L1 + c] = A.W1[e];
     const int o = e / H, jj = e % H;
-    W2p[o * (kThreads + 1) + jj] = A.W2[e];
+    W2p[o * L2 + jj] = A.W2[e];
   }
   const bool own_j = tid < H;
   const int er = tid / D, ec = tid % D;  // (row, component) of this thread
@@ -140,13 +146,16 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_adjoint_kernel(const AdjParam
           float z[R];
 #pragma unroll
           for (int r = 0; r < R; r++) z[r] = b1j;
-          const float* w = W1p + tid * (D + 1);
+          const float4* w = reinterpret_cast<const float4*>(W1p + tid * L1);
           const float* yf = Yf + (s * R) * D;
-#pragma unroll 8
-          for (int c = 0; c < D; c++) {
-            const float wc = w[c];
+#pragma unroll 4
+          for (int c4 = 0; c4 < D / 4; c4++) {
+            const float4 wc = w[c4];
 #pragma unroll
-            for (int r = 0; r < R; r++) z[r] = fmaf(wc, yf[r * D + c], z[r]);
+            for (int r = 0; r < R; r++) {
+              const float4 y4 = reinterpret_cast<const float4*>(yf + r * D)[c4];
+              z[r] = fmaf(wc.x, y4.x, fmaf(wc.y, y4.y, fmaf(wc.z, y4.z, fmaf(wc.w, y4.w, z[r]))));
+            }
           }
 #pragma unroll
           for (int r = 0; r < R; r++) Hs[(s * R + r) * kThreads + tid] = tanhf(z[r]);
@@ -156,12 +165,15 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_adjoint_kernel(const AdjParam
           float acc[R];
 #pragma unroll
           for (int r = 0; r < R; r++) acc[r] = 0.0f;
-          const float* w = W2p + po * (kThreads + 1);
+          const float* w = W2p + po * L2;
           const float* hs = Hs + (s * R) * kThreads;
-          for (int j = j_lo; j < j_hi; j++) {
-            const float wj = w[j];
+          for (int j = j_lo; j < j_hi; j += 4) {
+            const float4 w4 = *reinterpret_cast<const float4*>(w + j);
 #pragma unroll
-            for (int r = 0; r < R; r++) acc[r] = fmaf(wj, hs[r * kThreads + j], acc[r]);
+            for (int r = 0; r < R; r++) {
+              const float4 h4 = *reinterpret_cast<const float4*>(hs + r * kThreads + j);
+              acc[r] = fmaf(w4.x, h4.x, fmaf(w4.y, h4.y, fmaf(w4.z, h4.z, fmaf(w4.w, h4.w, acc[r]))));
+            }
           }
 #pragma unroll
           for (int r = 0; r < R; r++) Pp[(r * 4 + part) * 64 + po] = acc[r];
@@ -217,11 +229,15 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_adjoint_kernel(const AdjParam
 #pragma unroll
           for (int r = 0; r < R; r++) u[r] = 0.0f;
           const float* w = W2p + tid;
-#pragma unroll 8
-          for (int o = 0; o < D; o++) {
-            const float wo = w[o * (kThreads + 1)];
+#pragma unroll 4
+          for (int o4 = 0; o4 < D / 4; o4++) {
+            const float w0 = w[(4 * o4) * L2], w1 = w[(4 * o4 + 1) * L2];
+            const float w2 = w[(4 * o4 + 2) * L2], w3 = w[(4 * o4 + 3) * L2];
 #pragma unroll
-            for (int r = 0; r < R; r++) u[r] = fmaf(wo, gf[r * 64 + o], u[r]);
+            for (int r = 0; r < R; r++) {
+              const float4 g4 = reinterpret_cast<const float4*>(gf + r * 64)[o4];
+              u[r] = fmaf(w0, g4.x, fmaf(w1, g4.y, fmaf(w2, g4.z, fmaf(w3, g4.w, u[r]))));
+            }
           }
           float v[R], hj[R];
 #pragma unroll
@@ -233,11 +249,19 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_adjoint_kernel(const AdjParam
           }
           const float* yf = Yf + (s * R) * D;
 #pragma unroll
-          for (int c = 0; c < D; c++) {
+          for (int c4 = 0; c4 < D / 4; c4++) {
 #pragma unroll
             for (int r = 0; r < R; r++) {
-              gW1[c] = fmaf(v[r], yf[r * D + c], gW1[c]);
-              gW2[c] = fmaf(gf[r * 64 + c], hj[r], gW2[c]);
+              const float4 y4 = reinterpret_cast<const float4*>(yf + r * D)[c4];
+              const float4 g4 = reinterpret_cast<const float4*>(gf + r * 64)[c4];
+              gW1[4 * c4] = fmaf(v[r], y4.x, gW1[4 * c4]);
+              gW1[4 * c4 + 1] = fmaf(v[r], y4.y, gW1[4 * c4 + 1]);
+              gW1[4 * c4 + 2] = fmaf(v[r], y4.z, gW1[4 * c4 + 2]);
+              gW1[4 * c4 + 3] = fmaf(v[r], y4.w, gW1[4 * c4 + 3]);
+              gW2[4 * c4] = fmaf(g4.x, hj[r], gW2[4 * c4]);
+              gW2[4 * c4 + 1] = fmaf(g4.y, hj[r], gW2[4 * c4 + 1]);
+              gW2[4 * c4 + 2] = fmaf(g4.z, hj[r], gW2[4 * c4 + 2]);
+              gW2[4 * c4 + 3] = fmaf(g4.w, hj[r], gW2[4 * c4 + 3]);
             }
           }
         }
@@ -246,10 +270,14 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_adjoint_kernel(const AdjParam
           float acc[R];
 #pragma unroll
           for (int r = 0; r < R; r++) acc[r] = 0.0f;
-          for (int j = j_lo; j < j_hi; j++) {
-            const float wj = W1p[j * (D + 1) + po];
+          for (int j = j_lo; j < j_hi; j += 4) {
+            const float w0 = W1p[j * L1 + po], w1 = W1p[(j + 1) * L1 + po];
+            const float w2 = W1p[(j + 2) * L1 + po], w3 = W1p[(j + 3) * L1 + po];
 #pragma unroll
-            for (int r = 0; r < R; r++) acc[r] = fmaf(wj, Vs[r * kThreads + j], acc[r]);
+            for (int r = 0; r < R; r++) {
+              const float4 v4 = *reinterpret_cast<const float4*>(Vs + r * kThreads + j);
+              acc[r] = fmaf(w0, v4.x, fmaf(w1, v4.y, fmaf(w2, v4.z, fmaf(w3, v4.w, acc[r]))));
+            }
           }
 #pragma unroll
           for (int r = 0; r < R; r++) Pp[(r * 4 + part) * 64 + po] = acc[r];
