@@ -135,3 +135,60 @@ def test_cli_parser_mirrors_reference_flags():
             p.parse_args(bad)
         assert e.value.code == 2
     assert cli.main(["pid-sweep", "--presets", "nope", "--out", "/dev/null"]) == 2
+
+
+def _valid_args(kind="vdp", d=2, hidden=0):
+    a = _abi.SolveArgs()
+    a.abi_version = _abi.ABI_VERSION
+    a.n, a.d = 4, d
+    a.dyn.kind = _abi.DYN[kind]
+    a.dyn.hidden = hidden
+    if kind == "mlp":  # fake non-null pointers: validation never dereferences them
+        a.dyn.W1 = a.dyn.b1 = a.dyn.W2 = a.dyn.b2 = 0x1000
+    a.ctrl.beta1, a.ctrl.safety, a.ctrl.factor_min, a.ctrl.factor_max = 1.0, 0.9, 0.2, 10.0
+    a.max_steps = 10
+    a.atol = a.rtol = 1e-6
+    a.y0 = a.t_start = a.t_end = 0x1000
+    a.n_emitted = a.n_steps = a.n_accepted = a.final_dt = a.status = a.n_f_evals = 0x1000
+    return a
+
+
+def test_adjoint_abi_validation_without_gpu():
+    """bode_solve_adjoint / trajectory recording reject what they do not
+    support before touching the device (BODE_EINVAL / BODE_EUNSUPPORTED)."""
+    lib = _abi.load()
+    a = _valid_args()
+    assert lib.bode_adjoint_workspace_size(C.byref(a)) > 0
+    g = _abi.AdjointArgs()
+    with pytest.raises(ValueError, match="traj"):  # no trajectory
+        _abi.check(lib.bode_solve_adjoint(C.byref(a), C.byref(g)))
+    g.traj = g.traj_offsets = g.n_emitted = g.grad_y0 = 0x1000
+    with pytest.raises(ValueError, match="workspace"):
+        _abi.check(lib.bode_solve_adjoint(C.byref(a), C.byref(g)))
+    a.joint = 1
+    with pytest.raises(NotImplementedError):
+        _abi.check(lib.bode_solve_adjoint(C.byref(a), C.byref(g)))
+    m = _valid_args("mlp", d=6, hidden=32)  # MLP widths outside the compiled set
+    with pytest.raises(NotImplementedError, match="MLP gradients"):
+        _abi.check(lib.bode_solve_adjoint(C.byref(m), C.byref(g)))
+    m = _valid_args("mlp", d=8, hidden=40)  # hidden not a multiple of 16
+    with pytest.raises(NotImplementedError, match="MLP gradients"):
+        _abi.check(lib.bode_solve_adjoint(C.byref(m), C.byref(g)))
+    r = _valid_args()
+    r.traj = 0x1000  # recording without offsets
+    with pytest.raises(ValueError, match="traj_offsets"):
+        _abi.check(lib.bode_solve(C.byref(r)))
+    assert _abi.traj_stride(2) == 8 and _abi.traj_stride(64) == 68 and _abi.traj_stride(1) == 4
+
+
+def test_adjoint_oracle_tableau_matches_product_tableau():
+    """The gradient oracle's coefficients (parsed from the generated header)
+    equal the facade's ButcherTableau data (pinned to the reference)."""
+    import adjoint_oracle as AO
+
+    for name, tab in (("dopri5", bode.dopri5()), ("tsit5", bode.tsit5()), ("heun", bode.heun())):
+        T = AO.tableau(name)
+        S = T["S"]
+        assert np.array_equal(T["a"], np.asarray(tab.a)[:S, :S])
+        assert np.array_equal(T["b"], np.asarray(tab.b)[:S])
+        assert np.array_equal(T["c"], np.asarray(tab.c)[:S])
