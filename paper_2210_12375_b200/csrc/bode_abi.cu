@@ -387,8 +387,9 @@ int bode_solve_host(const bode_solve_args* h) {
   if (h->order || h->trace_cap > 0 || h->dyn.kind == BODE_DYN_MLP || h->joint) chunks = 1;
   if (chunks > n) chunks = (int)n;
   if (chunks > 64) chunks = 64;
-  // largest chunk (the middle ones when the first/last are half-size)
-  const int64_t cmax = chunks >= 3 ? (n + chunks - 2) / (chunks - 1) + 1 : chunk_max(n, chunks);
+  // largest chunk (a middle one when the first/last are smaller); sized for
+  // the smallest edge fraction BODE_EDGE_FRAC may request (0.1)
+  const int64_t cmax = chunks >= 3 ? (int64_t)((double)n / ((chunks - 2) + 0.2)) + 2 : chunk_max(n, chunks);
 
   // one device block for every array; per-instance arrays move in chunk
   // slices so chunk k can start as soon as its own rows landed.  Pinned
@@ -498,13 +499,18 @@ int bode_solve_host(const bode_solve_args* h) {
     cudaStreamWaitEvent(cout, ready, 0);
     if (st2 != st) cudaStreamWaitEvent(st2, ready, 0);
   }
-  // chunk boundaries: the first and last chunks are half-size, so the
-  // first solve starts (and the last download ends) sooner
+  // chunk boundaries: the first and last chunks are `edge` of a middle
+  // chunk (half; BODE_EDGE_FRAC overrides it -- on C2, 3 chunks: 4.23 ms e2e
+  // at 0.5 and 0.3, 4.90 at 0.15), so the first solve starts (and the last
+  // download ends) sooner
+  double edge = 0.5;
+  if (const char* ev = std::getenv("BODE_EDGE_FRAC")) edge = std::atof(ev);
+  if (!(edge >= 0.1 && edge <= 1.0)) edge = 0.5;
   int64_t bnd[65];
   bnd[0] = 0;
   for (int k = 1; k <= chunks; k++) {
-    const double units = chunks >= 3 ? 2.0 * (chunks - 1) : (double)chunks;  // in half-chunks
-    const double done = chunks >= 3 ? (k == chunks ? units : 2.0 * k - 1.0) : (double)k;
+    const double units = chunks >= 3 ? (chunks - 2) + 2.0 * edge : (double)chunks;
+    const double done = chunks >= 3 ? (k == chunks ? units : edge + (k - 1)) : (double)k;
     bnd[k] = k == chunks ? n : (int64_t)((double)n * done / units);
   }
   auto rows = [&](int k, int64_t& lo, int64_t& hi) {
