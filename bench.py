@@ -476,7 +476,11 @@ def run_bode(args, rank, world, local_rank):
             config=dict(workload=cfg["workload"], instances_per_gpu=n,
                         global_instances=n * world, method=cfg["method"],
                         controller="PI42" if cfg["ctrl"] is PI42 else "I",
-                        tol=cfg["tol"], mode=args.mode, lpt_order=bool(args.lpt),
+                        tol=cfg["tol"],
+                        # the MLP path has one arithmetic mode: the reference's
+                        # operation order in its fp64 control (bode_mlp*.cu)
+                        mode=args.mode if cfg["dyn"] != "mlp" else "exact (MLP control)",
+                        lpt_order=bool(args.lpt),
                         parallelism=f"shard{world}", l2="flushed (256 MiB write) between steps",
                         accepted_per_step=accepted / args.steps,
                         attempted_per_step=attempted / args.steps),
