@@ -9,7 +9,7 @@ PI42 = dict(betas=(0.6, -0.2, 0.0), safety=0.9, factor_min=0.2, factor_max=10.0,
 INTEGRAL = dict(betas=(1.0, 0.0, 0.0), safety=0.9, factor_min=0.2, factor_max=10.0, hist=True)
 SLOTS = {"vdp": ("mu",), "lorenz": ("sigma", "rho", "beta"), "linear_cos": ("lam", "amp", "omega"),
          "damped": (), "harmonic": (), "logistic": (), "relax_cos": ("lam", "omega"),
-         "linear": ("lam",), "sin_plus_t": ()}
+         "linear": ("lam",), "sin_plus_t": (), "square": ("thr",)}
 
 
 def case(name: str, n: int = 16):
@@ -54,11 +54,17 @@ def case(name: str, n: int = 16):
         te = np.linspace(0.0, 8.0, 17)
         return dict(method="dopri5", dyn="vdp", params={"mu": mu}, y0=y0, t_start=0.0,
                     t_end=np.full(n, 8.0), t_eval=[te] * n, ctrl=INTEGRAL, tol=1e-6, max_steps=60)
+    if name == "square_blowup":  # y' = y^2: STEP_UNDERFLOW rows, INFINITE_DYNAMICS at init
+        y0 = np.resize(np.array([0.3, 0.45, 0.9, 2.0]), n)[:, None] * np.ones((n, 1))
+        te = np.linspace(0.0, 2.0, 5)
+        return dict(method="dopri5", dyn="square", params={"thr": 1.5}, y0=y0, t_start=0.0,
+                    t_end=np.full(n, 2.0), t_eval=[te] * n, ctrl=INTEGRAL, tol=1e-6,
+                    max_steps=100_000)
     raise KeyError(name)
 
 
 CASES = ["vdp_pi42", "lorenz_tsit5", "linear_cos_heun", "damped_backward", "relax_cos_tsit5",
-         "vdp_max_steps"]
+         "vdp_max_steps", "square_blowup"]
 
 
 def oracle_dyn(c: dict) -> dict:
