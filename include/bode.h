@@ -215,10 +215,12 @@ typedef struct bode_solve_args {
   /* optional (gradients, bode_solve_adjoint): record every accepted step.
    * Row traj_offsets[i] + k (k < n_accepted[i]) receives the k-th accepted
    * step of instance i: t_old, h, the t_eval cursor before the step,
-   * y_old[d], padded to BODE_TRAJ_STRIDE(d) doubles (whole 32-byte sectors,
-   * so the scattered per-instance row writes never partially fill one).  traj_offsets (n+1) is the exclusive
-   * prefix sum of n_accepted from an earlier identical solve (the solve is
-   * deterministic).  Analytic dynamics only; not with joint. */
+   * y_old[d], padded to BODE_TRAJ_STRIDE(d) doubles (whole 32-byte
+   * sectors, so the scattered per-instance row writes never partially fill
+   * one).  traj_offsets (n+1) is the exclusive prefix sum of n_accepted
+   * from an earlier identical solve (the solve is deterministic).  Not with
+   * joint.  MLP dynamics record through the lockstep tensor-core path
+   * (bit-identical to the fused kernel). */
   double* traj;
   const int64_t* traj_offsets;
 } bode_solve_args;
