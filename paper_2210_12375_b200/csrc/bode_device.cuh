@@ -417,6 +417,15 @@ struct CtrlParams {
 };
 
 // 1/x to ~1 ulp: hardware approximation + two Newton steps (fast mode only)
+// 1/x to ~2^-46 relative (one Newton step): enough for the squared-norm
+// controller, whose accept decisions only move when a norm lies within
+// that distance of 1
+__device__ __forceinline__ double fast_rcp1(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  return fma(r, fma(-x, r, 1.0), r);
+}
+
 __device__ __forceinline__ double fast_rcp(double x) {
   double r;
   asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
@@ -460,7 +469,7 @@ __device__ __forceinline__ double error_ms(const double* e, const double* y0, co
 #pragma unroll
   for (int j = 0; j < D; j++) {
     const double scale = O::mad(rtol, np_max(fabs(y0[j]), fabs(y1[j])), atol);
-    const double r = e[j] * fast_rcp(scale);
+    const double r = e[j] * fast_rcp1(scale);
     sq[j] = O::mul(r, r);
   }
   const double s = pairwise_sum<D, O>(sq);
