@@ -468,7 +468,9 @@ __device__ __forceinline__ double error_ms(const double* e, const double* y0, co
   double sq[D];
 #pragma unroll
   for (int j = 0; j < D; j++) {
-    const double scale = O::mad(rtol, np_max(fabs(y0[j]), fabs(y1[j])), atol);
+    // fmax instead of NumPy's NaN-propagating maximum: a NaN |y1| implies a
+    // NaN error estimate here, so the ratio is NaN (-> rejection) either way
+    const double scale = O::mad(rtol, fmax(fabs(y0[j]), fabs(y1[j])), atol);
     const double r = e[j] * fast_rcp1(scale);
     sq[j] = O::mul(r, r);
   }
@@ -614,7 +616,7 @@ __device__ __forceinline__ bool adapt_pi_ms(const CtrlParams& C, double ms, LogC
       double y = fma(C.e1, La.h, C.e1 * La.l);
       if (C.e2 != 0.0) y = fma(C.e2, L1.h, fma(C.e2, L1.l, y));
       if (y < 700.0 && y > -700.0)
-        factor = np_min(np_max(C.safety * fast_exp(y, T), C.fmin), C.fmax);
+        factor = fmin(fmax(C.safety * fast_exp(y, T), C.fmin), C.fmax);  // finite, > 0
       else
         factor = (y > 0.0 && y < 709.78) ? C.fmax : C.fmin;
     }
