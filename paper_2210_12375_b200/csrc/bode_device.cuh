@@ -593,9 +593,10 @@ __device__ __forceinline__ bool adapt_cached(const CtrlParams& C, double norm, d
 //   factor  = safety * a^e1 * n1^e2 = safety * exp(e1 log a + e2 log n1)
 // with log a = log(ms)/2 (a = max(norm, NORM_FLOOR), controller.py:26), the
 // history term from the cached log of the previous norm, and ONE exp of the
-// combined exponent (a few ulp, like the two ~1-ulp pows it replaces: the
-// accept decisions are insensitive at that level -- statuses and step counts
-// stay equal to the oracle's at full scale, tests/test_gpu_parity.py).  The
+// combined exponent (fast_log1 / fast_exp3: a few ulp, like the two ~1-ulp
+// pows it replaces: the accept decisions are insensitive at that level --
+// statuses and step counts stay equal to the oracle's at full scale,
+// tests/test_gpu_parity.py, tools/parity_report.py --extra fast).  The
 // non-finite cases resolve to what the reference computes: a = +inf or
 // n1 = +inf make the product 0 or inf, i.e. factor_min; an exponent beyond
 // the double range gives inf (factor_min) or a finite huge / tiny factor
@@ -605,18 +606,16 @@ __device__ __forceinline__ bool adapt_pi_ms(const CtrlParams& C, double ms, LogC
   const bool accept = ms <= 1.0000000000000002;
   LogCache La;
   La.ok = ms < INFINITY;
+  La.l = 0.0;  // single-double logs on this path (fast_log1)
   double factor = C.fmin;
   if (La.ok) {
     const bool tiny = !(ms >= 1e-20);  // norm below the floor: a = 1e-10 exactly
-    fast_log(tiny ? 1e-10 : ms, T, La.h, La.l);
-    const double sc = tiny ? 1.0 : 0.5;
-    La.h *= sc;
-    La.l *= sc;
+    La.h = fast_log1(tiny ? 1e-10 : ms, T) * (tiny ? 1.0 : 0.5);
     if (C.e2 == 0.0 || L1.ok) {
-      double y = fma(C.e1, La.h, C.e1 * La.l);
-      if (C.e2 != 0.0) y = fma(C.e2, L1.h, fma(C.e2, L1.l, y));
+      double y = C.e1 * La.h;
+      if (C.e2 != 0.0) y = fma(C.e2, L1.h, y);
       if (y < 700.0 && y > -700.0)
-        factor = fmin(fmax(C.safety * fast_exp(y, T), C.fmin), C.fmax);  // finite, > 0
+        factor = fmin(fmax(C.safety * fast_exp3(y, T), C.fmin), C.fmax);  // finite, > 0
       else
         factor = (y > 0.0 && y < 709.78) ? C.fmax : C.fmin;
     }

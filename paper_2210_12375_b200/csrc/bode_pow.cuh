@@ -294,6 +294,42 @@ BODE_HD double fast_exp(double y, const PowTables& T) {
   return from_bits(bits(res) + (ke << 52));
 }
 
+// Reduced-precision pair for the fast-mode I / PI controller
+// (bode_device.cuh adapt_pi_ms), whose step counts are insensitive below
+// ~1e-13 relative: log of a positive NORMAL finite x as one double (a few
+// ulp; the log1p series stops at r^6/6, |r| < 2^-7.9, omitted < 2^-58) and
+// exp with the series stopped at r^5/120 (omitted < 2^-56 relative).
+BODE_HD double fast_log1(double x, const PowTables& T) {
+  using namespace powimpl;
+  const int64_t ix = bits(x);
+  const int k = (int)(ix >> 52) - 1023;
+  const int i = (int)((ix >> 45) & 127);
+  const double m = from_bits((ix & 0x000FFFFFFFFFFFFFLL) | 0x3FF0000000000000LL);
+  const double r = fma_(m, T.log_tab[i][0], -1.0);
+  double q = fma_(BODE_PK(3), r, BODE_PK(4));  // 1/3 - r/4 + r^2/5 - r^3/6
+  q = fma_(q, r, BODE_PK(5));
+  q = fma_(q, r, BODE_PK(6));
+  const double p = fma_(mul(r, r), fma_(r, q, BODE_PK(7)), r);
+  const double kd = (double)k;
+  return add(fma_(kd, BODE_PK(14), T.log_tab[i][1]),
+             add(p, fma_(kd, BODE_PK(15), T.log_tab[i][2])));
+}
+
+BODE_HD double fast_exp3(double y, const PowTables& T) {
+  using namespace powimpl;
+  const double kd = rint(mul(y, BODE_PK(18)));
+  const int64_t kf = (int64_t)kd;
+  const int j = (int)(kf & 127);
+  const int64_t ke = (kf - j) / 128;
+  const double r = fma_(-kd, BODE_PK(17), fma_(-kd, BODE_PK(16), y));
+  double c = fma_(BODE_PK(10), r, BODE_PK(11));
+  c = fma_(c, r, BODE_PK(12));
+  c = fma_(c, r, BODE_PK(13));
+  const double p = fma_(mul(r, r), c, r);
+  const double th = T.exp_tab[j][0], tl = T.exp_tab[j][1];
+  return from_bits(bits(add(th, fma_(th, p, tl))) + (ke << 52));
+}
+
 // Correctly rounded (w.h.p.) x**e for x > 0 finite, e finite; everything
 // else -- and results near overflow/underflow -- goes to the libm pow.
 BODE_HD double cr_pow(double x, double e, const PowTables& T) {
