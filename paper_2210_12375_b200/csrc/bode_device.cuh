@@ -25,11 +25,17 @@ struct ExactOps {
   }
 };
 
+// Fast mode fuses exactly where the code says so (mad, explicit fma) and
+// nowhere else: mul/add/sub are round-to-nearest intrinsics, which the
+// compiler may not contract.  Implicit contraction is decided per
+// instantiation (it depends on register allocation), so without this the
+// trajectory-recording instantiation of the solver could round differently
+// from the plain one.
 struct FastOps {
   static constexpr bool kFast = true;
-  static __device__ __forceinline__ double mul(double a, double b) { return a * b; }
-  static __device__ __forceinline__ double add(double a, double b) { return a + b; }
-  static __device__ __forceinline__ double sub(double a, double b) { return a - b; }
+  static __device__ __forceinline__ double mul(double a, double b) { return __dmul_rn(a, b); }
+  static __device__ __forceinline__ double add(double a, double b) { return __dadd_rn(a, b); }
+  static __device__ __forceinline__ double sub(double a, double b) { return __dsub_rn(a, b); }
   static __device__ __forceinline__ double mad(double a, double b, double c) { return fma(a, b, c); }
 };
 
@@ -206,7 +212,11 @@ struct VdP {  // problems.py:45-48: (v, mu*(1-x*x)*v - x)
   __device__ __forceinline__ void operator()(double, const double* y, double* f) const {
     const double x = y[0], v = y[1];
     f[0] = v;
-    f[1] = O::sub(O::mul(O::mul(mu, O::sub(1.0, O::mul(x, x))), v), x);
+    if constexpr (O::kFast) {
+      f[1] = fma(__dmul_rn(mu, fma(-x, x, 1.0)), v, -x);
+    } else {
+      f[1] = O::sub(O::mul(O::mul(mu, O::sub(1.0, O::mul(x, x))), v), x);
+    }
   }
   // adjoint (bode_adjoint.cu): yb = J^T g, pb[slot] += (df/dp)^T g
   __device__ __forceinline__ void vjp(double, const double* y, const double* g, double* yb,
@@ -232,10 +242,11 @@ struct Lorenz {  // (s*(y-x), x*(r-z)-y, x*y - b*z)
   __device__ __forceinline__ void operator()(double, const double* y, double* f) const {
     const double x = y[0], yy = y[1], z = y[2];
     f[0] = O::mul(s, O::sub(yy, x));
-    f[1] = O::sub(O::mul(x, O::sub(r, z)), yy);
     if constexpr (O::kFast) {
-      f[2] = fma(x, yy, -(b * z));
+      f[1] = fma(x, __dsub_rn(r, z), -yy);
+      f[2] = fma(x, yy, -__dmul_rn(b, z));
     } else {
+      f[1] = O::sub(O::mul(x, O::sub(r, z)), yy);
       f[2] = O::sub(O::mul(x, yy), O::mul(b, z));
     }
   }
@@ -272,7 +283,11 @@ struct Damped {  // (y1, -y0 - 0.1*y1*|y1|)
   __device__ __forceinline__ void load(const DynParams&, int64_t) {}
   __device__ __forceinline__ void operator()(double, const double* y, double* f) const {
     f[0] = y[1];
-    f[1] = O::sub(-y[0], O::mul(O::mul(0.1, y[1]), fabs(y[1])));
+    if constexpr (O::kFast) {
+      f[1] = fma(-__dmul_rn(0.1, y[1]), fabs(y[1]), -y[0]);
+    } else {
+      f[1] = O::sub(-y[0], O::mul(O::mul(0.1, y[1]), fabs(y[1])));
+    }
   }
   __device__ __forceinline__ void vjp(double, const double* y, const double* g, double* yb,
                                       double*) const {
@@ -465,16 +480,23 @@ __device__ __forceinline__ double error_norm(const double* e, const double* y0, 
 template <int D, class O>
 __device__ __forceinline__ double error_ms(const double* e, const double* y0, const double* y1,
                                            double atol, double rtol) {
-  double sq[D];
+  double sq[D], rr[D];
 #pragma unroll
   for (int j = 0; j < D; j++) {
     // fmax instead of NumPy's NaN-propagating maximum: a NaN |y1| implies a
     // NaN error estimate here, so the ratio is NaN (-> rejection) either way
     const double scale = O::mad(rtol, fmax(fabs(y0[j]), fabs(y1[j])), atol);
-    const double r = e[j] * fast_rcp1(scale);
-    sq[j] = O::mul(r, r);
+    rr[j] = __dmul_rn(e[j], fast_rcp1(scale));
+    sq[j] = O::mul(rr[j], rr[j]);
   }
-  const double s = pairwise_sum<D, O>(sq);
+  double s;
+  if constexpr (D < 8) {  // NumPy's sequential order, the squares fused in
+    s = sq[0];
+#pragma unroll
+    for (int j = 1; j < D; j++) s = fma(rr[j], rr[j], s);
+  } else {
+    s = pairwise_sum<D, O>(sq);
+  }
   const double mean = s * (1.0 / D);  // (exact for power-of-two D, ~1 ulp otherwise)
   return mean < INFINITY ? mean : __longlong_as_double(0x7ff0000000000000LL);  // NaN -> inf
 }
@@ -673,6 +695,18 @@ __device__ __forceinline__ double initial_step(const F& f, double t0, const doub
   return bad ? __longlong_as_double(0x7ff8000000000000LL) : dt;
 }
 
+// True when the last stage's input IS the solution: a[S-1][j] == b[j] for
+// every j and b[S-1] == 0 (dopri5 and tsit5, the FSAL property).  The
+// stage-(S-1) input and y_next are then the same sum of the same terms in
+// the same order (zero terms skipped alike), i.e. bitwise equal, so y_next
+// is taken from the stage instead of being summed a second time.
+template <class T>
+__device__ __forceinline__ constexpr bool last_stage_is_solution() {
+  for (int j = 0; j < T::S - 1; j++)
+    if (T::za(T::S - 1, j) != T::zb(j)) return false;
+  return T::zb(T::S - 1) == 0.0;
+}
+
 // Stepper.step, stepper.py:54-110 (one instance).  k[0] must hold f0 for
 // FSAL tableaus; on return k[0..S-1] are the stage derivatives.
 template <class T, class F, class O>
@@ -686,6 +720,7 @@ __device__ __forceinline__ void rk_step(const F& f, double t, double h, const do
   // term, hence every later stage and err, non-finite.)  The only
   // representable difference left is the sign of an exactly-zero sum.
   constexpr int D = F::D, S = T::S;
+  constexpr bool kLast = last_stage_is_solution<T>();
   if constexpr (!T::FSAL) f(t, y, k[0]);
 #pragma unroll
   for (int i = 1; i < S; i++) {
@@ -697,6 +732,7 @@ __device__ __forceinline__ void rk_step(const F& f, double t, double h, const do
       for (int j = 1; j < i; j++)
         if (T::za(i, j) != 0.0) s = O::mad(T::a(i, j), k[j][c], s);
       ys[c] = O::mad(h, s, y[c]);
+      if (kLast && i == S - 1) y_next[c] = ys[c];
     }
     f(O::mad(T::c(i), h, t), ys, k[i]);
   }
@@ -707,7 +743,7 @@ __device__ __forceinline__ void rk_step(const F& f, double t, double h, const do
     bool skipped_nonfinite = false;
 #pragma unroll
     for (int i = 1; i < S; i++) {
-      if (T::zb(i) != 0.0) s = O::mad(T::b(i), k[i][c], s);
+      if (!kLast && T::zb(i) != 0.0) s = O::mad(T::b(i), k[i][c], s);
       if (T::ze(i) != 0.0) e = O::mad(T::e(i), k[i][c], e);
       // (exact mode only: in fast mode a non-finite stage already makes err
       // non-finite through the following stages, so the step is rejected and
@@ -715,7 +751,7 @@ __device__ __forceinline__ void rk_step(const F& f, double t, double h, const do
       if (!O::kFast && (T::zb(i) == 0.0 || T::ze(i) == 0.0))
         skipped_nonfinite |= !isfinite(k[i][c]);
     }
-    y_next[c] = O::mad(h, s, y[c]);
+    if constexpr (!kLast) y_next[c] = O::mad(h, s, y[c]);
     err[c] = O::mul(h, e);
     if (skipped_nonfinite) {
       y_next[c] = __longlong_as_double(0x7ff8000000000000LL);

@@ -249,7 +249,9 @@ __global__ void __launch_bounds__(128) mlp_control_kernel(MlpWs W, CtrlArgs A, i
   int64_t cursor = A.n_emitted[i];
   int status = BODE_RUNNING;
   double t_new = y_t;
-  if (acc_i && A.traj) {  // record (t_old, h, cursor, y_old) for the adjoint
+  if (acc_i && A.traj && nacc_before < A.traj_offsets[i + 1] - A.traj_offsets[i]) {
+    // record (t_old, h, cursor, y_old) for the adjoint (rows bounded: they
+    // were sized by an identical solve)
     const int W = BODE_TRAJ_STRIDE(D);
     double* rec = A.traj + (A.traj_offsets[i] + nacc_before) * W;
     if (lane == 0) {

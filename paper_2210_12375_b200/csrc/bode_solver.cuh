@@ -78,6 +78,12 @@ struct Workspace {
   }
 };
 
+// a recording lane's trajectory rows (shared memory, set at refill)
+struct TrajRows {
+  double* base;
+  double* end;
+};
+
 // per-lane output bases (t_eval row, ys row) kept in shared memory from
 // the refill on, so a lane emitting a point does not stall its warp on a
 // dependent offsets load
@@ -194,13 +200,13 @@ struct Lane {
   // true when the row just rejected and is still running (FSAL refresh at
   // the next iteration, solver.py:220-226)
   // trec (recording only): shared-memory slot holding this lane's
-  // trajectory row base, set at resume -- no per-step global load
+  // trajectory rows [base, end), set at resume -- no per-step global load
   // PI (fast mode only): the launch was specialised for an I / PI
   // controller (CtrlParams::plain_pi), so the general controller is not
   // compiled into the loop
   template <bool PI>
   __device__ __forceinline__ bool step(const SolveParams& P, const PowTables& PT, bool tracing,
-                                       double* const* trec, const EmitBase& eb) {
+                                       const TrajRows* trec, const EmitBase& eb) {
     const int32_t j = nsteps;
     const double remaining = O::sub(t_end, t);
     const bool trunc = fabs(dt) >= fabs(remaining);
@@ -228,11 +234,13 @@ struct Lane {
         double rec[kTrajStride<D>] = {t, h, (double)cursor};
 #pragma unroll
         for (int c = 0; c < D; c++) rec[kTrajExtra + c] = y[c];
-        double* r = *trec + (int64_t)nacc * kTrajStride<D>;
+        double* r = trec->base + (int64_t)nacc * kTrajStride<D>;
+        if (r < trec->end) {  // (the rows were sized by an identical solve)
 #pragma unroll
-        for (int q = 0; q < kTrajStride<D>; q += 4)
-          asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(r + q), "d"(rec[q]),
-                       "d"(rec[q + 1]), "d"(rec[q + 2]), "d"(rec[q + 3]) : "memory");
+          for (int q = 0; q < kTrajStride<D>; q += 4)
+            asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(r + q), "d"(rec[q]),
+                         "d"(rec[q + 1]), "d"(rec[q + 2]), "d"(rec[q + 3]) : "memory");
+        }
       }
       nacc++;
       const double t_old = t;
@@ -314,8 +322,8 @@ __global__ void __launch_bounds__(128, (F::D <= 2 && !REC ? BODE_BLOCKS_2D : 4))
 
   Lane<M, F, O> L;
   const bool tracing = P.trace_cap > 0;  // uniform: hoisted out of the step loop
-  __shared__ double* s_trec[REC ? 128 : 1];  // per-lane trajectory row base
-  double* const* trec = REC ? &s_trec[threadIdx.x] : nullptr;
+  __shared__ TrajRows s_trec[REC ? 128 : 1];  // per-lane trajectory rows
+  const TrajRows* trec = REC ? &s_trec[threadIdx.x] : nullptr;
   __shared__ EmitBase s_eb[128];
   bool have = false, done = false;
   unsigned long long my_max = 0;
@@ -340,7 +348,9 @@ __global__ void __launch_bounds__(128, (F::D <= 2 && !REC ? BODE_BLOCKS_2D : 4))
           L.resume(P, i);
           s_eb[threadIdx.x] = EmitBase{L.te_of(P), L.ys_of(P)};
           if (st == BODE_RUNNING) {
-            if constexpr (REC) s_trec[threadIdx.x] = P.traj + P.traj_offsets[i] * kTrajStride<F::D>;
+            if constexpr (REC)
+              s_trec[threadIdx.x] = TrajRows{P.traj + P.traj_offsets[i] * kTrajStride<F::D>,
+                                             P.traj + P.traj_offsets[i + 1] * kTrajStride<F::D>};
             have = true;
           }
         }

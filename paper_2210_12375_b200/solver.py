@@ -528,7 +528,10 @@ def solve_device(y0, t_start, t_end, f, *, t_eval=None, t_eval_offsets=None, met
         traj = torch.empty((max(rows, 1), _abi.traj_stride(d)), **f64)
         keep += [toff, traj]
         a.traj, a.traj_offsets = traj.data_ptr(), toff.data_ptr()
+        n_acc0 = out["n_accepted"].clone()
         _abi.check(lib.bode_solve(_abi.C.byref(a)))
+        if not torch.equal(n_acc0, out["n_accepted"]):  # (the rows are bounded in-kernel)
+            raise _abi.BodeLibraryError("the recording solve diverged from the sizing solve")
         out["traj"], out["traj_offsets"] = traj[:rows], toff
         out["_args"], out["_keep"] = a, keep
     # keep inputs alive until the stream has consumed them
