@@ -219,8 +219,7 @@ typedef struct bode_solve_args {
    * sectors, so the scattered per-instance row writes never partially fill
    * one).  traj_offsets (n+1) is the exclusive prefix sum of n_accepted
    * from an earlier identical solve (the solve is deterministic).  Not with
-   * joint.  MLP dynamics record through the lockstep tensor-core path
-   * (bit-identical to the fused kernel). */
+   * joint. */
   double* traj;
   const int64_t* traj_offsets;
 } bode_solve_args;

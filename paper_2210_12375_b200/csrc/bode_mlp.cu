@@ -537,10 +537,7 @@ static cudaError_t mlp_solve_m(const bode_solve_args* a, const SolveParams& P, c
   if (a->mlp_backend == BODE_MLP_TCGEN05 && !tc_ok) return cudaErrorNotSupported;
   if (a->mlp_backend == BODE_MLP_FUSED && !fused_ok) return cudaErrorNotSupported;
   const bool use_tc = tc_ok && a->mlp_backend != BODE_MLP_CUDA_CORE;
-  // a recording pass (gradients) runs the lockstep tensor-core path, which is
-  // bit-identical to the fused kernel (tests/test_gpu_solver.py), so the
-  // trajectory is that of the solve being differentiated
-  const bool use_fused = fused_ok && !a->traj &&
+  const bool use_fused = fused_ok &&
                          (a->mlp_backend == BODE_MLP_AUTO || a->mlp_backend == BODE_MLP_FUSED);
   if (use_tc && (e = mlp_tc_prep(W1, W2, H, W.wprep, st)) != cudaSuccess) return e;
   int64_t nl = use_tc ? 1 : 0;  // kernels launched
@@ -625,6 +622,8 @@ static cudaError_t mlp_solve_m(const bode_solve_args* a, const SolveParams& P, c
     F.max_n = P.max_n;
     F.refresh = P.refresh;
     F.prof = nullptr;
+    F.traj = a->traj;
+    F.traj_offsets = a->traj_offsets;
 #ifdef BODE_FUSED_PROF
     static unsigned long long* prof_buf = nullptr;
     if (!prof_buf) cudaMalloc(&prof_buf, 148 * 3 * 32 * 8);

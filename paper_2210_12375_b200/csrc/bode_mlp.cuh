@@ -61,6 +61,8 @@ struct MlpFusedArgs {
   unsigned long long* max_n;
   uint32_t* refresh;
   unsigned long long* prof;      // debug builds (-DBODE_FUSED_PROF): (grid*3, 32) cycles
+  double* traj;                  // optional accepted-step trajectory (gradients),
+  const int64_t* traj_offsets;   // SolveParams::traj layout
 };
 bool mlp_fused_supported(int64_t D, int64_t H, int method);
 template <int M>

@@ -555,6 +555,7 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_fused_kernel(const MlpFusedAr
       bool accept = false;
       double dtn = h;
       if (have) accept = adapt(A.ctrl, nrm, n1, n2, dtn);
+      const int64_t cursor_before = cursor;
       // dense output for every crossed point (solver.py:284-322), pre-commit state
       bool pend = have && accept && cursor < m && h != 0.0;
       while (__any_sync(0xffffffffu, pend)) {
@@ -595,6 +596,22 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_fused_kernel(const MlpFusedAr
         if (pend) {
           cursor++;
           pend = cursor < m;
+        }
+      }
+      // gradients: record (t_old, h, cursor before the step, y_old) of an
+      // accepted step; each row group writes its 32 columns, group 0 the
+      // scalars (rows bounded: they were sized by an identical solve)
+      if (A.traj && have && accept) {
+        const int64_t r0 = A.traj_offsets[idx];
+        if (nacc < A.traj_offsets[idx + 1] - r0) {
+          double* rec = A.traj + (r0 + nacc) * BODE_TRAJ_STRIDE(kD);
+          if (wg == 0) {
+            rec[0] = t;
+            rec[1] = h;
+            rec[2] = (double)cursor_before;
+          }
+#pragma unroll 8
+          for (int c = 32 * wg; c < 32 * wg + 32; c++) rec[BODE_TRAJ_EXTRA + c] = sm.ys[c][row];
         }
       }
       // commit: y <- y_next, FSAL k_0 <- k_{S-1} on accepted rows (my columns)
