@@ -302,13 +302,15 @@ static __device__ unsigned g_exit_count;
 
 // 2-D systems fit 5 blocks of 128 threads per SM (<= 102 registers); wider
 // ones keep 4 (<= 128 registers) to avoid spilling the stage vectors.  The
-// trajectory-recording instantiation (REC, gradients only) follows the same
-// rule (its row bases live in shared memory, so it fits without spills).
+// trajectory-recording instantiation (REC, gradients only) fits 5 blocks
+// without spills only in the fast-mode I / PI specialisation; the general
+// controller (exact mode, PID betas) spills at 96 registers, so those REC
+// instantiations keep 4 blocks.
 #ifndef BODE_BLOCKS_2D
 #define BODE_BLOCKS_2D 5
 #endif
 template <int M, class F, class O, bool REC, bool PI>
-__global__ void __launch_bounds__(128, (F::D <= 2 ? BODE_BLOCKS_2D : 4)) bode_persistent_kernel(const SolveParams P) {
+__global__ void __launch_bounds__(128, ((F::D <= 2 && (!REC || PI)) ? BODE_BLOCKS_2D : 4)) bode_persistent_kernel(const SolveParams P) {
   extern __shared__ uint32_t s_refresh[];
   __shared__ PowTables s_pow;  // pow tables: divergent lookups, so shared not constant
   const int lane = threadIdx.x & 31;

@@ -522,18 +522,22 @@ def solve_device(y0, t_start, t_end, f, *, t_eval=None, t_eval_offsets=None, met
     a.launch_count_out = _abi.C.addressof(nlaunch)
     _abi.check(lib.bode_solve(_abi.C.byref(a)))
     if record_trajectory:
-        toff = torch.zeros(n + 1, dtype=torch.int64, device=dev)
-        torch.cumsum(out["n_accepted"], 0, out=toff[1:])
-        rows = int(toff[-1])
-        traj = torch.empty((max(rows, 1), _abi.traj_stride(d)), **f64)
-        keep += [toff, traj]
-        a.traj, a.traj_offsets = traj.data_ptr(), toff.data_ptr()
-        n_acc0 = out["n_accepted"].clone()
-        _abi.check(lib.bode_solve(_abi.C.byref(a)))
-        if not torch.equal(n_acc0, out["n_accepted"]):  # (the rows are bounded in-kernel)
-            raise _abi.BodeLibraryError("the recording solve diverged from the sizing solve")
+        # the sizing reads (cumsum, row count, divergence check) run on the
+        # solve's own stream, so they see the sizing solve's n_accepted even
+        # when the caller passed a non-current `stream`
+        with torch.cuda.stream(st):
+            toff = torch.zeros(n + 1, dtype=torch.int64, device=dev)
+            torch.cumsum(out["n_accepted"], 0, out=toff[1:])
+            rows = int(toff[-1])
+            traj = torch.empty((max(rows, 1), _abi.traj_stride(d)), **f64)
+            keep += [toff, traj]
+            a.traj, a.traj_offsets = traj.data_ptr(), toff.data_ptr()
+            n_acc0 = out["n_accepted"].clone()
+            _abi.check(lib.bode_solve(_abi.C.byref(a)))
+            if not torch.equal(n_acc0, out["n_accepted"]):  # (the rows are bounded in-kernel)
+                raise _abi.BodeLibraryError("the recording solve diverged from the sizing solve")
         out["traj"], out["traj_offsets"] = traj[:rows], toff
-        out["_args"], out["_keep"] = a, keep
+        out["_args"], out["_keep"], out["_stream"] = a, keep, st
     # keep inputs alive until the stream has consumed them
     for t in keep:
         if isinstance(t, torch.Tensor):
@@ -592,8 +596,12 @@ def adjoint_device(fwd: dict, grad_ys):
     g.workspace, g.workspace_bytes = ws.data_ptr(), wsb
     nlaunch = _abi.C.c_int64(0)
     g.launch_count_out = _abi.C.addressof(nlaunch)
-    _abi.check(lib.bode_solve_adjoint(_abi.C.byref(a), _abi.C.byref(g)))
+    # the adjoint runs on the caller's current stream (where grad_y0 and the
+    # weight gradients were allocated), after the forward's stream
     st = torch.cuda.current_stream(dev)
+    st.wait_stream(fwd["_stream"])
+    a.stream = st.cuda_stream
+    _abi.check(lib.bode_solve_adjoint(_abi.C.byref(a), _abi.C.byref(g)))
     for t in keep:
         t.record_stream(st)
     fwd["adjoint_launches"] = int(nlaunch.value)

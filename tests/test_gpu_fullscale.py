@@ -1,0 +1,115 @@
+"""Full-scale parity of the bench's headline mode (fast) against the pinned
+oracle, at the sizes BASELINE.json quotes:
+
+* C5 stiff VdP, 2^20 instances, mu log-U[1,1000], dopri5 PI42, 1e-6
+  (heavy-tailed step counts, up to ~9,000 per instance);
+* C3 Lorenz-63, 2^18 instances, tsit5, 1e-8, 1000 shared t_eval points
+  (the dense-output path, 2.6e8 interpolated points);
+* C4 neural ODE, 65,536 instances, D=64 / H=256 tanh, dopri5 integral
+  controller, 1e-6, on the fused tcgen05 kernel.
+
+Bars (north_star; reference controller.py:200-238, solver.py:208-322):
+fp64 analytic configs -- every status, n_steps, n_accepted, n_emitted
+identical per instance, batch-global n_f_evals identical, ys within 1e-10
+of each instance's max |y| (1e-9 for the chaotic C3 flow, whose ulp-level
+controller differences are amplified by ~e^(0.9*10) over the horizon).
+C4 (fp32/3xTF32 dynamics vs the oracle's fp32 MLP with a different
+summation order) -- statuses identical, aggregate sum n_steps within 2%,
+y(T) within 1e-4 of each instance's scale.
+
+The inputs are bench.py's own configs (the same seeded arrays the bench
+times), so these tests pin exactly the numbers the bench reports.
+"""
+import os
+
+import numpy as np
+import pytest
+
+import bench
+import oracle as O
+import paper_2210_12375_b200 as bode
+
+pytestmark = [pytest.mark.gpu, pytest.mark.slow]
+NT = os.cpu_count() or 1
+
+
+def _solve_both(name, te=None):
+    cfg = bench.make_config(name, 0)
+    n = cfg["n"]
+    te = cfg.get("te1d", cfg.get("te2d")) if te is None else te
+    if cfg["dyn"] == "vdp":
+        dyn = bode.vdp_dynamics(bode.VdpParams(cfg["mu"]))
+        odyn = dict(name="vdp", inst=cfg["mu"][:, None])
+    elif cfg["dyn"] == "lorenz":
+        dyn = bode.lorenz_dynamics()
+        odyn = dict(name="lorenz", inst=None, shared=(10.0, 28.0, 8.0 / 3.0))
+    else:
+        dyn = bode.mlp_dynamics(*cfg["mlp"])
+        odyn = dict(name="mlp", inst=None, shared=(), mlp=cfg["mlp"])
+    tab = {"dopri5": bode.dopri5, "tsit5": bode.tsit5}[cfg["method"]]()
+    sol = bode.solve(bode.IvpBatch(cfg["y0"], cfg["t_start"], cfg["t_end"],
+                                   te if te is not None else [np.empty(0)] * n),
+                     dyn, tableau=tab, tol=bode.Tolerances(cfg["tol"], cfg["tol"]),
+                     controller=bode.PidCoefficients(*cfg["ctrl"]["betas"]),
+                     max_steps=cfg["max_steps"], mode="fast", cost_hint=cfg["cost"])
+    ote = te if (te is None or te.ndim == 1) else [te[i] for i in range(n)]
+    ref = O.solve(cfg["y0"], cfg["t_start"], cfg["t_end"], ote, odyn, method=cfg["method"],
+                  atol=cfg["tol"], rtol=cfg["tol"], ctrl=cfg["ctrl"],
+                  max_steps=cfg["max_steps"], nthreads=NT)
+    return cfg, sol, ref
+
+
+def _scaled_ys_err(sol, ref, n):
+    a, b = sol.ys_flat.reshape(n, -1), ref["ys"].reshape(n, -1)
+    scale = np.maximum(np.abs(b).max(axis=1), 1e-300)
+    return float(np.max(np.abs(a - b).max(axis=1) / scale))
+
+
+def _exact_counts(sol, ref):
+    assert np.array_equal(sol.status, ref["status"]), "status"
+    ds = int(np.sum(sol.stats.n_steps != ref["n_steps"]))
+    da = int(np.sum(sol.stats.n_accepted != ref["n_accepted"]))
+    assert ds == 0 and da == 0, f"instances with different n_steps {ds}, n_accepted {da}"
+    assert np.array_equal(sol.n_emitted, ref["n_emitted"]), "n_emitted"
+    assert sol.stats.n_f_evals[0] == ref["n_f_evals"][0], "n_f_evals"
+
+
+def test_c5_stiff_full_scale_fast_mode():
+    # the bench times C5 without output points (the metric is steps); the
+    # final state y(10) is requested here so it can be compared -- an output
+    # point changes no step decision
+    cfg, sol, ref = _solve_both("c5", te=np.full((2 ** 20, 1), 10.0))
+    assert cfg["n"] == 2 ** 20
+    _exact_counts(sol, ref)
+    err = _scaled_ys_err(sol, ref, cfg["n"])
+    assert err <= 1e-10, err
+    # final_dt is the controller's proposal after the last step; on stiff
+    # rows the step-size sequence amplifies ulp-level controller
+    # differences (test_gpu_parity.py DT_TOL), so it is reported, not gated
+    rel = np.abs(sol.stats.final_dt - ref["final_dt"]) / np.abs(ref["final_dt"])
+    print(f"C5 2^20 fast: accepted {int(sol.stats.n_accepted.sum())}, "
+          f"max n_steps {int(sol.stats.n_steps.max())}, n_f_evals {sol.stats.n_f_evals[0]}, "
+          f"scaled y(10) err {err:.2e}, final_dt rel diff max {rel.max():.2e} "
+          f"(>1e-5 on {int(np.sum(rel > 1e-5))} rows)")
+
+
+def test_c3_lorenz_full_scale_fast_mode():
+    cfg, sol, ref = _solve_both("c3")
+    assert cfg["n"] == 2 ** 18 and cfg["te1d"].size == 1000
+    _exact_counts(sol, ref)
+    err = _scaled_ys_err(sol, ref, cfg["n"])
+    assert err <= 1e-9, err
+    print(f"C3 2^18 x 1000 points fast: scaled ys err {err:.2e}")
+
+
+def test_c4_mlp_full_scale_fused():
+    cfg, sol, ref = _solve_both("c4")
+    assert cfg["n"] == 65536
+    assert np.array_equal(sol.status, ref["status"]), "status"
+    ratio = sol.stats.n_steps.sum() / ref["n_steps"].sum()
+    assert abs(ratio - 1.0) < 0.02, ratio
+    err = _scaled_ys_err(sol, ref, cfg["n"])
+    assert err < 1e-4, err
+    same = float(np.mean(sol.stats.n_steps == ref["n_steps"]))
+    print(f"C4 64K fused: sum n_steps ratio {ratio:.5f}, per-instance identical {same:.1%}, "
+          f"scaled y(T) err {err:.2e}")
