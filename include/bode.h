@@ -309,6 +309,18 @@ int bode_initial_step(const bode_dynamics* dyn, int64_t n, int64_t d,
                       double rtol, const double* direction, double* dt,
                       double* f0, void* stream);
 
+/* Multi-GPU shard plan (the reference has one process and
+ * no partition -- a shard is bitwise equal to its rows of the full batch,
+ * tests/test_solver.py:140-168).  With cost (device, n): instances dealt to
+ * `world` shards in decreasing cost in a snake pattern over the longest-first
+ * order; perm (device, n) = shard 0's instance indices, then shard 1's, ...,
+ * each shard longest-first (its queue order).  cost == NULL: contiguous
+ * blocks, perm = identity.  shard_sizes (HOST, world) is filled before the
+ * call returns (it depends on n and world only).  Asynchronous on stream. */
+size_t bode_partition_workspace_size(int64_t n);
+int bode_partition(const double* cost, int64_t n, int32_t world, int64_t* perm,
+                   int64_t* shard_sizes, void* ws, size_t ws_bytes, void* stream);
+
 /* Measurement utility (not on the solve path): launches blocks x 256
  * threads each running 8 independent chains of `iters` DFMAs, so a timed
  * launch gives the FP64 roofline denominator (2 flops per DFMA). */

@@ -13,6 +13,7 @@
 // results never depend on the order, only the schedule does.
 #include <cuda_runtime.h>
 
+#include "../../include/bode.h"
 #include "bode_sched.cuh"
 
 namespace bode {
@@ -99,4 +100,65 @@ cudaError_t lpt_order(const double* cost, int64_t n, void* ws, int64_t** order_o
   return cudaGetLastError();
 }
 
+
+// ------------------------------------------------------------ partition --
+// Multi-GPU shard plan: instances dealt to `world` shards
+// in decreasing cost in a snake pattern over the longest-first order
+// (positions p = j*W + k go to shard k on even laps j, W-1-k on odd ones),
+// which keeps per-shard cost sums within one instance's cost of each other.
+// perm = shard 0's instances, then shard 1's, ...; inside a shard they stay
+// longest-first, so a shard's own queue order is its row order.
+namespace {
+// first position of shard r (snake sizes: laps, plus one for the shards the
+// last, partial lap reaches -- the first rem on an even lap, the last rem on
+// an odd one)
+__device__ __forceinline__ int64_t shard_off(int64_t r, int64_t laps, int64_t rem, int64_t w) {
+  const int64_t ex = (laps & 1) ? (r > w - rem ? r - (w - rem) : 0) : (r < rem ? r : rem);
+  return r * laps + ex;
+}
+
+__global__ void shard_perm_kernel(const int64_t* order, int64_t n, int32_t world, int64_t* perm) {
+  const int64_t laps = n / world, rem = n % world;
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n;
+       q += (int64_t)gridDim.x * blockDim.x) {
+    int64_t r = 0;
+    while (r + 1 < world && q >= shard_off(r + 1, laps, rem, world)) r++;
+    const int64_t j = q - shard_off(r, laps, rem, world);
+    perm[q] = order ? order[j * world + ((j & 1) ? world - 1 - r : r)] : q;
+  }
+}
+}  // namespace
+
+void compute_shard_sizes(int64_t n, int32_t world, bool snake, int64_t* sizes) {
+  const int64_t laps = n / world, rem = n % world;
+  for (int r = 0; r < world; r++) {
+    if (!snake) {
+      sizes[r] = n * (r + 1) / world - n * r / world;
+    } else {
+      const bool extra = (laps & 1) ? (r >= world - rem) : (r < rem);
+      sizes[r] = laps + (extra ? 1 : 0);
+    }
+  }
+}
+
 }  // namespace bode
+
+extern "C" size_t bode_partition_workspace_size(int64_t n) {
+  return n < 1 ? 0 : bode::lpt_workspace_bytes(n);
+}
+
+extern "C" int bode_partition(const double* cost, int64_t n, int32_t world, int64_t* perm,
+                              int64_t* shard_sizes, void* ws, size_t ws_bytes, void* stream) {
+  using namespace bode;
+  if (n < 1 || world < 1 || world > 4096 || !perm || !shard_sizes) return BODE_EINVAL;
+  cudaStream_t st = (cudaStream_t)stream;
+  compute_shard_sizes(n, world, cost != nullptr, shard_sizes);
+  int64_t* order = nullptr;
+  if (cost) {
+    if (!ws || ws_bytes < bode_partition_workspace_size(n)) return BODE_EINVAL;
+    if (lpt_order(cost, n, ws, &order, st) != cudaSuccess) return BODE_ECUDA;
+  }
+  const int64_t nb = (n + 255) / 256;
+  shard_perm_kernel<<<(unsigned)(nb < 148 * 8 ? nb : 148 * 8), 256, 0, st>>>(order, n, world, perm);
+  return cudaGetLastError() == cudaSuccess ? BODE_OK : BODE_ECUDA;
+}
