@@ -271,7 +271,11 @@ def run_bode(args, rank, world, local_rank):
         else:
             dist.init_process_group("nccl", device_id=dev)
     lib = _abi.load()
-    cfg = make_config(args.config, rank)
+    # strong scaling (default for N > 1): every rank holds the same seeded
+    # batch and solves its cost-balanced shard of it; weak: rank r solves its
+    # own full-size batch (seed 1000 + r)
+    strong = world > 1 and args.scaling == "strong"
+    cfg = make_config(args.config, 0 if strong else rank)
     cfg["_name"] = args.config
     n, d = cfg["n"], cfg["d"]
     f64 = dict(dtype=torch.float64, device=dev)
@@ -296,6 +300,20 @@ def run_bode(args, rank, world, local_rank):
     from paper_2210_12375_b200 import distributed as bdist
 
     def one_step(prof=None):
+        if strong:
+            # the whole sharded job: device shard plan (cost-aware), shard
+            # row gathers, persistent solve of the shard, the n_f_evals
+            # all-reduce and the NCCL gather of every instance's results to
+            # rank 0 in batch order (distributed.solve_sharded_device)
+            out = bdist.solve_sharded_device(
+                y0, ts, tn, dyn, method=cfg["method"], atol=cfg["tol"], rtol=cfg["tol"],
+                controller=ctrl, max_steps=cfg["max_steps"], mode=args.mode,
+                cost_hint=torch.tensor(cfg["cost"], **f64) if cfg["cost"] is not None else None,
+                prof_events=prof, gather_to=0, **te_kw)
+            if out is None:  # ranks other than 0 hold no results after the gather
+                z = torch.zeros(1, dtype=torch.int64, device=dev)
+                out = dict(n_accepted=z, n_steps=z, launches=0)
+            return out
         out = bode.solve_device(y0, ts, tn, dyn, method=cfg["method"], atol=cfg["tol"],
                                 rtol=cfg["tol"], controller=ctrl, max_steps=cfg["max_steps"],
                                 mode=args.mode, cost_hint=cost, prof_events=prof,
@@ -332,6 +350,7 @@ def run_bode(args, rank, world, local_rank):
             # which synchronise, inside later timed steps)
             pend.append((e0, e1, k0, k1, out["n_accepted"].sum(), out["n_steps"].sum(),
                          out["launches"]))
+
             del out
         return pend
 
@@ -368,6 +387,7 @@ def run_bode(args, rank, world, local_rank):
     # steps above (bode_solve records them around the persistent launch)
     pts = n_points(cfg)
     kern_ms = float(np.mean(kern_times))
+    # attempted steps per persistent launch (one launch per rank per step)
     att_launch = attempted / args.steps / max(world, 1)
     traffic = None
     try:
@@ -426,7 +446,12 @@ def run_bode(args, rank, world, local_rank):
         kw = dict(tableau=tab, tol=bode.Tolerances(cfg["tol"], cfg["tol"]), controller=ctrl,
                   max_steps=cfg["max_steps"], mode=args.mode,
                   cost_hint=P(cfg["cost"]) if (args.lpt and cfg["cost"] is not None) else None)
-        bode.solve(prob, dyn_h, **kw)
+        def e2e_solve():
+            if strong:  # host arrays in, the full Solution on rank 0
+                return bdist.solve_sharded(prob, dyn_h, **kw)
+            return bode.solve(prob, dyn_h, **kw)
+
+        e2e_solve()
         if dist:
             dist.barrier()
         e2e_t, e2e_acc = [], 0
@@ -434,9 +459,9 @@ def run_bode(args, rank, world, local_rank):
             flush.zero_()
             torch.cuda.synchronize(dev)
             t0 = time.perf_counter()
-            sol = bode.solve(prob, dyn_h, **kw)
+            sol = e2e_solve()
             e2e_t.append(time.perf_counter() - t0)
-            e2e_acc += int(sol.stats.n_accepted.sum())
+            e2e_acc += int(sol.stats.n_accepted.sum()) if sol is not None else 0
             del sol  # result consumed: its page-locked buffers return to the host cache
         tot = float(np.sum(e2e_t))
         if dist:
@@ -471,17 +496,24 @@ def run_bode(args, rank, world, local_rank):
         line = dict(
             metric="accepted instance-steps/sec", value=value, unit="instance-steps/s",
             n_gpus=world, steps=args.steps, warmup=args.warmup,
-            ms_per_step=total_ms / args.steps, higher_is_better=True, scaling="weak",
+            ms_per_step=total_ms / args.steps, higher_is_better=True,
+            scaling="strong" if strong else "weak",
             vs_baseline=None, dtype="f64", data="synthetic",
-            config=dict(workload=cfg["workload"], instances_per_gpu=n,
-                        global_instances=n * world, method=cfg["method"],
+            config=dict(workload=cfg["workload"],
+                        instances_per_gpu=n if not strong else n / world,
+                        global_instances=n if strong else n * world, method=cfg["method"],
                         controller="PI42" if cfg["ctrl"] is PI42 else "I",
                         tol=cfg["tol"],
                         # the MLP path has one arithmetic mode: the reference's
                         # operation order in its fp64 control (bode_mlp*.cu)
                         mode=args.mode if cfg["dyn"] != "mlp" else "exact (MLP control)",
                         lpt_order=bool(args.lpt),
-                        parallelism=f"shard{world}", l2="flushed (256 MiB write) between steps",
+                        parallelism=(f"shard{world}: one {n}-instance batch, cost-balanced "
+                                     "device partition, NCCL gather of all results to rank 0 "
+                                     "inside every step") if strong else
+                                    (f"shard{world}: independent {n}-instance batch per GPU"
+                                     if world > 1 else "shard1"),
+                        l2="flushed (256 MiB write) between steps",
                         accepted_per_step=accepted / args.steps,
                         attempted_per_step=attempted / args.steps),
             roofline=roof,
@@ -509,7 +541,12 @@ def main():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--gather", action="store_true",
-                   help="N>1: also gather every shard's ys/stats to rank 0 inside the timed step")
+                   help="N>1 weak scaling: also gather every shard's ys/stats to rank 0 "
+                        "inside the timed step")
+    p.add_argument("--scaling", default="strong", choices=["strong", "weak"],
+                   help="N>1: strong = shard ONE batch over the ranks (cost-aware device "
+                        "partition, NCCL gather to rank 0 in every step); weak = an "
+                        "independent full batch per rank")
     args = p.parse_args()
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))

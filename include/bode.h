@@ -316,7 +316,10 @@ int bode_initial_step(const bode_dynamics* dyn, int64_t n, int64_t d,
  * order; perm (device, n) = shard 0's instance indices, then shard 1's, ...,
  * each shard longest-first (its queue order).  cost == NULL: contiguous
  * blocks, perm = identity.  shard_sizes (HOST, world) is filled before the
- * call returns (it depends on n and world only).  Asynchronous on stream. */
+ * call returns (it depends on n and world only).  Asynchronous on stream.
+ * Instances of equal cost bucket are ranked in arrival order, so two calls
+ * may deal them differently: a multi-rank caller computes the plan on one
+ * rank and broadcasts perm (the Python facade does). */
 size_t bode_partition_workspace_size(int64_t n);
 int bode_partition(const double* cost, int64_t n, int32_t world, int64_t* perm,
                    int64_t* shard_sizes, void* ws, size_t ws_bytes, void* stream);

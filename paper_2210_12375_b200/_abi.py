@@ -98,6 +98,8 @@ SIGNATURES = {
     "bode_initial_step": ([_P, _I64, _I64, _P, _P, _I32, _P, _P, _D, _D, _P, _P, _P, _P],
                           C.c_int),
     "bode_probe_fp64": ([_I64, _I32, _P, _P], C.c_int),
+    "bode_partition_workspace_size": ([_I64], _SZ),
+    "bode_partition": ([_P, _I64, _I32, _P, _P, _P, _SZ, _P], C.c_int),
     "bode_probe_tf32": ([_I32, _I32, _P], C.c_int),
 }
 

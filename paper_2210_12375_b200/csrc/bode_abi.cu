@@ -684,3 +684,20 @@ int bode_initial_step(const bode_dynamics* dyn, int64_t n, int64_t d, const doub
 }
 
 }  // extern "C"
+
+// ------------------------------------------------------------ partition --
+extern "C" size_t bode_partition_workspace_size(int64_t n) {
+  return n < 1 ? 0 : lpt_workspace_bytes(n);
+}
+
+extern "C" int bode_partition(const double* cost, int64_t n, int32_t world, int64_t* perm,
+                              int64_t* shard_sizes, void* ws, size_t ws_bytes, void* stream) {
+  if (n < 1) return fail(BODE_EINVAL, "bode_partition: need at least one instance");
+  if (world < 1 || world > 4096) return fail(BODE_EINVAL, "bode_partition: world must be in [1, 4096]");
+  if (!perm || !shard_sizes) return fail(BODE_EINVAL, "bode_partition: null output");
+  if (cost && (!ws || ws_bytes < bode_partition_workspace_size(n)))
+    return fail(BODE_EINVAL, "bode_partition: workspace too small");
+  compute_shard_sizes(n, world, cost != nullptr, shard_sizes);
+  const cudaError_t e = shard_partition(cost, n, world, perm, ws, (cudaStream_t)stream);
+  return e == cudaSuccess ? BODE_OK : cuda_fail(e, "bode_partition");
+}

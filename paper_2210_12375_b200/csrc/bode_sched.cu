@@ -141,24 +141,16 @@ void compute_shard_sizes(int64_t n, int32_t world, bool snake, int64_t* sizes) {
   }
 }
 
-}  // namespace bode
-
-extern "C" size_t bode_partition_workspace_size(int64_t n) {
-  return n < 1 ? 0 : bode::lpt_workspace_bytes(n);
-}
-
-extern "C" int bode_partition(const double* cost, int64_t n, int32_t world, int64_t* perm,
-                              int64_t* shard_sizes, void* ws, size_t ws_bytes, void* stream) {
-  using namespace bode;
-  if (n < 1 || world < 1 || world > 4096 || !perm || !shard_sizes) return BODE_EINVAL;
-  cudaStream_t st = (cudaStream_t)stream;
-  compute_shard_sizes(n, world, cost != nullptr, shard_sizes);
+cudaError_t shard_partition(const double* cost, int64_t n, int32_t world, int64_t* perm,
+                            void* ws, cudaStream_t st) {
   int64_t* order = nullptr;
   if (cost) {
-    if (!ws || ws_bytes < bode_partition_workspace_size(n)) return BODE_EINVAL;
-    if (lpt_order(cost, n, ws, &order, st) != cudaSuccess) return BODE_ECUDA;
+    const cudaError_t e = lpt_order(cost, n, ws, &order, st);
+    if (e != cudaSuccess) return e;
   }
   const int64_t nb = (n + 255) / 256;
   shard_perm_kernel<<<(unsigned)(nb < 148 * 8 ? nb : 148 * 8), 256, 0, st>>>(order, n, world, perm);
-  return cudaGetLastError() == cudaSuccess ? BODE_OK : BODE_ECUDA;
+  return cudaGetLastError();
 }
+
+}  // namespace bode

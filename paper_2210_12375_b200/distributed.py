@@ -25,7 +25,8 @@ import numpy as np
 from .solver import IvpBatch, Solution, SolveStats
 
 __all__ = ["partition", "combine_f_evals", "subset_problem", "solve_sharded",
-           "global_f_evals_device", "gather_device"]
+           "global_f_evals_device", "gather_device", "gather_rows", "shard_plan",
+           "solve_sharded_device"]
 
 
 def partition(n: int, world: int, cost=None) -> list:
@@ -104,26 +105,35 @@ def solve_sharded(problem: IvpBatch, f, *, group=None, cost_hint=None, gather_to
     sol.stats.n_f_evals = np.full(len(idx), nfe, dtype=np.int64)
     if gather_to is None:
         return idx, sol
-    payload = (idx, [np.asarray(y) for y in sol.ys], sol.stats.n_steps, sol.stats.n_accepted,
-               sol.stats.final_dt, sol.status, sol.n_emitted)
-    if world > 1:
-        objs = [None] * world if rank == gather_to else None
-        dist.gather_object(payload, objs, dst=gather_to, group=group)
-    else:
-        objs = [payload]
+    # results travel as tensors (NCCL on the GPU box, gloo on CPU): one
+    # (rows, 6) record per instance and the shard's flat ys rows
+    k, d = len(idx), problem.n_features
+    rec = np.empty((k, 6), np.int64)
+    rec[:, 0] = idx
+    rec[:, 1], rec[:, 2] = sol.stats.n_steps, sol.stats.n_accepted
+    rec[:, 3] = np.asarray(sol.stats.final_dt, np.float64).view(np.int64)
+    rec[:, 4], rec[:, 5] = sol.status, sol.n_emitted
+    flat = np.zeros((0, d)) if k == 0 else np.concatenate(
+        [np.asarray(y, np.float64).reshape(-1, d) for y in sol.ys])
+    recs = gather_rows(torch.from_numpy(rec).to(dev), gather_to, group)
+    ys_all = gather_rows(torch.from_numpy(np.ascontiguousarray(flat)).to(dev), gather_to, group)
     if rank != gather_to:
         return None
-    d = problem.n_features
+    recs = [r.cpu().numpy() for r in recs]
+    ys_all = [y.cpu().numpy() for y in ys_all]
     ys = [None] * n
     n_steps = np.zeros(n, np.int64)
     n_acc = np.zeros(n, np.int64)
     fdt = np.zeros(n)
     status = np.zeros(n, np.int64)
     n_emit = np.zeros(n, np.int64)
-    for ids, y, ns, na, fd, st, ne in objs:
+    for r, y in zip(recs, ys_all):
+        ids = r[:, 0]
+        n_steps[ids], n_acc[ids], status[ids], n_emit[ids] = r[:, 1], r[:, 2], r[:, 4], r[:, 5]
+        fdt[ids] = r[:, 3].view(np.float64)
+        o = np.concatenate([[0], np.cumsum(r[:, 5])])
         for j, i in enumerate(ids):
-            ys[i] = y[j]
-        n_steps[ids], n_acc[ids], fdt[ids], status[ids], n_emit[ids] = ns, na, fd, st, ne
+            ys[i] = y[o[j]:o[j + 1]]
     counts = problem.eval_counts()
     offs = np.zeros(n + 1, np.int64)
     np.cumsum(counts, out=offs[1:])
@@ -133,6 +143,52 @@ def solve_sharded(problem: IvpBatch, f, *, group=None, cost_hint=None, gather_to
     stats = SolveStats(n_steps=n_steps, n_accepted=n_acc,
                        n_f_evals=np.full(n, nfe, dtype=np.int64), final_dt=fdt)
     return Solution(flat, offs, 0, n_emit, stats, status, d)
+
+
+def gather_rows(t, dst: int = 0, group=None):
+    """Gather tensors whose first dimension differs per rank to rank ``dst``
+    (list in rank order there, None elsewhere): row counts are exchanged
+    first, then every rank sends its rows padded to the longest shard."""
+    import torch
+    import torch.distributed as dist
+
+    if not dist.is_initialized() or dist.get_world_size(group) == 1:
+        return [t]
+    world, rank = dist.get_world_size(group), dist.get_rank(group)
+    rows = torch.tensor([t.shape[0]], dtype=torch.int64, device=t.device)
+    sizes = [torch.zeros_like(rows) for _ in range(world)]
+    dist.all_gather(sizes, rows, group=group)
+    sizes = [int(x.item()) for x in sizes]
+    return _gather_padded(t, sizes, dst, group)
+
+
+def _gather_padded(t, sizes, dst, group):
+    import torch
+    import torch.distributed as dist
+
+    rank = dist.get_rank(group)
+    mrow = max(sizes)
+    home = t.device
+    t = _on_backend(t.contiguous(), group)
+    if t.shape[0] != mrow:
+        pad = torch.zeros((mrow,) + tuple(t.shape[1:]), dtype=t.dtype, device=t.device)
+        pad[:t.shape[0]] = t
+        t = pad
+    bufs = [torch.empty_like(t) for _ in sizes] if rank == dst else None
+    dist.gather(t, bufs, dst=dst, group=group)
+    if rank != dst:
+        return None
+    return [b[:s_].to(home) for b, s_ in zip(bufs, sizes)]
+
+
+def _on_backend(t, group):
+    """Collectives run on device tensors under NCCL; a gloo group (the CPU
+    tests, or several ranks sharing one GPU) takes host copies."""
+    import torch.distributed as dist
+
+    if t.is_cuda and dist.get_backend(group) == "gloo":
+        return t.cpu()
+    return t
 
 
 # ------------------------------------------------- device-side (NCCL) path --
@@ -150,8 +206,10 @@ def global_f_evals_device(out, stages: int = 7, fsal: bool = True, group=None):
     mx = out["max_iterations"].clone()
     rmap = out["refresh_map"].clone()
     if dist.is_initialized() and dist.get_world_size(group) > 1:
+        mx, rmap = _on_backend(mx, group), _on_backend(rmap, group)
         dist.all_reduce(mx, op=dist.ReduceOp.MAX, group=group)
         dist.all_reduce(rmap, op=dist.ReduceOp.MAX, group=group)
+        mx, rmap = mx.to(out["max_iterations"].device), rmap.to(out["max_iterations"].device)
     if not fsal:
         return 1 + stages * mx[0]
     it = torch.arange(rmap.numel(), device=rmap.device)
@@ -184,4 +242,116 @@ def gather_device(out, dst: int = 0, group=None, keys=("n_steps", "n_accepted", 
         dist.gather(pad, bufs, dst=dst, group=group)
         if rank == dst:
             res[k] = torch.cat([b[:s_] for b, s_ in zip(bufs, sizes)])
+    return res
+
+
+def shard_plan(n: int, world: int, cost=None, device=None, group=None):
+    """Device shard plan (``bode_partition``): returns (perm, sizes) with
+    perm an (n,) int64 device tensor = shard 0's instance indices, then
+    shard 1's, ... -- with ``cost`` dealt longest-first in a snake pattern
+    (each shard stays longest-first, i.e. in its own queue order), without
+    it contiguous blocks -- and sizes the per-shard counts (host ints, they
+    depend on n and world only).  The longest-first order ranks equal cost
+    buckets in arrival order (shared-memory atomics), so with several
+    ranks, rank 0's plan is broadcast (8 bytes per instance over NVLink)
+    and every rank works from the same permutation.  No host sync."""
+    import torch
+
+    from . import _abi
+
+    lib = _abi.load()
+    perm = torch.empty(n, dtype=torch.int64, device=device)
+    sizes = (_abi.C.c_int64 * world)()
+    st = torch.cuda.current_stream(device)
+    keep = []
+    if cost is not None:
+        c = torch.as_tensor(cost, dtype=torch.float64, device=device).expand(n).contiguous()
+        wsb = lib.bode_partition_workspace_size(n)
+        ws = torch.empty(wsb, dtype=torch.uint8, device=device)
+        keep += [c, ws]
+        rc = lib.bode_partition(c.data_ptr(), n, world, perm.data_ptr(), sizes, ws.data_ptr(),
+                                wsb, st.cuda_stream)
+    else:
+        rc = lib.bode_partition(None, n, world, perm.data_ptr(), sizes, None, 0, st.cuda_stream)
+    _abi.check(rc)
+    for t in keep:
+        t.record_stream(st)
+    import torch.distributed as dist
+    if cost is not None and world > 1 and dist.is_initialized():
+        p = _on_backend(perm, group)
+        dist.broadcast(p, src=dist.get_global_rank(group, 0) if group is not None else 0,
+                       group=group)
+        perm = p.to(perm.device)
+    return perm, [int(v) for v in sizes]
+
+
+def solve_sharded_device(y0, t_start, t_end, f, *, t_eval=None, cost_hint=None, method="dopri5",
+                         atol=1e-6, rtol=1e-6, dt0=None, group=None, gather_to: int | None = 0,
+                         **solve_kw):
+    """One batch solved across the ranks of ``group`` (one GPU each), device
+    tensors in and out, no host sync until the gather.
+
+    Every rank passes the same full batch description (resident on its
+    device).  The batch is partitioned on the device (``shard_plan``:
+    cost-aware when ``cost_hint`` is given), each rank gathers its shard's
+    rows and solves them with the persistent kernel (queue order = the
+    shard's longest-first row order), the batch-global ``n_f_evals`` is
+    combined with two MAX all-reduces, and the per-instance results are
+    gathered to rank ``gather_to`` over NCCL and put back in batch order.
+    Returns the solve_device-style dict for the whole batch on
+    ``gather_to`` (None on the other ranks); ``gather_to=None`` returns each
+    rank's shard dict (with ``idx``) instead.  ``t_eval``: None, a 1-D tensor
+    shared by every instance or an (n, m) tensor."""
+    import torch
+    import torch.distributed as dist
+
+    from .solver import solve_device
+    from .tableau import method_of
+
+    on = dist.is_initialized()
+    world = dist.get_world_size(group) if on else 1
+    rank = dist.get_rank(group) if on else 0
+    dev = y0.device
+    n, d = y0.shape
+    perm, sizes = shard_plan(n, world, cost_hint, dev, group)
+    off = int(np.sum(sizes[:rank]))
+    idx = perm[off:off + sizes[rank]]
+
+    def rows(x):
+        if isinstance(x, torch.Tensor) and x.dim() > 0 and x.shape[0] == n:
+            return x.index_select(0, idx)
+        return x
+
+    te = t_eval if (t_eval is None or t_eval.dim() == 1) else rows(t_eval)
+    sub_f = f.subset(idx) if hasattr(f, "subset") else f
+    m = method_of(method)
+    out = solve_device(rows(y0), rows(torch.as_tensor(t_start, dtype=torch.float64, device=dev)
+                                      .expand(n)),
+                       rows(torch.as_tensor(t_end, dtype=torch.float64, device=dev).expand(n)),
+                       sub_f, t_eval=te, method=m, atol=rows(atol), rtol=rows(rtol),
+                       dt0=rows(dt0), with_refresh_map=world > 1, **solve_kw)
+    stages, fsal = (2, False) if m == "heun" else (7, True)
+    nfe = global_f_evals_device(out, stages=stages, fsal=fsal, group=group) if world > 1 \
+        else out["n_f_evals"][0]
+    if gather_to is None:
+        out["idx"], out["n_f_evals"] = idx, nfe.reshape(1)
+        return out
+    k = sizes[rank]
+    rec = torch.stack([out["n_steps"], out["n_accepted"], out["final_dt"].view(torch.int64),
+                       out["status"], out["n_emitted"]], dim=1)
+    mpts = 0 if t_eval is None else (t_eval.numel() if t_eval.dim() == 1 else t_eval.shape[1])
+    ys = out["ys"].reshape(k, mpts * d) if mpts else None
+    if world > 1:
+        recs = _gather_padded(rec, sizes, gather_to, group)
+        yss = _gather_padded(ys, sizes, gather_to, group) if mpts else None
+        if rank != gather_to:
+            return None
+        rec = torch.cat(recs)
+        ys = torch.cat(yss) if mpts else None
+    full = torch.empty_like(rec).index_copy_(0, perm, rec)
+    res = dict(n_steps=full[:, 0], n_accepted=full[:, 1], final_dt=full[:, 2].view(torch.float64),
+               status=full[:, 3], n_emitted=full[:, 4], n_f_evals=nfe.reshape(1),
+               launches=out["launches"] + (4 if cost_hint is not None else 1))  # + the plan (LPT histogram, scan, scatter; permutation)
+    res["ys"] = (torch.empty_like(ys).index_copy_(0, perm, ys).reshape(n * mpts, d) if mpts
+                 else out["ys"][:0])
     return res
