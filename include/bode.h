@@ -35,14 +35,16 @@
 #ifndef BODE_H_
 #define BODE_H_
 
+#ifndef __CUDACC_RTC__
 #include <stddef.h>
 #include <stdint.h>
+#endif
 
 #ifdef __cplusplus
 extern "C" {
 #endif
 
-#define BODE_ABI_VERSION 4
+#define BODE_ABI_VERSION 5
 
 /* return codes */
 #define BODE_OK 0
@@ -61,6 +63,9 @@ extern "C" {
 #define BODE_METHOD_DOPRI5 0
 #define BODE_METHOD_TSIT5 1
 #define BODE_METHOD_HEUN 2
+/* a user ButcherTableau (tableau.py:17-83): coefficients compiled into a
+ * run-time program (bode_program_create), args->program required */
+#define BODE_METHOD_CUSTOM 3
 
 /* registered dynamics (the reference takes any NumPy callable f(t, y),
  * stepper.py:19-20; a device solver needs them compiled in).  Parameter
@@ -95,6 +100,11 @@ extern "C" {
 #define BODE_DYN_HARMONIC 12
 #define BODE_DYN_DAMPED 13
 #define BODE_DYN_MLP 20
+/* user dynamics compiled into a run-time program (bode_program_create):
+ * the facade translates the reference's NumPy callable f(t, y) into a
+ * device functor; inst_params = (n, desc.n_params) per-instance values it
+ * reads, args->program required */
+#define BODE_DYN_PROGRAM 30
 
 /* arithmetic mode: EXACT = unfused IEEE ops in the reference's operation
  * order; FAST = FMA contraction allowed. */
@@ -222,6 +232,9 @@ typedef struct bode_solve_args {
    * joint. */
   double* traj;
   const int64_t* traj_offsets;
+  /* run-time program (bode_program_create) for a BODE_METHOD_CUSTOM tableau
+   * and/or BODE_DYN_PROGRAM dynamics; NULL for the built-in kernels */
+  const struct bode_program* program;
 } bode_solve_args;
 
 #define BODE_TRAJ_EXTRA 3
@@ -258,6 +271,22 @@ typedef struct bode_adjoint_args {
 #define BODE_MLP_TCGEN05 2
 #define BODE_MLP_FUSED 3
 
+/* A ButcherTableau by value (tableau.py:17-57) for the unit ops of the
+ * stepping API: row-major a (stride BODE_TABLEAU_MAX_STAGES), interp row i
+ * = ascending theta^1..theta^n_interp coefficients (stride
+ * BODE_TABLEAU_MAX_INTERP).  Device memory. */
+#define BODE_TABLEAU_MAX_STAGES 16
+#define BODE_TABLEAU_MAX_INTERP 8
+typedef struct bode_tableau {
+  int32_t stages, n_interp, fsal, _pad;
+  double a[BODE_TABLEAU_MAX_STAGES * BODE_TABLEAU_MAX_STAGES];
+  double b[BODE_TABLEAU_MAX_STAGES];
+  double b_err[BODE_TABLEAU_MAX_STAGES];
+  double c[BODE_TABLEAU_MAX_STAGES];
+  double interp[BODE_TABLEAU_MAX_STAGES * BODE_TABLEAU_MAX_INTERP];
+} bode_tableau;
+
+#ifndef __CUDACC_RTC__ /* entry points: host code only */
 int bode_abi_version(void);
 /* sizeof(bode_solve_args) as compiled, for binding layout checks */
 size_t bode_sizeof_args(void);
@@ -309,6 +338,81 @@ int bode_initial_step(const bode_dynamics* dyn, int64_t n, int64_t d,
                       double rtol, const double* direction, double* dt,
                       double* f0, void* stream);
 
+/* ---- run-time programs: the reference's plugin surface on the device ----
+ * The reference accepts any ButcherTableau (tableau.py:17-83) and any NumPy
+ * callable f(t, y) (stepper.py:19-20).  libbode compiles a solver
+ * specialisation for such a pair at run time (NVRTC, sm_100a): `source`
+ * is CUDA C++ that, inside namespace bode, defines `template <class O>
+ * struct UserDyn` (a functor with D, load(), operator(); or an alias of a
+ * registered one) and, for method == BODE_METHOD_CUSTOM, specialises
+ * TabShape<3> / Tab<3> with the tableau's coefficients.  The library
+ * appends the kernel instantiations the `kernels` mask asks for.  Compile
+ * errors return BODE_EINVAL with the NVRTC log in bode_last_error().
+ * Programs are cached on disk by content ($BODE_JIT_CACHE, default
+ * ~/.cache/bode_jit).  A program is bound to the device current at
+ * creation. */
+#define BODE_PROGRAM_SOLVE 1 /* init pass + persistent kernel (both modes) */
+#define BODE_PROGRAM_STEP 2  /* BatchSolver stepping (bode_step_begin/once) */
+#define BODE_PROGRAM_UNITS 4 /* rk_step / interpolate / initial_step */
+#define BODE_PROGRAM_JOINT 8 /* solve_joint (args->joint) */
+typedef struct bode_program_desc {
+  int32_t method;   /* BODE_METHOD_* (CUSTOM: the source specialises Tab<3>) */
+  int32_t kernels;  /* BODE_PROGRAM_* mask */
+  int64_t d;        /* state width = UserDyn<O>::D */
+  int32_t n_params; /* per-instance parameter columns of BODE_DYN_PROGRAM */
+  /* tableau metadata (CUSTOM only; must match the source) */
+  int32_t stages, order, error_order, fsal;
+  int32_t _pad;
+} bode_program_desc;
+typedef struct bode_program bode_program;
+int bode_program_create(const char* source, const bode_program_desc* desc, bode_program** out);
+/* Compile only (no device needed): BODE_OK if the specialisation builds,
+ * BODE_EINVAL with the NVRTC log otherwise. */
+int bode_program_check(const char* source, const bode_program_desc* desc);
+void bode_program_destroy(bode_program* prog);
+
+
+/* BatchSolver (solver.py:141-349): the stepping API, one launch per loop
+ * iteration, on device state.  args describe the batch exactly as for
+ * bode_solve (program required, BODE_PROGRAM_STEP); its outputs double as
+ * state (final_dt = ControllerState.dt, n_emitted = t_eval cursor,
+ * n_steps, n_accepted, status, ys, trace).  The caller initialises
+ * t = t_start, y = y0, norm_prev = norm_prev2 = 1, fsal_valid = 1,
+ * n_steps = n_accepted = 0. */
+typedef struct bode_step_state {
+  double* t;            /* (n) */
+  double* y;            /* (n, d) */
+  double* f0;           /* (n, d) FSAL cache */
+  double* norm_prev;    /* (n) ControllerState.norm_prev */
+  double* norm_prev2;   /* (n) ControllerState.norm_prev2 */
+  double* te_next;      /* (n) scratch */
+  uint8_t* fsal_valid;  /* (n) */
+  int32_t* flags;       /* (2) device: [0] any instance still running,
+                           [1] an FSAL refresh evaluation happened */
+} bode_step_state;
+/* BatchSolver.__init__ (solver.py:148-206): f0, dt0 / initial_step,
+ * INFINITE_DYNAMICS, points at t_start. */
+int bode_step_begin(const bode_solve_args* args, const bode_step_state* s);
+/* One step_once iteration (solver.py:208-282); flags are zeroed first. */
+int bode_step_once(const bode_solve_args* args, const bode_step_state* s);
+
+/* Unit ops for any tableau / dynamics (Stepper.step, stepper.py:54-110;
+ * Stepper.interpolate, :112-139; initial_step, controller.py:145-197):
+ * the tableau from device memory (bode_tableau), the dynamics from a
+ * program compiled with BODE_PROGRAM_UNITS (its method is not used). */
+int bode_program_rk_step(const bode_program* prog, const bode_tableau* tab,
+                         const bode_dynamics* dyn, int64_t n, int64_t d, const double* t,
+                         const double* dt, const double* y, const double* f0, double* y_next,
+                         double* err, double* k, void* stream);
+int bode_interpolate_tab(const bode_tableau* tab, int64_t n, int64_t d, const double* k,
+                         const double* y0, const double* dt, const double* theta, double* out,
+                         void* stream);
+int bode_program_initial_step(const bode_program* prog, const bode_dynamics* dyn, int64_t n,
+                              int64_t d, const double* t0, const double* y0, int32_t order,
+                              const double* atol_v, const double* rtol_v, double atol,
+                              double rtol, const double* direction, double* dt, double* f0,
+                              void* stream);
+
 /* Multi-GPU shard plan (the reference has one process and
  * no partition -- a shard is bitwise equal to its rows of the full batch,
  * tests/test_solver.py:140-168).  With cost (device, n): instances dealt to
@@ -333,6 +437,8 @@ int bode_probe_fp64(int64_t iters, int32_t blocks, double* out, void* stream);
  * tcgen05.mma kind::tf32 M=128 N=256 K=8 back to back; a timed launch gives
  * the TF32 tensor roofline denominator (2*128*256*8 flops per MMA). */
 int bode_probe_tf32(int32_t reps, int32_t blocks, void* stream);
+
+#endif /* __CUDACC_RTC__ */
 
 #ifdef __cplusplus
 }

@@ -67,7 +67,8 @@ class Args(C.Structure):
                 ("mlp_backend", C.c_int32), ("_pad3", C.c_int32),
                 ("prof_event_start", C.c_void_p), ("prof_event_stop", C.c_void_p),
                 ("launch_count_out", C.c_void_p),
-                ("traj", C.c_void_p), ("traj_offsets", C.c_void_p)]
+                ("traj", C.c_void_p), ("traj_offsets", C.c_void_p),
+                ("program", C.c_void_p)]
 
 
 _lib = None

@@ -15,6 +15,10 @@ from .dynamics import (AnalyticProblem, DeviceDynamics, VdpParams, analytic_prob
 from .solver import (DEFAULT_MAX_STEPS, IvpBatch, Solution, SolveStats, SolveStatus, host_empty,
                      pinned, solve, solve_device, solve_joint, adjoint_device)
 from .tableau import ButcherTableau, dopri5, heun, tsit5
+from .units import ControllerState, StepResult, adapt_step, error_norm, initial_step
+from .stepping import BatchSolver, Stepper, interpolate, rk_step
+from .problems import vdp_batch, vdp_limit_cycle
+from .trace import TraceError
 
 __version__ = "0.1.0"
 
@@ -26,4 +30,7 @@ __all__ = [
     "relaxation_dynamics", "sin_plus_t_dynamics", "square_dynamics", "vdp_dynamics",
     "zero_dynamics", "DEFAULT_MAX_STEPS", "IvpBatch", "Solution", "SolveStats", "SolveStatus",
     "solve", "solve_joint", "solve_device", "adjoint_device", "pinned", "host_empty", "ButcherTableau", "dopri5", "heun", "tsit5",
+    # the rest of batchode's public names (pkg/src/batchode/__init__.py:3-66)
+    "BatchSolver", "Stepper", "StepResult", "ControllerState", "rk_step", "interpolate",
+    "error_norm", "adapt_step", "initial_step", "vdp_batch", "vdp_limit_cycle", "TraceError",
 ]

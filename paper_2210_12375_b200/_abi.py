@@ -12,7 +12,7 @@ import os
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("BODE_LIB") or os.path.join(HERE, "_build", "libbode.so")
 
-ABI_VERSION = 4
+ABI_VERSION = 5
 TRAJ_EXTRA = 3
 
 
@@ -21,11 +21,12 @@ def traj_stride(d: int) -> int:
     return (d + TRAJ_EXTRA + 3) // 4 * 4
 OK, EINVAL, ECUDA, EUNSUPPORTED = 0, 1, 2, 3
 METHOD = {"dopri5": 0, "tsit5": 1, "heun": 2}
+METHOD_CUSTOM = 3
 MODE = {"exact": 0, "fast": 1}
 DT0_HEURISTIC, DT0_SCALAR, DT0_ARRAY = 0, 1, 2
 DYN = {"vdp": 1, "lorenz": 2, "zero": 3, "const": 4, "linear": 5, "linear_cos": 6,
        "linear_sin": 7, "relax_cos": 8, "square": 9, "logistic": 10, "sin_plus_t": 11,
-       "harmonic": 12, "damped": 13, "mlp": 20}
+       "harmonic": 12, "damped": 13, "mlp": 20, "program": 30}
 
 
 class BodeLibraryError(RuntimeError):
@@ -68,7 +69,31 @@ class SolveArgs(C.Structure):
                 ("mlp_backend", C.c_int32), ("_pad3", C.c_int32),
                 ("prof_event_start", C.c_void_p), ("prof_event_stop", C.c_void_p),
                 ("launch_count_out", C.c_void_p),
-                ("traj", C.c_void_p), ("traj_offsets", C.c_void_p)]
+                ("traj", C.c_void_p), ("traj_offsets", C.c_void_p),
+                ("program", C.c_void_p)]
+
+
+class ProgramDesc(C.Structure):
+    _fields_ = [("method", C.c_int32), ("kernels", C.c_int32), ("d", C.c_int64),
+                ("n_params", C.c_int32), ("stages", C.c_int32), ("order", C.c_int32),
+                ("error_order", C.c_int32), ("fsal", C.c_int32), ("_pad", C.c_int32)]
+
+
+TAB_MAX_STAGES, TAB_MAX_INTERP = 16, 8
+
+
+class Tableau_(C.Structure):
+    _fields_ = [("stages", C.c_int32), ("n_interp", C.c_int32), ("fsal", C.c_int32),
+                ("_pad", C.c_int32), ("a", C.c_double * (TAB_MAX_STAGES * TAB_MAX_STAGES)),
+                ("b", C.c_double * TAB_MAX_STAGES), ("b_err", C.c_double * TAB_MAX_STAGES),
+                ("c", C.c_double * TAB_MAX_STAGES),
+                ("interp", C.c_double * (TAB_MAX_STAGES * TAB_MAX_INTERP))]
+
+
+class StepState(C.Structure):
+    _fields_ = [("t", C.c_void_p), ("y", C.c_void_p), ("f0", C.c_void_p),
+                ("norm_prev", C.c_void_p), ("norm_prev2", C.c_void_p), ("te_next", C.c_void_p),
+                ("fsal_valid", C.c_void_p), ("flags", C.c_void_p)]
 
 
 class AdjointArgs(C.Structure):
@@ -99,6 +124,15 @@ SIGNATURES = {
                           C.c_int),
     "bode_probe_fp64": ([_I64, _I32, _P, _P], C.c_int),
     "bode_partition_workspace_size": ([_I64], _SZ),
+    "bode_program_create": ([C.c_char_p, _P, _P], C.c_int),
+    "bode_program_check": ([C.c_char_p, _P], C.c_int),
+    "bode_program_destroy": ([_P], None),
+    "bode_step_begin": ([C.POINTER(SolveArgs), _P], C.c_int),
+    "bode_step_once": ([C.POINTER(SolveArgs), _P], C.c_int),
+    "bode_program_rk_step": ([_P, _P, _P, _I64, _I64, _P, _P, _P, _P, _P, _P, _P, _P], C.c_int),
+    "bode_interpolate_tab": ([_P, _I64, _I64, _P, _P, _P, _P, _P, _P], C.c_int),
+    "bode_program_initial_step": ([_P, _P, _I64, _I64, _P, _P, _I32, _P, _P, _D, _D, _P, _P,
+                                   _P, _P], C.c_int),
     "bode_partition": ([_P, _I64, _I32, _P, _P, _P, _SZ, _P], C.c_int),
     "bode_probe_tf32": ([_I32, _I32, _P], C.c_int),
 }

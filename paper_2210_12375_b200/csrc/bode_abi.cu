@@ -21,10 +21,13 @@
 #include "bode_hostio.cuh"
 #include "bode_joint.cuh"
 #include "bode_mlp.cuh"
+#include "bode_program_host.cuh"
 #include "bode_sched.cuh"
 #include "bode_units.cuh"
 
 using namespace bode;
+
+int bode::set_error(int code, const std::string& msg);
 
 namespace {
 thread_local std::string g_err;
@@ -45,15 +48,32 @@ int cuda_fail(cudaError_t e, const char* where) {
   return fail(BODE_ECUDA, std::string(where) + ": " + cudaGetErrorString(e));
 }
 
-int stages_of(int method) { return method == BODE_METHOD_HEUN ? 2 : 7; }
-int error_order_of(int method) { return method == BODE_METHOD_HEUN ? 1 : 4; }
-int fsal_of(int method) { return method == BODE_METHOD_HEUN ? 0 : 1; }
+// tableau metadata: built-in methods, or a CUSTOM tableau's from its program
+int stages_of(const bode_solve_args* a) {
+  if (a->method == BODE_METHOD_CUSTOM) return program_desc(a->program).stages;
+  return a->method == BODE_METHOD_HEUN ? 2 : 7;
+}
+int error_order_of(const bode_solve_args* a) {
+  if (a->method == BODE_METHOD_CUSTOM) return program_desc(a->program).error_order;
+  return a->method == BODE_METHOD_HEUN ? 1 : 4;
+}
+int fsal_of(const bode_solve_args* a) {
+  if (a->method == BODE_METHOD_CUSTOM) return program_desc(a->program).fsal;
+  return a->method == BODE_METHOD_HEUN ? 0 : 1;
+}
 
-DynParams make_dyn(const bode_dynamics& d) {
+// per-instance parameter columns: the registered functors' masked slots,
+// or a program's n_params
+int inst_cols(const bode_dynamics& d, const bode_program* prog) {
+  if (d.kind == BODE_DYN_PROGRAM) return prog ? program_desc(prog).n_params : 0;
+  return __builtin_popcount(d.inst_mask);
+}
+
+DynParams make_dyn(const bode_dynamics& d, const bode_program* prog = nullptr) {
   DynParams p;
   p.kind = d.kind;
   p.inst_mask = d.inst_mask;
-  p.n_inst = __builtin_popcount(d.inst_mask);
+  p.n_inst = inst_cols(d, prog);
   p.inst = d.inst_params;
   for (int k = 0; k < 8; k++) p.shared[k] = d.shared_params[k];
   return p;
@@ -77,7 +97,7 @@ CtrlParams make_ctrl(const bode_controller& c, int error_order) {
 }
 
 bool valid_kind(int k) {
-  return (k >= BODE_DYN_VDP && k <= BODE_DYN_DAMPED) || k == BODE_DYN_MLP;
+  return (k >= BODE_DYN_VDP && k <= BODE_DYN_DAMPED) || k == BODE_DYN_MLP || k == BODE_DYN_PROGRAM;
 }
 
 int validate(const bode_solve_args* a) {
@@ -85,8 +105,17 @@ int validate(const bode_solve_args* a) {
   if (a->abi_version != BODE_ABI_VERSION) return fail(BODE_EINVAL, "abi_version mismatch");
   if (a->n < 1 || a->d < 1)
     return fail(BODE_EINVAL, "need at least one instance and one state component");
-  if (a->method < BODE_METHOD_DOPRI5 || a->method > BODE_METHOD_HEUN)
+  if (a->method < BODE_METHOD_DOPRI5 || a->method > BODE_METHOD_CUSTOM)
     return fail(BODE_EINVAL, "unknown method");
+  if ((a->method == BODE_METHOD_CUSTOM || a->dyn.kind == BODE_DYN_PROGRAM) && !a->program)
+    return fail(BODE_EINVAL, "a custom tableau / program dynamics needs args->program");
+  if (a->program) {
+    const bode_program_desc& pd = program_desc(a->program);
+    if (pd.method != a->method) return fail(BODE_EINVAL, "program compiled for another method");
+    if (pd.d != a->d) return fail(BODE_EINVAL, "program compiled for another state width");
+    if (a->dyn.kind == BODE_DYN_MLP) return fail(BODE_EUNSUPPORTED, "programs: analytic dynamics only");
+    if (a->traj) return fail(BODE_EUNSUPPORTED, "programs: no trajectory recording");
+  }
   if (a->mode != BODE_MODE_EXACT && a->mode != BODE_MODE_FAST) return fail(BODE_EINVAL, "unknown mode");
   if (!valid_kind(a->dyn.kind)) return fail(BODE_EINVAL, "unknown dynamics");
   if (a->max_steps < 1) return fail(BODE_EINVAL, "max_steps must be at least 1");
@@ -103,7 +132,8 @@ int validate(const bode_solve_args* a) {
   if (!(c.safety > 0.0 && c.safety <= 1.0)) return fail(BODE_EINVAL, "safety must be in (0, 1]");
   if (!(0.0 < c.factor_min && c.factor_min < 1.0 && 1.0 < c.factor_max))
     return fail(BODE_EINVAL, "need 0 < factor_min < 1 < factor_max");
-  if (a->dyn.inst_mask && !a->dyn.inst_params) return fail(BODE_EINVAL, "per-instance params missing");
+  if (inst_cols(a->dyn, a->program) && !a->dyn.inst_params)
+    return fail(BODE_EINVAL, "per-instance params missing");
   if (a->dyn.kind == BODE_DYN_MLP &&
       (!a->dyn.W1 || !a->dyn.b1 || !a->dyn.W2 || !a->dyn.b2 || a->dyn.hidden < 1))
     return fail(BODE_EINVAL, "MLP weights required");
@@ -138,7 +168,7 @@ Layout layout(const bode_solve_args* a, int64_t n_chunk, int slots) {
   L.lpt_slot = a->cost_hint && !a->order ? ((lpt_workspace_bytes(n_chunk) + 255) & ~(size_t)255) : 0;
   L.mlp = L.lpt + L.lpt_slot * slots;
   L.total = L.mlp + (a->dyn.kind == BODE_DYN_MLP ? mlp_workspace_bytes(a) : 0);
-  if (a->joint) L.total = L.f0 + joint_workspace_bytes(a->n, a->d, a->method);
+  if (a->joint) L.total = L.f0 + joint_workspace_bytes(a->n, a->d, stages_of(a));
   return L;
 }
 
@@ -156,7 +186,7 @@ int reset_workspace(const bode_solve_args* a, cudaStream_t st) {
 int run_chunk(const bode_solve_args* a, int64_t lo, int64_t hi, const Layout& L, cudaStream_t st,
               int slot = 0) {
   const int64_t n = hi - lo, d = a->d;
-  const int n_inst = __builtin_popcount(a->dyn.inst_mask);
+  const int n_inst = inst_cols(a->dyn, a->program);
   char* ws = (char*)a->workspace;
   const size_t qoff = slot ? 16 : 0;
   cudaError_t e = cudaMemsetAsync(ws + qoff, 0, 8, st);  // queue counter
@@ -165,9 +195,9 @@ int run_chunk(const bode_solve_args* a, int64_t lo, int64_t hi, const Layout& L,
   SolveParams P;
   memset(&P, 0, sizeof(P));
   P.n = n;
-  P.dyn = make_dyn(a->dyn);
+  P.dyn = make_dyn(a->dyn, a->program);
   if (P.dyn.inst) P.dyn.inst += lo * n_inst;
-  P.ctrl = make_ctrl(a->ctrl, error_order_of(a->method));
+  P.ctrl = make_ctrl(a->ctrl, error_order_of(a));
   P.y0 = a->y0 + lo * d;
   P.t_start = a->t_start + lo;
   P.t_end = a->t_end + lo;
@@ -219,12 +249,22 @@ int run_chunk(const bode_solve_args* a, int64_t lo, int64_t hi, const Layout& L,
   }
   if (a->joint) {
     g_launches += 1;
-    e = joint_solve(a->method, a->mode, a->dyn.kind, d, P, ws + L.f0, a->n_f_evals, st);
+    e = joint_solve(a->method, a->mode, a->dyn.kind, d, P, ws + L.f0, a->n_f_evals, st,
+                    a->program, stages_of(a));
+    if (e == cudaErrorNotSupported && a->program)
+      return fail(BODE_EINVAL, "program was not compiled with BODE_PROGRAM_JOINT");
     return e == cudaSuccess ? BODE_OK : cuda_fail(e, "joint solve");
   }
   if (a->dyn.kind == BODE_DYN_MLP) {
     e = mlp_solve(a, P, ws + L.mlp, st, &g_launches);
     return e == cudaSuccess ? BODE_OK : cuda_fail(e, "mlp solve");
+  }
+  if (a->program) {
+    e = program_solve(a->program, a->mode, P, a->threads_per_block, a->blocks, st);
+    g_launches += 2;
+    if (e == cudaErrorNotSupported)
+      return fail(BODE_EINVAL, "program was not compiled with BODE_PROGRAM_SOLVE");
+    return e == cudaSuccess ? BODE_OK : cuda_fail(e, "program solve launch");
   }
   switch (a->method) {
     case BODE_METHOD_DOPRI5: e = solve_dopri5(a->mode, a->dyn.kind, d, P, a->threads_per_block, a->blocks, st); break;
@@ -241,7 +281,7 @@ int finalize(const bode_solve_args* a, cudaStream_t st) {
   g_launches += 1;
   bode_finalize_kernel<<<1, 256, 0, st>>>((unsigned long long*)(ws + 8),
                                           (uint32_t*)(ws + Workspace::kHeader),
-                                          stages_of(a->method), fsal_of(a->method), a->n_f_evals,
+                                          stages_of(a), fsal_of(a), a->n_f_evals,
                                           a->max_iterations_out, a->refresh_map_out,
                                           a->max_steps + 2);
   cudaError_t e = cudaGetLastError();
@@ -292,6 +332,8 @@ HostStreams& host_streams() {
 
 }  // namespace
 
+int bode::set_error(int code, const std::string& msg) { return fail(code, msg); }
+
 extern "C" {
 
 int bode_abi_version(void) { return BODE_ABI_VERSION; }
@@ -330,6 +372,7 @@ int bode_solve_adjoint(const bode_solve_args* a, const bode_adjoint_args* g) {
   if (rc != BODE_OK) return rc;
   if (!g) return fail(BODE_EINVAL, "null adjoint args");
   if (a->joint) return fail(BODE_EUNSUPPORTED, "gradients: independent solve only");
+  if (a->program) return fail(BODE_EUNSUPPORTED, "gradients: built-in methods and dynamics only");
   if (a->dyn.kind == BODE_DYN_MLP &&
       !((a->d == 4 || a->d == 8 || a->d == 16 || a->d == 32 || a->d == 64) &&
         a->dyn.hidden <= 256 && a->dyn.hidden % 16 == 0))
@@ -382,7 +425,7 @@ int bode_solve_host(const bode_solve_args* h) {
   const bool csr = h->t_eval_offsets != nullptr;
   const int64_t n_te = csr ? h->t_eval_offsets[n] : h->t_eval_len;
   const int64_t ys_rows = csr ? n_te : n * h->t_eval_len;
-  const int n_inst = __builtin_popcount(h->dyn.inst_mask);
+  const int n_inst = inst_cols(h->dyn, h->program);
   int chunks = h->pipeline_chunks > 1 ? h->pipeline_chunks : 1;
   if (h->order || h->trace_cap > 0 || h->dyn.kind == BODE_DYN_MLP || h->joint) chunks = 1;
   if (chunks > n) chunks = (int)n;
@@ -700,4 +743,113 @@ extern "C" int bode_partition(const double* cost, int64_t n, int32_t world, int6
   compute_shard_sizes(n, world, cost != nullptr, shard_sizes);
   const cudaError_t e = shard_partition(cost, n, world, perm, ws, (cudaStream_t)stream);
   return e == cudaSuccess ? BODE_OK : cuda_fail(e, "bode_partition");
+}
+
+// ------------------------------------------------- stepping API (programs) --
+namespace {
+int step_params(const bode_solve_args* a, const bode_step_state* s, SolveParams& P) {
+  int rc = validate(a);
+  if (rc != BODE_OK) return rc;
+  if (!a->program) return fail(BODE_EINVAL, "the stepping API runs a program (args->program)");
+  if (!s || !s->t || !s->y || !s->f0 || !s->norm_prev || !s->norm_prev2 || !s->te_next ||
+      !s->fsal_valid || !s->flags)
+    return fail(BODE_EINVAL, "bode_step_state: every buffer is required");
+  if (a->order || a->cost_hint) return fail(BODE_EINVAL, "stepping: natural order only");
+  memset(&P, 0, sizeof(P));
+  P.n = a->n;
+  P.dyn = make_dyn(a->dyn, a->program);
+  P.ctrl = make_ctrl(a->ctrl, error_order_of(a));
+  P.y0 = a->y0;
+  P.t_start = a->t_start;
+  P.t_end = a->t_end;
+  P.t_eval = a->t_eval;
+  P.t_eval_offsets = a->t_eval_offsets;
+  P.t_eval_len = a->t_eval_offsets ? 0 : a->t_eval_len;
+  P.ys = a->ys;
+  P.atol_v = a->atol_v;
+  P.rtol_v = a->rtol_v;
+  P.atol = a->atol;
+  P.rtol = a->rtol;
+  P.max_steps = a->max_steps;
+  P.dt0_mode = a->dt0_mode;
+  P.dt0 = a->dt0;
+  P.dt0_v = a->dt0_v;
+  P.n_emitted = a->n_emitted;
+  P.n_steps = a->n_steps;
+  P.n_accepted = a->n_accepted;
+  P.final_dt = a->final_dt;
+  P.status = a->status;
+  P.trace_t = a->trace_t;
+  P.trace_dt = a->trace_dt;
+  P.trace_accept = a->trace_accept;
+  P.trace_cap = a->trace_cap;
+  P.f0 = s->f0;
+  P.te_next = s->te_next;
+  return BODE_OK;
+}
+}  // namespace
+
+extern "C" int bode_step_begin(const bode_solve_args* a, const bode_step_state* s) {
+  SolveParams P;
+  int rc = step_params(a, s, P);
+  if (rc != BODE_OK) return rc;
+  const cudaError_t e = program_init(a->program, a->mode, P, (cudaStream_t)a->stream);
+  if (e == cudaErrorNotSupported)
+    return fail(BODE_EINVAL, "program was not compiled with BODE_PROGRAM_STEP");
+  if (a->launch_count_out) *a->launch_count_out = 1;
+  return e == cudaSuccess ? BODE_OK : cuda_fail(e, "bode_step_begin");
+}
+
+extern "C" int bode_step_once(const bode_solve_args* a, const bode_step_state* s) {
+  SolveParams P;
+  int rc = step_params(a, s, P);
+  if (rc != BODE_OK) return rc;
+  cudaStream_t st = (cudaStream_t)a->stream;
+  cudaError_t e = cudaMemsetAsync(s->flags, 0, 8, st);
+  if (e != cudaSuccess) return cuda_fail(e, "bode_step_once");
+  StepState S{s->t, s->y, s->norm_prev, s->norm_prev2, s->fsal_valid, s->flags};
+  e = program_step(a->program, a->mode, P, S, st);
+  if (e == cudaErrorNotSupported)
+    return fail(BODE_EINVAL, "program was not compiled with BODE_PROGRAM_STEP");
+  if (a->launch_count_out) *a->launch_count_out = 1;
+  return e == cudaSuccess ? BODE_OK : cuda_fail(e, "bode_step_once");
+}
+
+// ------------------------------------------------------- program unit ops --
+extern "C" int bode_program_rk_step(const bode_program* prog, const bode_tableau* tab,
+                                    const bode_dynamics* dyn, int64_t n, int64_t d,
+                                    const double* t, const double* dt, const double* y,
+                                    const double* f0, double* y_next, double* err, double* k,
+                                    void* stream) {
+  if (!prog || !tab || !dyn || n < 1 || d != program_desc(prog).d || !t || !dt || !y || !y_next ||
+      !err || !k)
+    return fail(BODE_EINVAL, "bode_program_rk_step: invalid arguments");
+  const cudaError_t e = program_rk_step(prog, tab, make_dyn(*dyn, prog), n, t, dt, y, f0, y_next,
+                                        err, k, (cudaStream_t)stream);
+  if (e == cudaErrorNotSupported) return fail(BODE_EINVAL, "program was not compiled with BODE_PROGRAM_UNITS");
+  return e == cudaSuccess ? BODE_OK : cuda_fail(e, "bode_program_rk_step");
+}
+
+extern "C" int bode_interpolate_tab(const bode_tableau* tab, int64_t n, int64_t d,
+                                    const double* k, const double* y0, const double* dt,
+                                    const double* theta, double* out, void* stream) {
+  if (!tab || n < 1 || d < 1 || !k || !y0 || !dt || !theta || !out)
+    return fail(BODE_EINVAL, "bode_interpolate_tab: invalid arguments");
+  const cudaError_t e = unit_interpolate_tab(tab, n, d, k, y0, dt, theta, out, (cudaStream_t)stream);
+  return e == cudaSuccess ? BODE_OK : cuda_fail(e, "bode_interpolate_tab");
+}
+
+extern "C" int bode_program_initial_step(const bode_program* prog, const bode_dynamics* dyn,
+                                         int64_t n, int64_t d, const double* t0, const double* y0,
+                                         int32_t order, const double* atol_v,
+                                         const double* rtol_v, double atol, double rtol,
+                                         const double* direction, double* dt, double* f0,
+                                         void* stream) {
+  if (!prog || !dyn || n < 1 || d != program_desc(prog).d || !t0 || !y0 || !direction || !dt || !f0)
+    return fail(BODE_EINVAL, "bode_program_initial_step: invalid arguments");
+  const cudaError_t e = program_initial_step(prog, make_dyn(*dyn, prog), n, t0, y0, order, atol_v,
+                                             rtol_v, atol, rtol, direction, dt, f0,
+                                             (cudaStream_t)stream);
+  if (e == cudaErrorNotSupported) return fail(BODE_EINVAL, "program was not compiled with BODE_PROGRAM_UNITS");
+  return e == cudaSuccess ? BODE_OK : cuda_fail(e, "bode_program_initial_step");
 }

@@ -4,8 +4,7 @@
 // NumPy operation order; Ops selects exact (separately rounded IEEE ops,
 // SURVEY.md Appendix A) or fast (FMA-contracted) arithmetic.
 #pragma once
-#include <cstdint>
-#include <cuda_runtime.h>
+#include "bode_rtc.cuh"
 
 #include "../../include/bode.h"
 #include "bode_pow.cuh"

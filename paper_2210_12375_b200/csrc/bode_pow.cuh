@@ -16,9 +16,13 @@
 // Host and device share this code: the host build backs the CPU tests that
 // check it against 60-digit decimal arithmetic.
 #pragma once
+#if defined(__CUDACC__)
+#include "bode_rtc.cuh"
+#else
 #include <cmath>
 #include <cstdint>
 #include <cstring>
+#endif
 
 #include "pow_tables.h"
 
@@ -39,7 +43,9 @@ struct PowTables {
 #if defined(__CUDACC__)
 static __device__ const PowTables g_pow_tables = {BODE_POW_LOG_TABLE_INIT, BODE_POW_EXP_TABLE_INIT};
 #endif
+#if !defined(__CUDACC_RTC__)
 static const PowTables h_pow_tables = {BODE_POW_LOG_TABLE_INIT, BODE_POW_EXP_TABLE_INIT};
+#endif
 
 // Polynomial coefficients and split constants.  On the device they live in
 // the constant bank (FP64 instructions take them via LDCU, two per load)
@@ -51,7 +57,9 @@ static const PowTables h_pow_tables = {BODE_POW_LOG_TABLE_INIT, BODE_POW_EXP_TAB
 #if defined(__CUDACC__)
 static __constant__ double c_pow_k[20] = BODE_POW_K_INIT;
 #endif
+#if !defined(__CUDACC_RTC__)
 static const double h_pow_k[20] = BODE_POW_K_INIT;
+#endif
 #if defined(__CUDA_ARCH__)
 #define BODE_PK(i) c_pow_k[i]
 #else

@@ -408,6 +408,7 @@ __global__ void __launch_bounds__(128) bode_init_kernel(const SolveParams P) {
     L.initialize(P, i);
 }
 
+#if BODE_HOST_CODE
 // n_f_evals = 1 + (S-1)*max_n + #refresh iterations in [1, max_n)  (FSAL)
 //           = 1 + S*max_n                                        (non-FSAL)
 __global__ void bode_finalize_kernel(const unsigned long long* max_n, const uint32_t* refresh,
@@ -448,5 +449,7 @@ cudaError_t launch_persistent(const SolveParams& P, int threads, int blocks, cud
   if (P.ev_stop) cudaEventRecord((cudaEvent_t)P.ev_stop, st);
   return cudaGetLastError();
 }
+
+#endif  // BODE_HOST_CODE
 
 }  // namespace bode

@@ -4,6 +4,7 @@
 // against the GPU.  One thread per instance; these are test/diagnostic
 // entry points, not the hot path (that is bode_persistent_kernel).
 #include "bode_units.cuh"
+#include "bode_units_dev.cuh"
 
 namespace bode {
 
@@ -41,51 +42,6 @@ __global__ void bode_finalize_kernel(const unsigned long long* max_n, const uint
                       : (int64_t)(1 + (unsigned long long)stages * mx);
 }
 
-template <int M, class F>
-__global__ void rk_step_kernel(DynParams dp, int64_t n, const double* t, const double* dt,
-                               const double* y, const double* f0, double* y_next, double* err,
-                               double* k) {
-  constexpr int D = F::D, S = Tab<M>::S;
-  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  F f;
-  f.load(dp, i);
-  double kk[S][D], yy[D], yn[D], e[D];
-#pragma unroll
-  for (int c = 0; c < D; c++) {
-    yy[c] = y[i * D + c];
-    kk[0][c] = Tab<M>::FSAL ? f0[i * D + c] : 0.0;
-  }
-  rk_step<Tab<M>, F, ExactOps>(f, t[i], dt[i], yy, kk, yn, e);
-#pragma unroll
-  for (int c = 0; c < D; c++) {
-    y_next[i * D + c] = yn[c];
-    err[i * D + c] = e[c];
-  }
-#pragma unroll
-  for (int s = 0; s < S; s++)
-#pragma unroll
-    for (int c = 0; c < D; c++) k[(s * n + i) * D + c] = kk[s][c];
-}
-
-template <int M, int D>
-__global__ void interpolate_kernel(int64_t n, const double* k, const double* y0, const double* dt,
-                                   const double* theta, double* out) {
-  constexpr int S = Tab<M>::S;
-  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  double kk[S][D], yy[D], o[D];
-#pragma unroll
-  for (int c = 0; c < D; c++) yy[c] = y0[i * D + c];
-#pragma unroll
-  for (int s = 0; s < S; s++)
-#pragma unroll
-    for (int c = 0; c < D; c++) kk[s][c] = k[(s * n + i) * D + c];
-  interpolate<Tab<M>, D, ExactOps>(kk, yy, dt[i], theta[i], o);
-#pragma unroll
-  for (int c = 0; c < D; c++) out[i * D + c] = o[c];
-}
-
 __global__ void error_norm_kernel(int64_t n, int64_t d, const double* err, const double* y0,
                                   const double* y1, const double* atol_v, const double* rtol_v,
                                   double atol, double rtol, double* norm, double* scratch) {
@@ -114,26 +70,37 @@ __global__ void adapt_step_kernel(int64_t n, const double* norm, CtrlParams C, d
   dt_next[i] = h;
 }
 
-template <class F>
-__global__ void initial_step_kernel(DynParams dp, int64_t n, const double* t0, const double* y0,
-                                    int order, const double* atol_v, const double* rtol_v,
-                                    double atol, double rtol, const double* direction, double* dt,
-                                    double* f0) {
-  constexpr int D = F::D;
+static inline unsigned grid_for(int64_t n) { return (unsigned)((n + 127) / 128); }
+
+// Stepper.interpolate (stepper.py:112-139) for any tableau: Horner weights
+// with separate roundings, every stage term included, y0 + dt * sum
+__global__ void interpolate_tab_kernel(const bode_tableau* __restrict__ T, int64_t n, int64_t d,
+                                       const double* k, const double* y0, const double* dt,
+                                       const double* theta, double* out) {
+  using O = ExactOps;
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= n) return;
-  F f;
-  f.load(dp, i);
-  double yy[D], ff[D];
-#pragma unroll
-  for (int c = 0; c < D; c++) yy[c] = y0[i * D + c];
-  dt[i] = initial_step<F, ExactOps>(f, t0[i], yy, order, atol_v ? atol_v[i] : atol,
-                                    rtol_v ? rtol_v[i] : rtol, direction[i], ff);
-#pragma unroll
-  for (int c = 0; c < D; c++) f0[i * D + c] = ff[c];
+  const int S = T->stages, M = T->n_interp;
+  const double th = theta[i], h = dt[i];
+  double w[BODE_TABLEAU_MAX_STAGES];
+  for (int s = 0; s < S; s++) {
+    double v = T->interp[s * BODE_TABLEAU_MAX_INTERP + M - 1];
+    for (int j = M - 2; j >= 0; j--) v = O::add(O::mul(v, th), T->interp[s * BODE_TABLEAU_MAX_INTERP + j]);
+    w[s] = O::mul(v, th);
+  }
+  for (int64_t c = 0; c < d; c++) {
+    double acc = O::mul(w[0], k[i * d + c]);
+    for (int s = 1; s < S; s++) acc = O::add(acc, O::mul(w[s], k[(s * n + i) * d + c]));
+    out[i * d + c] = O::add(y0[i * d + c], O::mul(h, acc));
+  }
 }
 
-static inline unsigned grid_for(int64_t n) { return (unsigned)((n + 127) / 128); }
+cudaError_t unit_interpolate_tab(const bode_tableau* tab, int64_t n, int64_t d, const double* k,
+                                 const double* y0, const double* dt, const double* theta,
+                                 double* out, cudaStream_t st) {
+  interpolate_tab_kernel<<<grid_for(n), 128, 0, st>>>(tab, n, d, k, y0, dt, theta, out);
+  return cudaGetLastError();
+}
 
 template <int M, class F>
 static cudaError_t launch_rk(const DynParams& dp, int64_t n, const double* t, const double* dt,

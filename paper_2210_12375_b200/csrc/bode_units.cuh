@@ -19,4 +19,7 @@ cudaError_t unit_initial_step(const DynParams& dp, int64_t n, int64_t d, const d
                               const double* y0, int order, const double* av, const double* rv,
                               double a, double r, const double* dir, double* dt, double* f0,
                               cudaStream_t st);
+cudaError_t unit_interpolate_tab(const bode_tableau* tab, int64_t n, int64_t d, const double* k,
+                                 const double* y0, const double* dt, const double* theta,
+                                 double* out, cudaStream_t st);
 }  // namespace bode

@@ -28,7 +28,7 @@ __all__ = ["DeviceDynamics", "VdpParams", "vdp_dynamics", "lorenz_dynamics",
            "forced_linear_dynamics", "relaxation_dynamics", "square_dynamics",
            "logistic_dynamics", "sin_plus_t_dynamics", "harmonic_dynamics",
            "damped_dynamics", "mlp_dynamics", "AnalyticProblem", "analytic_problems",
-           "as_device_dynamics"]
+           "as_device_dynamics", "ProgramDynamics"]
 
 # parameter slot order per functor (must match include/bode.h)
 SLOTS = {
@@ -109,12 +109,46 @@ def _is_tensor(v) -> bool:
     return type(v).__module__.startswith("torch") and hasattr(v, "dim")
 
 
-def as_device_dynamics(f) -> DeviceDynamics:
-    if isinstance(f, DeviceDynamics):
+class ProgramDynamics:
+    """A NumPy dynamics callable traced into a device functor (trace.py) and
+    compiled into a run-time program with the solver templates
+    (program.py): the reference's plugin surface (stepper.py:19-20) for any
+    callable the tracer can follow.  ``params`` holds the (n, P) per-instance
+    values the callable closes over (None when there are none)."""
+
+    kind = "program"
+
+    def __init__(self, traced, params, d, source_fn=None):
+        self.traced, self.params, self.d = traced, params, d
+        self.n_params = 0 if params is None else int(params.shape[1])
+        self.source_fn = source_fn
+
+    def check_width(self, d: int) -> None:
+        if d != self.d:
+            raise ValueError(f"dynamics traced for d={self.d}, got d={d}")
+
+    def subset(self, idx) -> "ProgramDynamics":
+        p = None if self.params is None else self.params[idx]
+        return ProgramDynamics(self.traced, p, self.d, self.source_fn)
+
+    def __call__(self, t, y):
+        raise TypeError("traced dynamics are evaluated inside the B200 solver")
+
+
+def as_device_dynamics(f, n: int | None = None, d: int | None = None):
+    """Registered functors pass through; a NumPy callable f(t, y) is traced
+    for a batch of n instances of width d (trace.py) -- raising
+    NotImplementedError when it cannot run on the device (no CPU fallback)."""
+    if isinstance(f, (DeviceDynamics, ProgramDynamics)):
         return f
+    if callable(f) and n is not None and d is not None:
+        from .trace import trace_dynamics
+        tf = trace_dynamics(f, int(n), int(d))
+        return ProgramDynamics(tf, tf.params, int(d), f)
     raise NotImplementedError(
-        "arbitrary Python callables cannot run inside the sm_100a solver; use a registered "
-        "device functor from paper_2210_12375_b200.dynamics (no CPU fallback)")
+        "this Python callable cannot run inside the sm_100a solver; pass a registered device "
+        "functor from paper_2210_12375_b200.dynamics or a traceable NumPy callable "
+        "(no CPU fallback)")
 
 
 @dataclass(frozen=True)
@@ -243,10 +277,19 @@ def build_struct(dyn: DeviceDynamics, n: int, keep: list, device_arrays=None):
     device pointers (device path); without it host pointers are used."""
     s = _abi.Dynamics_()
     s.kind = _abi.DYN[dyn.kind]
+    ptr = device_arrays if device_arrays is not None else (lambda a: a.ctypes.data)
+    if dyn.kind == "program":
+        if dyn.params is not None:
+            if dyn.params.shape[0] != n:
+                raise ValueError(f"traced per-instance parameters have {dyn.params.shape[0]} "
+                                 f"rows, the batch has {n}")
+            inst = np.ascontiguousarray(dyn.params, dtype=np.float64)
+            keep.append(inst)
+            s.inst_params = ptr(inst)
+        return s
     shared, mask, cols = dyn.pack(n)
     s.shared_params = (_abi.C.c_double * 8)(*shared)
     s.inst_mask = mask
-    ptr = device_arrays if device_arrays is not None else (lambda a: a.ctypes.data)
     if cols:
         if device_arrays is not None and any(_is_tensor(c) for c in cols):
             import torch

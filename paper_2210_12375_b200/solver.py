@@ -23,7 +23,7 @@ import numpy as np
 from . import _abi
 from .controller import PidCoefficients, Tolerances, integral_controller
 from .dynamics import DeviceDynamics, as_device_dynamics, build_struct
-from .tableau import method_of
+from .tableau import is_custom, method_of
 
 __all__ = ["DEFAULT_MAX_STEPS", "SolveStatus", "IvpBatch", "SolveStats", "Solution",
            "solve", "solve_joint", "solve_device", "adjoint_device", "pinned", "host_empty"]
@@ -236,6 +236,27 @@ def _controller_struct(controller: PidCoefficients):
     return c
 
 
+def _bind_method(a, method, dyn, d: int, keep: list, kernels: int = 1):
+    """Set args.method (+ args.program for a custom tableau, traced dynamics
+    or a registered elementwise functor wider than the compiled-in widths:
+    a run-time specialisation of the same kernels, program.py)."""
+    need = is_custom(method) or dyn.kind == "program"
+    if not need and dyn.kind != "mlp":
+        try:
+            dyn.check_width(d)
+        except NotImplementedError:
+            need = True
+    else:
+        dyn.check_width(d)
+    a.method = _abi.METHOD_CUSTOM if is_custom(method) else _abi.METHOD[method]
+    if need:
+        from .program import get_program
+        prog = get_program(method, dyn, d, kernels)
+        keep.append(prog)
+        a.program = prog.handle
+    return need
+
+
 def _tol_arrays(tol: Tolerances, n: int):
     out = []
     for v in (tol.atol, tol.rtol):
@@ -259,16 +280,15 @@ def solve(problem: IvpBatch, f, tableau=None, tol: Tolerances | None = None,
     if max_steps < 1:
         raise ValueError("max_steps must be at least 1")
     lib = _abi.load()
-    dyn = as_device_dynamics(f)
+    n, d = problem.batch_size, problem.n_features
+    dyn = as_device_dynamics(f, n, d)
     method = method_of(tableau)
     tol = tol if tol is not None else Tolerances()
     controller = controller if controller is not None else integral_controller()
-    n, d = problem.batch_size, problem.n_features
-    dyn.check_width(d)
     keep = []
     a = _abi.SolveArgs()
     a.abi_version = _abi.ABI_VERSION
-    a.method = _abi.METHOD[method]
+    _bind_method(a, method, dyn, d, keep, kernels=8 if _joint else 1)  # program JOINT / SOLVE
     a.mode = _abi.MODE[mode]
     a.n, a.d = n, d
     a.dyn = build_struct(dyn, n, keep)
@@ -416,7 +436,6 @@ def solve_device(y0, t_start, t_end, f, *, t_eval=None, t_eval_offsets=None, met
     lib = _abi.load()
     if max_steps < 1:
         raise ValueError("max_steps must be at least 1")
-    dyn = as_device_dynamics(f)
     method = method_of(method)
     controller = controller if controller is not None else integral_controller()
     dev = y0.device
@@ -425,7 +444,7 @@ def solve_device(y0, t_start, t_end, f, *, t_eval=None, t_eval_offsets=None, met
     f64 = dict(dtype=torch.float64, device=dev)
     y0 = y0.to(**f64).contiguous()
     n, d = y0.shape
-    dyn.check_width(d)
+    dyn = as_device_dynamics(f, n, d)
     t_start = torch.as_tensor(t_start, **f64).expand(n).contiguous()
     t_end = torch.as_tensor(t_end, **f64).expand(n).contiguous()
     keep = [y0, t_start, t_end]
@@ -437,7 +456,7 @@ def solve_device(y0, t_start, t_end, f, *, t_eval=None, t_eval_offsets=None, met
 
     a = _abi.SolveArgs()
     a.abi_version = _abi.ABI_VERSION
-    a.method = _abi.METHOD[method]
+    _bind_method(a, method, dyn, d, keep)
     a.mode = _abi.MODE[mode]
     a.n, a.d = n, d
     a.dyn = build_struct(dyn, n, keep, device_arrays=dptr)

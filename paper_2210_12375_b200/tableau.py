@@ -8,9 +8,8 @@ and ``tsit5`` (:152-254, interpolant expanded with ``np.polymul`` as
 values are compiled in from ``csrc/tableau_coeffs.h``, which
 ``csrc/gen_tableau.py`` renders from the functions below; a test checks
 the committed header, these arrays and the reference tables agree bit for
-bit.  A tableau is therefore identified by ``method`` ("dopri5", "tsit5",
-"heun"); arbitrary user tableaus have no device implementation and are
-rejected with NotImplementedError (no CPU fallback).
+bit.  Any other (validated) tableau runs through a run-time specialisation
+of the same kernels with its coefficients compiled in (program.py).
 """
 
 from dataclasses import dataclass
@@ -148,20 +147,49 @@ def heun() -> ButcherTableau:
     return _make("heun", _heun_data())
 
 
-def method_of(tableau) -> str:
-    """Device method id for a tableau; only the built-in pairs run on B200."""
+def method_of(tableau):
+    """Device method for a tableau: the name of a built-in pair (compiled
+    into libbode) when the coefficients equal one -- whatever object carries
+    them, e.g. a reference-built ``batchode.dopri5()`` -- else the validated
+    tableau itself, which runs through a run-time program (program.py)."""
     if tableau is None:
         return "dopri5"
     if isinstance(tableau, str):
         if tableau not in ("dopri5", "tsit5", "heun"):
             raise ValueError(f"unknown method {tableau!r}")
         return tableau
-    m = getattr(tableau, "method", "")
-    if m in ("dopri5", "tsit5", "heun"):
-        ref = {"dopri5": dopri5, "tsit5": tsit5, "heun": heun}[m]()
-        if all(np.array_equal(getattr(tableau, k), getattr(ref, k))
-               for k in ("a", "b", "b_err", "c", "interp_coeffs")):
-            return m
-    raise NotImplementedError(
-        "only the built-in dopri5/tsit5/heun tableaus have sm_100a kernels; "
-        "custom tableaus are not supported (no CPU fallback)")
+    for k in ("stages", "a", "b", "b_err", "c", "order", "error_order", "interp_coeffs", "fsal"):
+        if not hasattr(tableau, k):
+            raise TypeError(f"tableau has no {k!r}: expected a ButcherTableau")
+    for name, make in (("dopri5", dopri5), ("tsit5", tsit5), ("heun", heun)):
+        ref = make()
+        if int(tableau.stages) == ref.stages and bool(tableau.fsal) == ref.fsal and \
+                int(tableau.order) == ref.order and int(tableau.error_order) == ref.error_order and \
+                all(np.array_equal(np.asarray(getattr(tableau, k), dtype=np.float64),
+                                   getattr(ref, k))
+                    for k in ("a", "b", "b_err", "c", "interp_coeffs")):
+            return name
+    S = int(tableau.stages)
+    if S < 1 or S > 16 or np.shape(tableau.interp_coeffs)[1] > 8:
+        raise NotImplementedError("device tableaus: at most 16 stages and 8 interpolant terms")
+    return tableau
+
+
+def is_custom(method) -> bool:
+    return not isinstance(method, str)
+
+
+def stages_of(method) -> int:
+    return int(method.stages) if is_custom(method) else (2 if method == "heun" else 7)
+
+
+def fsal_of(method) -> bool:
+    return bool(method.fsal) if is_custom(method) else method != "heun"
+
+
+def order_of(method) -> int:
+    return int(method.order) if is_custom(method) else (2 if method == "heun" else 5)
+
+
+def error_order_of(method) -> int:
+    return int(method.error_order) if is_custom(method) else (1 if method == "heun" else 4)

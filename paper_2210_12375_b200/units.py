@@ -141,10 +141,15 @@ def initial_step(f, t0, y0, order: int, tol: Tolerances, direction=1.0):
     """Two-evaluation starting step (controller.py:145-197) -> (dt, f0)."""
     torch = _torch()
     lib = _abi.load()
-    dyn = as_device_dynamics(f)
     y0 = np.atleast_2d(np.asarray(y0, dtype=float))
     n, d = y0.shape
-    dyn.check_width(d)
+    dyn = as_device_dynamics(f, n, d)
+    prog = None
+    if dyn.kind == "program":
+        from .program import UNITS, get_program
+        prog = get_program("dopri5", dyn, d, UNITS)
+    else:
+        dyn.check_width(d)
     keep = []
     dptr = lambda a: (keep.append(_dev(a)), keep[-1].data_ptr())[1]  # noqa: E731
     ds = build_struct(dyn, n, keep, device_arrays=dptr)
@@ -154,10 +159,13 @@ def initial_step(f, t0, y0, order: int, tol: Tolerances, direction=1.0):
     dr = _dev(np.broadcast_to(np.asarray(direction, dtype=float), (n,)))
     dt = torch.empty(n, dtype=torch.float64, device="cuda")
     f0 = torch.empty((n, d), dtype=torch.float64, device="cuda")
-    _abi.check(lib.bode_initial_step(_abi.C.addressof(ds), n, d, tt.data_ptr(), yy.data_ptr(),
-                                     int(order), av.data_ptr() if av is not None else None,
-                                     rv.data_ptr() if rv is not None else None, a, r,
-                                     dr.data_ptr(), dt.data_ptr(), f0.data_ptr(), _stream()))
+    args = (_abi.C.addressof(ds), n, d, tt.data_ptr(), yy.data_ptr(), int(order),
+            av.data_ptr() if av is not None else None, rv.data_ptr() if rv is not None else None,
+            a, r, dr.data_ptr(), dt.data_ptr(), f0.data_ptr(), _stream())
+    if prog is not None:  # traced dynamics: the program's initial_step kernel
+        _abi.check(lib.bode_program_initial_step(prog.handle, *args))
+    else:
+        _abi.check(lib.bode_initial_step(*args))
     return dt.cpu().numpy(), f0.cpu().numpy()
 
 

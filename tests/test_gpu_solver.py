@@ -232,9 +232,11 @@ def test_acceptance_4_large_batch_accuracy():  # tests/test_acceptance.py:116-12
     assert err < 1e-3
 
 
-def test_unregistered_callable_is_rejected():
+def test_untraceable_callable_is_rejected():
+    # a NumPy callable runs on the device once traced (tests/test_gpu_dropin.py);
+    # Python control flow on state values cannot be traced: no CPU fallback
     with pytest.raises(NotImplementedError):
-        bode.solve(_prob(np.ones((1, 1))), lambda t, y: y)
+        bode.solve(_prob(np.ones((1, 1))), lambda t, y: y if y[0, 0] > 0 else -y)
 
 
 def test_pipelined_host_path_matches_single_chunk():

@@ -77,18 +77,24 @@ def test_config_validation():  # reference tests/test_controller.py:31-58
         bode.VdpParams(-1.0)
 
 
-def test_tableaus_validate_and_custom_rejected():
+def test_tableaus_validate_and_custom_resolution():
     for tab in (bode.dopri5(), bode.tsit5(), bode.heun()):
         tab.validate()
         assert method_of(tab) == tab.method
     t = bode.dopri5()
+    # the same coefficients on any object (e.g. a reference-built tableau) are the built-in pair
+    clone = bode.ButcherTableau(stages=7, a=t.a.copy(), b=t.b.copy(), b_err=t.b_err.copy(),
+                                c=t.c.copy(), order=5, error_order=4,
+                                interp_coeffs=t.interp_coeffs.copy(), fsal=True)
+    assert method_of(clone) == "dopri5"
     custom = bode.ButcherTableau(stages=t.stages, a=t.a, b=t.b, b_err=t.b_err * 2, c=t.c,
                                  order=5, error_order=4, interp_coeffs=t.interp_coeffs, fsal=True)
-    with pytest.raises(NotImplementedError):
-        method_of(custom)
+    assert method_of(custom) is custom  # runs through a run-time program
+    with pytest.raises(TypeError):
+        method_of(object())
 
 
-def test_dynamics_packing_and_callables_rejected():
+def test_dynamics_packing_and_untraceable_callables():
     f = bode.forced_linear_dynamics(np.array([1.0, 2.0]), 0.5, 3.0)
     shared, mask, cols = f.pack(2)
     assert mask == 0b001 and shared[1] == 0.5 and shared[2] == 3.0
@@ -97,8 +103,12 @@ def test_dynamics_packing_and_callables_rejected():
         f.pack(3)
     with pytest.raises(ValueError):
         bode.vdp_dynamics(bode.VdpParams(2.0)).check_width(3)
+
+    def branchy(t, y):  # Python control flow on state values cannot be traced
+        return y if y[0, 0] > 0 else -y
+
     with pytest.raises(NotImplementedError):
-        bode.solve(bode.IvpBatch(np.ones((1, 1)), [0.0], [1.0], [np.empty(0)]), lambda t, y: y)
+        bode.solve(bode.IvpBatch(np.ones((1, 1)), [0.0], [1.0], [np.empty(0)]), branchy)
     with pytest.raises(TypeError):
         bode.vdp_dynamics(bode.VdpParams(2.0))(np.zeros(1), np.ones((1, 2)))
 
