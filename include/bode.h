@@ -320,6 +320,11 @@ int bode_interpolate(int32_t method, int32_t mode, int64_t n, int64_t d,
                      const double* k, const double* y0, const double* dt,
                      const double* theta, double* out, void* stream);
 
+/* f(t, y) of a registered functor on the batch (the reference's dynamics
+ * are callables, problems.py:41-50): t (n), y (n, d), out (n, d). */
+int bode_eval_dynamics(const bode_dynamics* dyn, int64_t n, int64_t d, const double* t,
+                       const double* y, double* out, void* stream);
+
 /* Mixed-tolerance RMS norm, NumPy pairwise summation order. */
 int bode_error_norm(int64_t n, int64_t d, const double* err, const double* y0,
                     const double* y1, const double* atol_v, const double* rtol_v,

@@ -123,6 +123,7 @@ SIGNATURES = {
     "bode_initial_step": ([_P, _I64, _I64, _P, _P, _I32, _P, _P, _D, _D, _P, _P, _P, _P],
                           C.c_int),
     "bode_probe_fp64": ([_I64, _I32, _P, _P], C.c_int),
+    "bode_eval_dynamics": ([_P, _I64, _I64, _P, _P, _P, _P], C.c_int),
     "bode_partition_workspace_size": ([_I64], _SZ),
     "bode_program_create": ([C.c_char_p, _P, _P], C.c_int),
     "bode_program_check": ([C.c_char_p, _P], C.c_int),

@@ -14,7 +14,7 @@ from dataclasses import dataclass
 import numpy as np
 
 __all__ = ["NORM_FLOOR", "PID_PRESETS", "Tolerances", "PidCoefficients",
-           "integral_controller", "pid_controller"]
+           "integral_controller", "pid_controller", "ControllerState"]
 
 NORM_FLOOR = 1e-10
 
@@ -73,3 +73,17 @@ def pid_controller(preset: str, **overrides) -> PidCoefficients:
             f"unknown PID preset {preset!r}; available: {sorted(PID_PRESETS)}"
         ) from None
     return PidCoefficients(beta1=b1, beta2=b2, beta3=b3, **overrides)
+
+
+@dataclass
+class ControllerState:
+    """Per-instance controller memory (controller.py:102-117)."""
+
+    norm_prev: np.ndarray
+    norm_prev2: np.ndarray
+    dt: np.ndarray
+
+    @classmethod
+    def initial(cls, dt: np.ndarray) -> "ControllerState":
+        n = dt.shape[0]
+        return cls(norm_prev=np.ones(n), norm_prev2=np.ones(n), dt=np.array(dt, dtype=float))

@@ -853,3 +853,13 @@ extern "C" int bode_program_initial_step(const bode_program* prog, const bode_dy
   if (e == cudaErrorNotSupported) return fail(BODE_EINVAL, "program was not compiled with BODE_PROGRAM_UNITS");
   return e == cudaSuccess ? BODE_OK : cuda_fail(e, "bode_program_initial_step");
 }
+
+extern "C" int bode_eval_dynamics(const bode_dynamics* dyn, int64_t n, int64_t d, const double* t,
+                                  const double* y, double* out, void* stream) {
+  if (!dyn || n < 1 || d < 1 || !t || !y || !out)
+    return fail(BODE_EINVAL, "bode_eval_dynamics: invalid arguments");
+  if (dyn->kind == BODE_DYN_MLP || dyn->kind == BODE_DYN_PROGRAM || !valid_kind(dyn->kind))
+    return fail(BODE_EUNSUPPORTED, "bode_eval_dynamics: registered analytic functors only");
+  const cudaError_t e = unit_eval_dynamics(make_dyn(*dyn), n, d, t, y, out, (cudaStream_t)stream);
+  return e == cudaSuccess ? BODE_OK : cuda_fail(e, "bode_eval_dynamics");
+}

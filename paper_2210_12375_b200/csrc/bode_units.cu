@@ -219,4 +219,34 @@ cudaError_t unit_initial_step(const DynParams& dp, int64_t n, int64_t d, const d
   }
 }
 
+template <class F>
+static cudaError_t launch_eval(const DynParams& dp, int64_t n, const double* t, const double* y,
+                               double* out, cudaStream_t st) {
+  eval_dynamics_kernel<F><<<grid_for(n), 128, 0, st>>>(dp, n, t, y, out);
+  return cudaGetLastError();
+}
+
+cudaError_t unit_eval_dynamics(const DynParams& dp, int64_t n, int64_t d, const double* t,
+                               const double* y, double* out, cudaStream_t st) {
+  using O = ExactOps;
+  switch (dp.kind) {
+    case BODE_DYN_VDP:
+      return d == 2 ? launch_eval<VdP<O>>(dp, n, t, y, out, st) : cudaErrorInvalidValue;
+    case BODE_DYN_LORENZ:
+      return d == 3 ? launch_eval<Lorenz<O>>(dp, n, t, y, out, st) : cudaErrorInvalidValue;
+    case BODE_DYN_HARMONIC:
+      return d == 2 ? launch_eval<Harmonic<O>>(dp, n, t, y, out, st) : cudaErrorInvalidValue;
+    case BODE_DYN_DAMPED:
+      return d == 2 ? launch_eval<Damped<O>>(dp, n, t, y, out, st) : cudaErrorInvalidValue;
+    default:
+      switch (d) {
+        case 1: return launch_eval<Elementwise<O, 1>>(dp, n, t, y, out, st);
+        case 2: return launch_eval<Elementwise<O, 2>>(dp, n, t, y, out, st);
+        case 3: return launch_eval<Elementwise<O, 3>>(dp, n, t, y, out, st);
+        case 4: return launch_eval<Elementwise<O, 4>>(dp, n, t, y, out, st);
+        default: return cudaErrorNotSupported;
+      }
+  }
+}
+
 }  // namespace bode

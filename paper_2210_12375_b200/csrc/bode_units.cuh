@@ -22,4 +22,6 @@ cudaError_t unit_initial_step(const DynParams& dp, int64_t n, int64_t d, const d
 cudaError_t unit_interpolate_tab(const bode_tableau* tab, int64_t n, int64_t d, const double* k,
                                  const double* y0, const double* dt, const double* theta,
                                  double* out, cudaStream_t st);
+cudaError_t unit_eval_dynamics(const DynParams& dp, int64_t n, int64_t d, const double* t,
+                               const double* y, double* out, cudaStream_t st);
 }  // namespace bode

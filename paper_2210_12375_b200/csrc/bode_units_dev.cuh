@@ -72,6 +72,24 @@ __global__ void initial_step_kernel(DynParams dp, int64_t n, const double* t0, c
   for (int c = 0; c < D; c++) f0[i * D + c] = ff[c];
 }
 
+// f(t, y) on the batch: a registered functor evaluated for callers that
+// call the dynamics object itself (problems.py:41-50 returns a callable)
+template <class F>
+__global__ void eval_dynamics_kernel(DynParams dp, int64_t n, const double* t, const double* y,
+                                     double* out) {
+  constexpr int D = F::D;
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  F f;
+  f.load(dp, i);
+  double yy[D], ff[D];
+#pragma unroll
+  for (int c = 0; c < D; c++) yy[c] = y[i * D + c];
+  f(t[i], yy, ff);
+#pragma unroll
+  for (int c = 0; c < D; c++) out[i * D + c] = ff[c];
+}
+
 // ---- runtime-coefficient tableau (any ButcherTableau, tableau.py:17-83) --
 // The unit ops of the stepping API take the tableau by value from device
 // memory, so Stepper.step / interpolate with a user tableau need no

@@ -101,8 +101,28 @@ class DeviceDynamics:
         return DeviceDynamics(self.kind, params, self.mlp)
 
     def __call__(self, t, y):
-        raise TypeError(f"{self.kind} is a device functor evaluated inside the B200 solver; "
-                        "it has no CPU evaluation path")
+        """f(t, y) on the batch, like the reference's dynamics callables
+        (problems.py:41-50): the device functor evaluated by one kernel
+        (``bode_eval_dynamics``), NumPy in / out."""
+        import torch
+        if self.kind == "mlp":
+            raise TypeError("MLP dynamics are evaluated inside the fused tcgen05 solver only")
+        if not torch.cuda.is_available():
+            raise _abi.BodeLibraryError("evaluating a device functor needs a CUDA device "
+                                        "(no CPU fallback)")
+        y = np.atleast_2d(np.asarray(y, dtype=np.float64))
+        n, d = y.shape
+        self.check_width(d)
+        tt = np.broadcast_to(np.asarray(0.0 if t is None else t, dtype=np.float64), (n,))
+        keep = []
+        dev = lambda a: (keep.append(torch.as_tensor(np.ascontiguousarray(a)).to("cuda")),  # noqa: E731
+                         keep[-1].data_ptr())[1]
+        ds = build_struct(self, n, keep, device_arrays=dev)
+        out = torch.empty((n, d), dtype=torch.float64, device="cuda")
+        lib = _abi.load()
+        _abi.check(lib.bode_eval_dynamics(_abi.C.addressof(ds), n, d, dev(tt), dev(y),
+                                          out.data_ptr(), torch.cuda.current_stream().cuda_stream))
+        return out.cpu().numpy()
 
 
 def _is_tensor(v) -> bool:

@@ -15,7 +15,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import _abi
-from .controller import NORM_FLOOR, PidCoefficients, Tolerances  # noqa: F401
+from .controller import NORM_FLOOR, ControllerState, PidCoefficients, Tolerances  # noqa: F401
 from .dynamics import as_device_dynamics, build_struct
 from .tableau import ButcherTableau, method_of
 
@@ -49,20 +49,6 @@ class StepResult:
     stage_derivs: np.ndarray
     f_next: np.ndarray | None
     n_evals: int = 0
-
-
-@dataclass
-class ControllerState:
-    """Per-instance controller memory (controller.py:102-117)."""
-
-    norm_prev: np.ndarray
-    norm_prev2: np.ndarray
-    dt: np.ndarray
-
-    @classmethod
-    def initial(cls, dt: np.ndarray) -> "ControllerState":
-        n = dt.shape[0]
-        return cls(norm_prev=np.ones(n), norm_prev2=np.ones(n), dt=np.array(dt, dtype=float))
 
 
 def rk_step(f, tableau: ButcherTableau, t, dt, y, f0) -> StepResult:

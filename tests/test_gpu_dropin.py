@@ -358,3 +358,13 @@ def test_solve_device_with_traced_dynamics_fast_mode():
     assert abs(int(a["n_steps"].sum()) / int(b["n_steps"].sum()) - 1.0) < 1e-4
     scale = b["ys"].abs().max()
     assert float((a["ys"] - b["ys"]).abs().max() / scale) <= 1e-8
+
+
+def test_registered_functors_are_callable_like_the_reference():
+    # problems.py:41-50 returns a callable; tests/test_problems.py calls it
+    f = batchode.vdp_dynamics(batchode.VdpParams(mu=np.array([0.0, 3.0])))
+    y = np.array([[1.5, -0.5], [0.3, 2.0]])
+    out = f(np.zeros(2), y)
+    mu = np.array([0.0, 3.0])
+    want = np.stack([y[:, 1], mu * (1.0 - y[:, 0] * y[:, 0]) * y[:, 1] - y[:, 0]], axis=1)
+    assert np.array_equal(out, want)

@@ -109,7 +109,9 @@ def test_dynamics_packing_and_untraceable_callables():
 
     with pytest.raises(NotImplementedError):
         bode.solve(bode.IvpBatch(np.ones((1, 1)), [0.0], [1.0], [np.empty(0)]), branchy)
-    with pytest.raises(TypeError):
+    # a registered functor is callable like the reference's dynamics, but it
+    # is evaluated on the device: no CUDA device here -> no CPU fallback
+    with pytest.raises(bode._abi.BodeLibraryError):
         bode.vdp_dynamics(bode.VdpParams(2.0))(np.zeros(1), np.ones((1, 2)))
 
 
