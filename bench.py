@@ -127,7 +127,24 @@ def cpu_run(cfg, sample, nthreads):
 
 
 def cpu_sample_size(cfg):
-    return {"c2": 262_144, "c5": 16_384, "c3": 4_096, "c1": 256, "c4": 1024}[cfg["_name"]]
+    # BASELINE.md §3 / SURVEY §8(d): C1 and C2 at full size, C3 >= 16K and
+    # C5 >= 64K seeded prefixes (the rate is intensive); C4's fp32-MLP oracle
+    # is ~1e5 steps/s, so a 1024-instance prefix
+    return {"c2": 2 ** 20, "c5": 65_536, "c3": 16_384, "c1": 256, "c4": 1024}[cfg["_name"]]
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+CPU_NOTE = ("C oracle (bode_oracle.c, gcc -O2 -ffp-contract=off, libm pow; no NumPy, so "
+            "NPY_DISABLE_CPU_FEATURES does not apply), one pthread per host core")
 
 
 def run_reference(args, rank, world):
@@ -150,15 +167,18 @@ def run_reference(args, rank, world):
     line = dict(metric="accepted instance-steps/sec", value=value,
                 unit="instance-steps/s", n_gpus=args.gpus, steps=args.steps,
                 warmup=args.warmup, ms_per_step=1e3 * secs / args.steps, higher_is_better=True,
-                scaling="weak", vs_baseline=None, dtype="f64", data="synthetic",
-                impl="reference",
-                config=dict(workload=cfg["workload"], sample_instances=sample,
-                            parallelism="host threads"),
+                scaling="strong" if world > 1 else "weak", vs_baseline=None, dtype="f64",
+                data="synthetic", impl="reference",
+                config=dict(workload=cfg["workload"], instances_per_gpu=cfg["n"],
+                            global_instances=cfg["n"], method=cfg["method"],
+                            controller="PI42" if cfg["ctrl"] is PI42 else "I", tol=cfg["tol"],
+                            sample_instances=min(sample, cfg["n"]),
+                            parallelism=f"host threads ({nthreads})"),
                 cpu_baseline=dict(value=value, unit="instance-steps/s", cores=nthreads,
-                                  kind="port",
-                                  sample=f"first {sample} instances of the seeded "
-                                         f"{cfg['workload']} batch per step (C oracle = "
-                                         "restatement of batchode, pthreads)"),
+                                  kind="port", cpu_model=cpu_model(), note=CPU_NOTE,
+                                  sample=f"first {min(sample, cfg['n'])} of the {cfg['n']} "
+                                         f"instances of the seeded {cfg['workload']} batch "
+                                         "per step"),
                 e2e=dict(value=value, unit="instance-steps/s", h2d_bytes_per_step=0,
                          d2h_bytes_per_step=0))
     print(json.dumps(line), flush=True)
@@ -488,8 +508,9 @@ def run_bode(args, rank, world, local_rank):
         sample = cpu_sample_size(cfg)
         a, s, k = cpu_run(cfg, sample, nthreads)
         cpu = dict(value=a / s, unit="instance-steps/s", cores=nthreads, kind="port",
-                   sample=f"first {k} instances of the seeded batch, one solve "
-                          f"({s:.2f} s wall, C oracle restating batchode, pthreads)")
+                   cpu_model=cpu_model(), note=CPU_NOTE,
+                   sample=f"first {k} of the {cfg['n']} instances of the seeded batch, one "
+                          f"solve ({s:.2f} s wall)")
 
     clocks = clk.summary(dev.index)
     if rank == 0:

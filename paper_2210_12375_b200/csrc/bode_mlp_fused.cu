@@ -355,9 +355,13 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_fused_kernel(const MlpFusedAr
           mbar_arrive(&sm.epidone[wg]);
           PROF_MARK(6)
         }
-        g2_base += nc;
         mbar_wait(&sm.stage_done, ph_sd);
         ph_sd ^= 1;
+        // the last chunk's GEMM2 completion (already complete once stage_done
+        // is: tcgen05.commit tracks every earlier MMA) is consumed here, so
+        // every g2done phase has a waiter
+        mbar_wait(&sm.g2done[wg], (g2_base + nc - 1) & 1);
+        g2_base += nc;
         fence_after();
         PROF_MARK(7)
         // ============ k_s = acc + b2 (the reference adds b2 after the sum)

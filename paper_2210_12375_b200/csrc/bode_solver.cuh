@@ -204,23 +204,32 @@ struct Lane {
   // PI (fast mode only): the launch was specialised for an I / PI
   // controller (CtrlParams::plain_pi), so the general controller is not
   // compiled into the loop
+  // the arithmetic of one attempt: t_end truncation, the RK trial step, the
+  // error norm and the controller (no memory traffic, no branches on the
+  // fast I / PI path); commit() applies the decision
   template <bool PI>
-  __device__ __forceinline__ bool step(const SolveParams& P, const PowTables& PT, bool tracing,
-                                       const TrajRows* trec, const EmitBase& eb) {
-    const int32_t j = nsteps;
+  __device__ __forceinline__ bool attempt(const SolveParams& P, const PowTables& PT, double* yn,
+                                          double* err, double& dtn, double& h, bool& trunc) {
     const double remaining = O::sub(t_end, t);
-    const bool trunc = fabs(dt) >= fabs(remaining);
-    const double h = trunc ? remaining : dt;
-    double yn[D], err[D];
+    trunc = fabs(dt) >= fabs(remaining);
+    h = trunc ? remaining : dt;
     rk_step<T, F, O>(f, t, h, y, k, yn, err);
-    double dtn = h;
-    bool accept;
+    dtn = h;
     if constexpr (O::kFast && PI) {
-      accept = adapt_pi_ms(P.ctrl, error_ms<D, O>(err, y, yn, atol_of(P), rtol_of(P)), L1, dtn, PT);
+      return adapt_pi_ms(P.ctrl, error_ms<D, O>(err, y, yn, atol_of(P), rtol_of(P)), L1, dtn, PT);
     } else {
       const double norm = error_norm<D, O>(err, y, yn, atol_of(P), rtol_of(P));
-      accept = adapt_cached<O>(P.ctrl, norm, n1, n2, L1, dtn, PT);
+      return adapt_cached<O>(P.ctrl, norm, n1, n2, L1, dtn, PT);
     }
+  }
+
+  // the rest of step_once for this row: statistics, trace, dense output,
+  // the masked commit and the statuses; returns true when the row just
+  // rejected and is still running (FSAL refresh at the next iteration)
+  __device__ __forceinline__ bool commit(const SolveParams& P, bool tracing, const TrajRows* trec,
+                                         const EmitBase& eb, const double* yn, bool accept,
+                                         double dtn, double h, bool trunc) {
+    const int32_t j = nsteps;
     nsteps = j + 1;
     if (tracing && j < P.trace_cap) {
       const int64_t o = idx * P.trace_cap + j;  // (trace only)
@@ -264,6 +273,23 @@ struct Lane {
     if (status == BODE_RUNNING && O::add(t, dt) == t) status = BODE_STEP_UNDERFLOW;
     if (status == BODE_RUNNING && nsteps >= P.max_steps) status = BODE_MAX_STEPS_EXCEEDED;
     return !accept && status == BODE_RUNNING;
+  }
+
+  // one iteration of step_once for this row (solver.py:208-282); returns
+  // true when the row just rejected and is still running (FSAL refresh at
+  // the next iteration, solver.py:220-226)
+  // trec (recording only): shared-memory slot holding this lane's
+  // trajectory rows [base, end), set at resume -- no per-step global load
+  // PI (fast mode only): the launch was specialised for an I / PI
+  // controller (CtrlParams::plain_pi), so the general controller is not
+  // compiled into the loop
+  template <bool PI>
+  __device__ __forceinline__ bool step(const SolveParams& P, const PowTables& PT, bool tracing,
+                                       const TrajRows* trec, const EmitBase& eb) {
+    double yn[D], err[D], dtn, h;
+    bool trunc;
+    const bool accept = attempt<PI>(P, PT, yn, err, dtn, h, trunc);
+    return commit(P, tracing, trec, eb, yn, accept, dtn, h, trunc);
   }
 
   // _emit, solver.py:284-322: every point with theta in (.., 1] is
