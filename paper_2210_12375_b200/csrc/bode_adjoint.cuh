@@ -34,6 +34,11 @@ struct AdjParams {
 size_t adjoint_workspace_bytes(int64_t n, int64_t d, int kind, int64_t H);
 size_t mlp_adjoint_part_bytes(int64_t d, int64_t H);
 cudaError_t mlp_adjoint_run(int method, int64_t d, AdjParams A, cudaStream_t st, int64_t* launches);
+// tensor-core backward for D = 64 (bode_mlp_adjoint_tc.cu); the workspace
+// of adjoint_workspace_bytes is sized for 7 stages (the widest tableau)
+bool mlp_adjoint_tc_supported(int64_t d, int64_t H);
+size_t mlp_adjoint_tc_bytes(int64_t n, int64_t H, int method);
+cudaError_t mlp_adjoint_tc_run(int method, AdjParams A, void* ws, cudaStream_t st, int64_t* launches);
 // Builds the longest-first queue from the trajectory lengths, then launches
 // the persistent backward kernel; returns the number of kernels launched
 // through *launches.

@@ -22,6 +22,7 @@ struct MlpTcArgs {
   const float* b1;
   const float* b2;
   float* out;           // (n, 64) rows scattered through act
+  float* Yout;          // optional (n, 64): the fp32 stage inputs formed (adjoint)
 };
 bool mlp_tc_supported(int64_t D, int64_t H);
 size_t mlp_tc_prep_bytes(int64_t H);

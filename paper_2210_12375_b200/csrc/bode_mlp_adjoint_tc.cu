@@ -1,0 +1,1005 @@
+// bode_mlp_adjoint_tc.cu -- the neural-ODE backward (SURVEY.md §8(f) row 1,
+// torchode's AutoDiffAdjoint for f(y) = W2 tanh(W1 y + b1) + b2) with every
+// contraction on the 5th-generation tensor cores.
+//
+// Same definition as the CUDA-core kernel (bode_mlp_adjoint.cu): reverse mode
+// through the recorded accepted steps -- stages, solution update, dense
+// output -- with step sizes and accept decisions held fixed; outputs dL/dy0
+// per instance and dL/dW1, db1, dW2, db2 summed over the batch.
+//
+// The rows are ordered by trajectory length, longest first (a stable radix
+// sort, so the order -- and every sum below -- is deterministic), and the
+// trajectories are reversed in lockstep: reverse iteration `it` undoes step
+// nrec-1-it of every row with nrec > it, i.e. of a prefix of the order.  Per
+// iteration:
+//   load     the step records of the live rows (t_old, h, cursor, y_old)
+//   forward  k_s = f(Y_s) for every stage: the tcgen05 stage kernel of the
+//            lockstep solve (bode_mlp_tc.cu), i.e. the forward's own MMAs
+//   seeds    dL/dk_s from dL/dy_next and the dense-output points of the step
+//   reverse  per stage s = S-1 .. 0, one tcgen05 kernel per 128-row tile:
+//              Z  = Y_s W1^T          (recomputed pre-activation, M=128 N=32 K=64)
+//              V  = g_s W2            (W2^T pre-split chunks, M=128 N=32 K=64)
+//              u  = V (1 - tanh(Z + b1)^2)         (epilogue, CUDA cores)
+//              Yb = sum_c u_c W1_c    (W1^T pre-split chunks, M=128 N=64 K=32)
+//            then dL/dk_j += h a_sj Yb (j < s), dL/dy_old += Yb;
+//            u^T, tanh^T, Y_s^T, g_s^T are written to global memory
+//            transposed (a warp of row threads writes 128 contiguous bytes)
+//   weights  one split-K tcgen05 GEMM over the iteration's (stage, row)
+//            columns: dW1 | db1 = u^T [Y | 1] (M=128 per half of H, N=80),
+//            dW2 | db2 = g^T [tanh | 1] (M=64, both halves interleaved in
+//            TMEM lanes 0-15 / 16-31 of each quadrant, N=144 / 128).
+// Every operand is K-major (tf32 MN-major descriptors read as zeros on this
+// part, tools/umma_probe.cu), so contractions over the rows read the
+// transposed copies.  3xTF32 throughout (hi*hi + hi*lo + lo*hi, fp32
+// accumulation), like the forward.
+#include <cub/cub.cuh>
+
+#include "bode_adjoint.cuh"
+#include "bode_mlp.cuh"
+#include "bode_solver.cuh"
+#include "bode_tc.cuh"
+
+namespace bode {
+namespace adjtc {
+using namespace tc;
+
+constexpr int kW = BODE_TRAJ_STRIDE(kD);  // trajectory row (doubles)
+constexpr int kN1 = 80;                   // dW1 | db1 accumulator width
+constexpr int kN2 = 144;                  // dW2 | db2 (half 0) width
+constexpr int kPartFloats = 2 * 128 * kN1 + 2 * 64 * kN2;  // one CTA's partial sums
+
+// The transposed weight-gradient operands (u^T, tanh^T: H rows; Y^T, g^T: 64
+// rows) are stored in 32-column blocks, [col / 32][row][col % 32], so one
+// K-slice of the GEMM is a contiguous block and a warp of row threads (32
+// consecutive columns) still writes 128 contiguous bytes per row.
+__host__ __device__ __forceinline__ int64_t blk(int64_t row, int64_t col, int64_t rows) {
+  return ((col >> 5) * rows + row) * 32 + (col & 31);
+}
+
+__host__ __device__ constexpr uint32_t idesc_mn(int M, int N) {
+  return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(N >> 3) << 17) |
+         ((uint32_t)(M >> 4) << 24);
+}
+
+// ---------------------------------------------------------------- glue ----
+
+__global__ void keys_kernel(const int64_t* off, int64_t n, int32_t* keys, int32_t* idx) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    keys[i] = (int32_t)(off[i + 1] - off[i]);
+    idx[i] = (int32_t)i;
+  }
+}
+
+__global__ void transpose_kernel(const float* in, int rows, int cols, float* out) {
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < rows * cols; e += gridDim.x * blockDim.x)
+    out[(e % cols) * rows + e / cols] = in[e];
+}
+
+struct RowState {
+  int64_t n, pmax;
+  const int32_t* order;  // LPT position -> instance
+  const int32_t* nrec;   // LPT position -> trajectory length (descending)
+  int32_t* count;        // rows live in this iteration
+  int64_t* hi;           // first point of the later step (the previous lo)
+  int64_t* lo;           // cursor of the step being reversed
+  double* t_old;
+  double* h;
+  double* y;             // (n, 64) y_old
+  double* kb;            // (S, n, 64) dL/dk_s
+  double* yb;            // (n, 64) dL/dy (carried as dL/dy_next to the next iteration)
+};
+
+__global__ void init_kernel(RowState R, const int64_t* n_emitted) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < R.n * kD;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    R.yb[e] = 0.0;
+    if (e % kD == 0) R.lo[e / kD] = n_emitted[R.order[e / kD]];
+  }
+}
+
+// rows live at iteration it: nrec is sorted descending
+__global__ void count_kernel(RowState R, int64_t it) {
+  int64_t lo = 0, hi = R.n;  // first position with nrec <= it
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) / 2;
+    if (R.nrec[mid] > it) lo = mid + 1; else hi = mid;
+  }
+  *R.count = (int32_t)lo;
+}
+
+__global__ void load_kernel(RowState R, const double* traj, const int64_t* traj_off, int64_t it) {
+  const int64_t cnt = *R.count;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < cnt * kD;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t p = e / kD;
+    const int c = (int)(e % kD);
+    const int64_t i = R.order[p];
+    const double* rec = traj + (traj_off[i] + R.nrec[p] - 1 - it) * kW;
+    R.y[e] = rec[kTrajExtra + c];
+    if (c == 0) {  // (only this thread touches the row's hi / lo)
+      R.t_old[p] = rec[0];
+      R.h[p] = rec[1];
+      R.hi[p] = R.lo[p];
+      R.lo[p] = (int64_t)rec[2];
+    }
+  }
+}
+
+// dL/dk_s seeds of the step: y_next = y + h sum b_s k_s and the Horner dense
+// output of the points in [lo, hi) (bode_mlp_adjoint.cu, same operations)
+template <int M>
+__global__ void seeds_kernel(RowState R, const double* t_eval, const int64_t* t_eval_offsets,
+                             int64_t t_eval_len, const double* grad_ys) {
+  using T = Tab<M>;
+  constexpr int S = T::S, NI = T::NI;
+  const int64_t cnt = *R.count;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < cnt * kD;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t p = e / kD;
+    const int c = (int)(e % kD);
+    const int64_t i = R.order[p];
+    const double h = R.h[p], a0 = R.yb[e];
+    double kb[S];
+#pragma unroll
+    for (int s = 0; s < S; s++) kb[s] = (h * T::b(s)) * a0;
+    double y_b = a0;
+    const double* te = t_eval_offsets ? t_eval + t_eval_offsets[i] : t_eval;
+    const double* gy = t_eval_offsets ? grad_ys + t_eval_offsets[i] * kD : grad_ys + i * t_eval_len * kD;
+    const double t_old = R.t_old[p];
+    const int64_t hi = R.hi[p];
+    for (int64_t q = R.lo[p]; q < hi; q++) {
+      double theta = ddiv(te[q] - t_old, h);
+      theta = np_max(theta, 0.0);
+      const double g = gy[q * kD + c];
+      y_b += g;
+#pragma unroll
+      for (int s = 0; s < S; s++) {
+        double v = T::w(s, NI - 1);
+#pragma unroll
+        for (int j = NI - 2; j >= 0; j--) v = fma(v, theta, T::w(s, j));
+        kb[s] = fma(h * (v * theta), g, kb[s]);
+      }
+    }
+#pragma unroll
+    for (int s = 0; s < S; s++) R.kb[(s * R.n + p) * kD + c] = kb[s];
+    R.yb[e] = y_b;
+  }
+}
+
+// dL/dy_old = dL/dy_next + points + sum over the stages (reversed order)
+template <int M>
+__global__ void fold_kernel(RowState R, const float* Ybar) {
+  constexpr int S = Tab<M>::S;
+  const int64_t cnt = *R.count;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < cnt * kD;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    double v = R.yb[e];
+#pragma unroll
+    for (int s = S - 1; s >= 0; s--) v += (double)Ybar[(int64_t)s * R.n * kD + e];
+    R.yb[e] = v;
+  }
+}
+
+__global__ void finish_kernel(RowState R, const double* grad_ys, const int64_t* t_eval_offsets,
+                              int64_t t_eval_len, double* grad_y0) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < R.n * kD;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t p = e / kD;
+    const int c = (int)(e % kD);
+    const int64_t i = R.order[p];
+    const double* gy = t_eval_offsets ? grad_ys + t_eval_offsets[i] * kD : grad_ys + i * t_eval_len * kD;
+    double a0 = R.yb[e];
+    const int64_t first = R.lo[p];  // cursor of the row's first step
+    for (int64_t q = 0; q < first; q++) a0 += gy[q * kD + c];  // points at t_start
+    grad_y0[i * kD + c] = a0;
+  }
+}
+
+// -DBODE_ADJ_PROF (debug builds): per-phase clock64 stamps of CTA 0's first
+// tiles, threads 0 (MMA issue) and 128 (producer), read by bode_debug_adj_prof
+#ifdef BODE_ADJ_PROF
+__device__ long long g_adj_prof[2][512];
+__device__ int g_adj_prof_n[2];
+#define ADJ_STAMP(w, tag)                                                             \
+  if (blockIdx.x == 0 && A.stage == 3) {                                              \
+    const int k_ = g_adj_prof_n[w]++;                                                 \
+    if (k_ < 256) {                                                                   \
+      g_adj_prof[w][2 * k_] = tag;                                                    \
+      g_adj_prof[w][2 * k_ + 1] = clock64();                                          \
+    }                                                                                 \
+  }
+#else
+#define ADJ_STAMP(w, tag)
+#endif
+
+// ------------------------------------------------- reverse stage (VJP) ----
+
+struct VjpArgs {
+  int64_t n, pmax;
+  int H, stage;
+  const int32_t* count;
+  const double* y;
+  const float* k;
+  const float* Ybuf;  // (S, n, 64) fp32 stage inputs from the forward recompute (stages < S-1)
+  const double* h;
+  const double* kb;   // (S, n, 64) dL/dk_s seeds (dense output, y_next)
+  float* Ybar;        // (S, n, 64) dL/dY_s of every stage reversed so far
+  const float* wfwd;  // forward chunks [W1_c | W2_c] (hi | lo each)
+  const float* wadj;  // adjoint chunks [(W2^T)_c | (W1^T)_c]
+  const float* b1;
+  float *uT, *AT, *YT, *gT;  // (rows, S * pmax), column = stage * pmax + row
+};
+
+// Y_s / g_s tiles in shared memory; the weights of two hidden chunks in
+// flight (buffer = chunk sequence number & 1); u_c lives in TMEM (the A
+// operand of the Yb GEMM), so the epilogue never writes shared memory
+struct VjpSmem {
+  uint8_t ay[2][kATile];     // Y_s hi, lo
+  uint8_t ag[2][kATile];     // g_s hi, lo
+  uint8_t w1[2][2][kW1];     // [buf] W1_c hi, lo
+  uint8_t wv[2][2][kW1];     // [buf] (W2^T)_c hi, lo
+  uint8_t wy[2][2][kW2];     // [buf] (W1^T)_c hi, lo
+  float b1[256];
+  uint64_t full, empty, wa[2], wy_full[2], g1[2], g2[2];
+  uint32_t tmem_base;
+};
+
+// Producer thread r owns tile row r.  vjp_stage_input forms the row's
+// stage input Y_s exactly as the forward did (bode_mlp_tc.cu: fp64 sum in
+// the reference order, rounded to fp32) into registers and writes its
+// transpose (a warp writes 128 contiguous bytes per column); it runs for the
+// NEXT tile while the consumer still works on this one.  vjp_store_tiles
+// then writes Y_s and g_s as TF32 hi/lo core matrices.
+template <int M>
+__device__ __forceinline__ void vjp_stage_input(const VjpArgs& A, int64_t p, bool lv, float* x) {
+  using T = Tab<M>;
+  const int stage = A.stage;
+  const int64_t col = (int64_t)stage * A.pmax + p;
+#pragma unroll
+  for (int g8 = 0; g8 < kD / 8; g8++) {  // 8 columns at a time: every load in flight
+    double yv[8];
+    float kv[T::S][8];
+    if (lv) {
+      const double2* yp = reinterpret_cast<const double2*>(A.y + p * kD + 8 * g8);
+#pragma unroll
+      for (int e = 0; e < 4; e++) {
+        const double2 d = __ldg(yp + e);
+        yv[2 * e] = d.x, yv[2 * e + 1] = d.y;
+      }
+#pragma unroll
+      for (int j = 0; j < T::S; j++)
+        if (j < stage) {
+          const float4* kp = reinterpret_cast<const float4*>(A.k + ((int64_t)j * A.n + p) * kD + 8 * g8);
+          const float4 k0 = __ldg(kp), k1 = __ldg(kp + 1);
+          kv[j][0] = k0.x, kv[j][1] = k0.y, kv[j][2] = k0.z, kv[j][3] = k0.w;
+          kv[j][4] = k1.x, kv[j][5] = k1.y, kv[j][6] = k1.z, kv[j][7] = k1.w;
+        }
+      const double hr = A.h[p];
+#pragma unroll
+      for (int e = 0; e < 8; e++) {
+        if (stage == 0) {
+          x[8 * g8 + e] = (float)yv[e];
+        } else {
+          double s = 0.0;
+#pragma unroll
+          for (int j = 0; j < T::S; j++) {
+            if (j >= stage) break;
+            s = j == 0 ? ExactOps::mul(T::a(stage, 0), (double)kv[0][e])
+                       : ExactOps::mad(T::a(stage, j), (double)kv[j][e], s);
+          }
+          x[8 * g8 + e] = (float)ExactOps::mad(hr, s, yv[e]);
+        }
+        A.YT[blk(8 * g8 + e, col, kD)] = x[8 * g8 + e];
+      }
+    } else {
+#pragma unroll
+      for (int e = 0; e < 8; e++) x[8 * g8 + e] = 0.0f;
+    }
+  }
+}
+
+template <int M>
+__device__ __forceinline__ void vjp_store_tiles(const VjpArgs& A, int64_t p, bool lv, int r,
+                                                const float* x, VjpSmem& S) {
+  const int64_t col = (int64_t)A.stage * A.pmax + p;
+  // dL/dk_s = seed + sum over the later stages s' (in the order they were
+  // reversed, S-1 down to s+1) of h a_s's dL/dY_s'
+  using T = Tab<M>;
+  const int stage = A.stage;
+  const double* kp = A.kb + ((int64_t)stage * A.n + p) * kD;
+  const double hp = lv ? A.h[p] : 0.0;
+  float gall[kD];
+#pragma unroll
+  for (int g8 = 0; g8 < kD / 8; g8++) {
+    double acc[8];
+    float yv[T::S][8];
+    if (lv) {
+#pragma unroll
+      for (int e = 0; e < 4; e++) {
+        const double2 d = __ldg(reinterpret_cast<const double2*>(kp + 8 * g8) + e);
+        acc[2 * e] = d.x, acc[2 * e + 1] = d.y;
+      }
+#pragma unroll
+      for (int s2 = T::S - 1; s2 > 0; s2--) {
+        if (s2 <= stage || T::za(s2, stage) == 0.0) continue;
+        const float4* yp = reinterpret_cast<const float4*>(A.Ybar + ((int64_t)s2 * A.n + p) * kD + 8 * g8);
+        const float4 a = __ldg(yp), b = __ldg(yp + 1);
+        yv[s2][0] = a.x, yv[s2][1] = a.y, yv[s2][2] = a.z, yv[s2][3] = a.w;
+        yv[s2][4] = b.x, yv[s2][5] = b.y, yv[s2][6] = b.z, yv[s2][7] = b.w;
+      }
+#pragma unroll
+      for (int s2 = T::S - 1; s2 > 0; s2--) {
+        if (s2 <= stage || T::za(s2, stage) == 0.0) continue;
+        const double w = hp * T::a(s2, stage);
+#pragma unroll
+        for (int e = 0; e < 8; e++) acc[e] = fma(w, (double)yv[s2][e], acc[e]);
+      }
+    } else {
+#pragma unroll
+      for (int e = 0; e < 8; e++) acc[e] = 0.0;
+    }
+#pragma unroll
+    for (int e = 0; e < 8; e++) gall[8 * g8 + e] = (float)acc[e];
+  }
+#pragma unroll
+  for (int q8 = 0; q8 < kD / 8; q8++) {
+    float gv[8];
+#pragma unroll
+    for (int e = 0; e < 8; e++) gv[e] = gall[8 * q8 + e];
+    if (lv) {
+#pragma unroll
+      for (int e = 0; e < 8; e++) A.gT[blk(8 * q8 + e, col, kD)] = gv[e];
+    } else {
+#pragma unroll
+      for (int e = 0; e < 8; e++) gv[e] = 0.0f;
+    }
+#pragma unroll
+    for (int h4 = 0; h4 < 2; h4++) {
+      const int q = 2 * q8 + h4;  // 4-column chunk
+      const uint32_t o = cm_off(r, 4 * q, kD);
+      const float* xs = x + 4 * q;
+      const float* gs = gv + 4 * h4;
+      float4 hi, lo;
+      hi.x = tf32_hi(xs[0]), hi.y = tf32_hi(xs[1]), hi.z = tf32_hi(xs[2]), hi.w = tf32_hi(xs[3]);
+      lo.x = xs[0] - hi.x, lo.y = xs[1] - hi.y, lo.z = xs[2] - hi.z, lo.w = xs[3] - hi.w;
+      *reinterpret_cast<float4*>(S.ay[0] + o) = hi;
+      *reinterpret_cast<float4*>(S.ay[1] + o) = lo;
+      hi.x = tf32_hi(gs[0]), hi.y = tf32_hi(gs[1]), hi.z = tf32_hi(gs[2]), hi.w = tf32_hi(gs[3]);
+      lo.x = gs[0] - hi.x, lo.y = gs[1] - hi.y, lo.z = gs[2] - hi.z, lo.w = gs[3] - hi.w;
+      *reinterpret_cast<float4*>(S.ag[0] + o) = hi;
+      *reinterpret_cast<float4*>(S.ag[1] + o) = lo;
+    }
+  }
+}
+
+template <int M>
+__global__ void __launch_bounds__(256, 1) vjp_kernel(const VjpArgs A) {
+  using T = Tab<M>;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  VjpSmem& S = *reinterpret_cast<VjpSmem*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+  const int tid = threadIdx.x, warp = tid >> 5;
+  const int cnt = *A.count;
+  const int ntiles = (cnt + kRows - 1) / kRows;
+  if ((int)blockIdx.x >= ntiles) return;
+  const int nchunk = A.H / kHc;
+
+  if (tid == 0) {
+    mbar_init(&S.full, 1);
+    mbar_init(&S.empty, 1);
+    for (int b = 0; b < 2; b++) {
+      mbar_init(&S.wa[b], 1);
+      mbar_init(&S.wy_full[b], 1);
+      mbar_init(&S.g1[b], 1);
+      mbar_init(&S.g2[b], 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  for (int j = tid; j < A.H; j += blockDim.x) S.b1[j] = A.b1[j];
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+        smem_u32(&S.tmem_base)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+
+  if (tid >= 128) {
+    // ============ producer: Y_s and g_s tiles (+ their transposes) ============
+    const int r = tid - 128;
+    float x[kD];
+    int kl = 0;
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, kl++) {
+      const int64_t p = (int64_t)tile * kRows + r;
+      const bool lv = p < cnt;
+      if (tid == 128) { ADJ_STAMP(1, 1) }
+      if (A.stage == T::S - 1) {
+        vjp_stage_input<M>(A, p, lv, x);  // overlaps the consumer's previous tile
+      } else {  // the forward recompute kept this stage's inputs
+        const float4* yp = reinterpret_cast<const float4*>(A.Ybuf + ((int64_t)A.stage * A.n + p) * kD);
+        float4 v[kD / 4];
+#pragma unroll
+        for (int e = 0; e < kD / 4; e++) v[e] = lv ? __ldg(yp + e) : make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+        const int64_t col = (int64_t)A.stage * A.pmax + p;
+#pragma unroll
+        for (int e = 0; e < kD / 4; e++) {
+          x[4 * e] = v[e].x, x[4 * e + 1] = v[e].y, x[4 * e + 2] = v[e].z, x[4 * e + 3] = v[e].w;
+          if (lv) {
+#pragma unroll
+            for (int f = 0; f < 4; f++) A.YT[blk(4 * e + f, col, kD)] = x[4 * e + f];
+          }
+        }
+      }
+      if (tid == 128) { ADJ_STAMP(1, 2) }
+      if (kl >= 1) mbar_wait(&S.empty, (kl - 1) & 1);
+      if (tid == 128) { ADJ_STAMP(1, 3) }
+      vjp_store_tiles<M>(A, p, lv, r, x, S);
+      fence_async_smem();
+      group_sync(1);
+      if (tid == 128) { ADJ_STAMP(1, 4) }
+      if (tid == 128) mbar_arrive(&S.full);
+    }
+  } else {
+    // ================== consumer: MMAs + epilogues ==================
+    // TMEM columns: Z / V accumulators of chunk buffer b at 64 b / 64 b + 32,
+    // Yb at 128, u_c hi / lo of buffer b at 192 + 64 b / 192 + 64 b + 32
+    const uint32_t tmem = S.tmem_base;
+    const uint32_t lane_off = (uint32_t)(warp * 32) << 16;
+    const uint32_t accY = tmem + 128;
+    const char* wf = (const char*)A.wfwd;
+    const char* wa = (const char*)A.wadj;
+    const int my_tiles = (ntiles - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;
+    const int total = my_tiles * nchunk;  // chunk sequence numbers q of this CTA
+    auto load_wa = [&](int q) {  // W1_c and (W2^T)_c of chunk q into buffer q & 1
+      const int b = q & 1, c = q % nchunk;
+      mbar_expect_tx(&S.wa[b], 4 * kW1);
+      bulk_g2s(S.w1[b][0], wf + (size_t)c * kWChunk, kW1, &S.wa[b]);
+      bulk_g2s(S.w1[b][1], wf + (size_t)c * kWChunk + kW1, kW1, &S.wa[b]);
+      bulk_g2s(S.wv[b][0], wa + (size_t)c * kWChunk, kW1, &S.wa[b]);
+      bulk_g2s(S.wv[b][1], wa + (size_t)c * kWChunk + kW1, kW1, &S.wa[b]);
+    };
+    auto load_wy = [&](int q) {  // (W1^T)_c
+      const int b = q & 1, c = q % nchunk;
+      mbar_expect_tx(&S.wy_full[b], 2 * kW2);
+      bulk_g2s(S.wy[b][0], wa + (size_t)c * kWChunk + 2 * kW1, kW2, &S.wy_full[b]);
+      bulk_g2s(S.wy[b][1], wa + (size_t)c * kWChunk + 2 * kW1 + kW2, kW2, &S.wy_full[b]);
+    };
+    auto phase = [](int q) { return (uint32_t)((q >> 1) & 1); };
+    const int ta[3] = {0, 0, 1}, tb[3] = {0, 1, 0};
+    auto issue_zv = [&](int q) {  // Z = Y_s W1_c^T, V = g_s (W2^T)_c^T into buffer q & 1
+      const int b = q & 1;
+      mbar_wait(&S.wa[b], phase(q));
+      fence_after();
+      const uint32_t az = tmem + 64 * b, av = az + 32;
+#pragma unroll
+      for (int s = 0; s < kD / 8; s++)
+#pragma unroll
+        for (int term = 0; term < 3; term++) {
+          mma_tf32(az, smem_desc(smem_u32(S.ay[ta[term]]) + 256 * s, 2048),
+                   smem_desc(smem_u32(S.w1[b][tb[term]]) + 256 * s, 2048), idesc(kHc), (term | s) ? 1u : 0u);
+          mma_tf32(av, smem_desc(smem_u32(S.ag[ta[term]]) + 256 * s, 2048),
+                   smem_desc(smem_u32(S.wv[b][tb[term]]) + 256 * s, 2048), idesc(kHc), (term | s) ? 1u : 0u);
+        }
+      mma_commit(&S.g1[b]);
+    };
+    if (tid == 0) {
+      load_wa(0);
+      load_wy(0);
+      if (total > 1) {
+        load_wa(1);
+        load_wy(1);
+      }
+    }
+    int kl = 0;
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, kl++) {
+      if (tid == 0) { ADJ_STAMP(0, 10) }
+      mbar_wait(&S.full, kl & 1);
+      if (tid == 0) { ADJ_STAMP(0, 11) }
+      const int64_t p = (int64_t)tile * kRows + tid;
+      const bool live = p < cnt;
+      const int64_t col = (int64_t)A.stage * A.pmax + p;
+      const int q0 = kl * nchunk;
+      if (tid == 0) issue_zv(q0);
+      for (int c = 0; c < nchunk; c++) {
+        const int q = q0 + c, b = q & 1;
+        if (tid == 0) { ADJ_STAMP(0, 20) }
+        if (tid == 0) {
+          if (c + 1 < nchunk) issue_zv(q + 1);   // runs under this chunk's epilogue
+          else mma_commit(&S.empty);             // Y_s / g_s tiles free after these
+          if (q >= 1) {                          // Yb(q-1) done: its weight buffer is free
+            mbar_wait(&S.g2[(q - 1) & 1], phase(q - 1));
+            if (q + 1 < total) load_wy(q + 1);
+          }
+        }
+        if (tid == 0) { ADJ_STAMP(0, 21) }
+        mbar_wait(&S.g1[b], phase(q));
+        fence_after();
+        if (tid == 0) { ADJ_STAMP(0, 22) }
+        if (tid == 0 && q + 2 < total) load_wa(q + 2);
+        if (q >= 2) mbar_wait(&S.g2[b], phase(q - 2));  // u buffer b free (Yb(q-2) done)
+        // ---- epilogue: tanh, u = V (1 - tanh^2) -> TMEM (hi, lo); u^T, tanh^T
+        {
+          float z[32], v[32];
+          tmem_ld32(tmem + 64 * b + lane_off, z);
+          tmem_ld32(tmem + 64 * b + 32 + lane_off, v);
+          float uh[32], ul[32];
+          const int c32 = (q % nchunk) * kHc;
+#pragma unroll
+          for (int j = 0; j < kHc; j++) {
+            const float a = tanhf(z[j] + S.b1[c32 + j]);
+            const float uu = v[j] * (1.0f - a * a);
+            uh[j] = tf32_hi(uu);
+            ul[j] = uu - uh[j];
+            if (live) {
+              A.uT[blk(c32 + j, col, A.H)] = uu;
+              A.AT[blk(c32 + j, col, A.H)] = a;
+            }
+          }
+          const uint32_t ub = tmem + 192 + 64 * b + lane_off;
+          tmem_st16(ub, uh);
+          tmem_st16(ub + 16, uh + 16);
+          tmem_st16(ub + 32, ul);
+          tmem_st16(ub + 48, ul + 16);
+          tmem_wait_st();
+        }
+        if (tid == 0) { ADJ_STAMP(0, 23) }
+        fence_before();
+        group_sync(2);
+        if (tid == 0) { ADJ_STAMP(0, 24) }
+        // ---- Yb += u_c (W1^T)_c^T  (A from TMEM, 3xTF32, K = 32 in 4 steps)
+        if (tid == 0) {
+          fence_after();
+          mbar_wait(&S.wy_full[b], phase(q));
+          const uint32_t uhi = tmem + 192 + 64 * b, ulo = uhi + 32;
+#pragma unroll
+          for (int s = 0; s < kHc / 8; s++) {
+            const uint64_t wh = smem_desc(smem_u32(S.wy[b][0]) + 256 * s, 1024);
+            const uint64_t wl = smem_desc(smem_u32(S.wy[b][1]) + 256 * s, 1024);
+            mma_tf32_ts(accY, uhi + 8 * s, wh, idesc(kD), (c | s) ? 1u : 0u);
+            mma_tf32_ts(accY, uhi + 8 * s, wl, idesc(kD), 1u);
+            mma_tf32_ts(accY, ulo + 8 * s, wh, idesc(kD), 1u);
+          }
+          mma_commit(&S.g2[b]);
+        }
+      }
+      // ---- dL/dY_s of the row: dL/dy_old += Yb, dL/dk_j += h a_sj Yb (j < s)
+      if (tid == 0) { ADJ_STAMP(0, 30) }
+      mbar_wait(&S.g2[(q0 + nchunk - 1) & 1], phase(q0 + nchunk - 1));
+      fence_after();
+      if (tid == 0) { ADJ_STAMP(0, 31) }
+      {
+        float yb[kD];
+        tmem_ld32(accY + lane_off, yb);
+        tmem_ld32(accY + lane_off + 32, yb + 32);
+        if (live) {
+          float4* dst = reinterpret_cast<float4*>(A.Ybar + ((int64_t)A.stage * A.n + p) * kD);
+#pragma unroll
+          for (int e = 0; e < kD / 4; e++)
+            dst[e] = make_float4(yb[4 * e], yb[4 * e + 1], yb[4 * e + 2], yb[4 * e + 3]);
+        }
+      }
+      if (tid == 0) { ADJ_STAMP(0, 32) }
+      fence_before();
+      group_sync(2);
+    }
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(S.tmem_base));
+}
+
+// --------------------------------------------- weight gradients (GEMM) ----
+
+struct WgArgs {
+  int H, S;
+  int64_t pmax, ldt;
+  const int32_t* count;
+  const float *uT, *AT, *YT, *gT;
+  float* part;  // (grid, kPartFloats)
+};
+
+struct WgSmem {
+  uint8_t au[2][2][128 * 32 * 4];  // u^T halves [h][hi, lo]
+  uint8_t ag[2][64 * 32 * 4];      // g^T [hi, lo]
+  uint8_t by[2][kN1 * 32 * 4];     // [Y^T | 1] [hi, lo]
+  uint8_t ba[2][2][kN2 * 32 * 4];  // [tanh^T half | 1 (half 0)] [h][hi, lo]
+  uint64_t mb;
+  uint32_t tmem_base;
+};
+
+// One K-slice (32 columns) of the weight-gradient operands, held in
+// registers between its global loads and its shared-memory stores so the
+// loads of slice i+1 are in flight while the MMAs of slice i run.  A source
+// tile is rows [0, nrows) of a row-major (., ldt) fp32 matrix, columns
+// [c0, c0 + 32) with those >= cmax zeroed; rows >= nrows are zero and row
+// `ones` (if >= 0) is 1.0 (the bias column of the GEMM).
+struct WgTile {
+  const float* src;   // the matrix (blocked layout); set to the slice's block per fetch
+  int nrows, ones;
+  int64_t rows;       // the matrix's row count (block stride)
+  int64_t row0;       // first row of this tile
+  uint8_t *hi, *lo;
+};
+template <int TROWS>
+constexpr int wg_vec() { return (TROWS * 8 + 255) / 256; }
+
+template <int TROWS>
+__device__ __forceinline__ void wg_fetch(WgTile T, int64_t ldt, int64_t c0, int64_t cmax,
+                                         float4 (&v)[wg_vec<TROWS>()]) {
+  T.src += ((c0 >> 5) * T.rows + T.row0) * 32;
+#pragma unroll
+  for (int q = 0; q < wg_vec<TROWS>(); q++) {
+    const int e = threadIdx.x + 256 * q;
+    const int r = e >> 3, k4 = e & 7;
+    float4 x = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+    if (e < TROWS * 8) {
+      if (r < T.nrows)  // (src: this slice's 32-column block, row-major)
+        x = __ldg(reinterpret_cast<const float4*>(T.src + (int64_t)r * 32 + 4 * k4));
+      else if (r == T.ones)
+        x = make_float4(1.0f, 1.0f, 1.0f, 1.0f);
+      const int64_t c = c0 + 4 * k4;
+      if (c >= cmax) x.x = 0.0f;
+      if (c + 1 >= cmax) x.y = 0.0f;
+      if (c + 2 >= cmax) x.z = 0.0f;
+      if (c + 3 >= cmax) x.w = 0.0f;
+    }
+    v[q] = x;
+  }
+}
+
+template <int TROWS>
+__device__ __forceinline__ void wg_store(const WgTile& T, const float4 (&v)[wg_vec<TROWS>()]) {
+#pragma unroll
+  for (int q = 0; q < wg_vec<TROWS>(); q++) {
+    const int e = threadIdx.x + 256 * q;
+    if (e < TROWS * 8) {
+      const int r = e >> 3, k4 = e & 7;
+      const float4 x = v[q];
+      float4 hi, lo;
+      hi.x = tf32_hi(x.x), hi.y = tf32_hi(x.y), hi.z = tf32_hi(x.z), hi.w = tf32_hi(x.w);
+      lo.x = x.x - hi.x, lo.y = x.y - hi.y, lo.z = x.z - hi.z, lo.w = x.w - hi.w;
+      const uint32_t o = cm_off(r, 4 * k4, 32);
+      *reinterpret_cast<float4*>(T.hi + o) = hi;
+      *reinterpret_cast<float4*>(T.lo + o) = lo;
+    }
+  }
+}
+
+// the operand tiles of one slice: u^T and [tanh^T | 1] per half of H,
+// g^T, [Y^T | 1]; the second half is loaded only when H > 128
+struct WgRegs {
+  float4 u0[wg_vec<128>()], a0[wg_vec<kN2>()], u1[wg_vec<128>()], a1[wg_vec<128>()];
+  float4 g[wg_vec<64>()], y[wg_vec<kN1>()];
+};
+struct WgTiles {
+  WgTile u0, a0, u1, a1, g, y;
+};
+__device__ __forceinline__ void wg_fetch_all(const WgTiles& T, bool two, int64_t ldt, int64_t c0,
+                                             int64_t cmax, WgRegs& R) {
+  wg_fetch<128>(T.u0, ldt, c0, cmax, R.u0);
+  wg_fetch<kN2>(T.a0, ldt, c0, cmax, R.a0);
+  if (two) {
+    wg_fetch<128>(T.u1, ldt, c0, cmax, R.u1);
+    wg_fetch<128>(T.a1, ldt, c0, cmax, R.a1);
+  }
+  wg_fetch<64>(T.g, ldt, c0, cmax, R.g);
+  wg_fetch<kN1>(T.y, ldt, c0, cmax, R.y);
+}
+__device__ __forceinline__ void wg_store_all(const WgTiles& T, bool two, const WgRegs& R) {
+  wg_store<128>(T.u0, R.u0);
+  wg_store<kN2>(T.a0, R.a0);
+  if (two) {
+    wg_store<128>(T.u1, R.u1);
+    wg_store<128>(T.a1, R.a1);
+  }
+  wg_store<64>(T.g, R.g);
+  wg_store<kN1>(T.y, R.y);
+}
+
+__global__ void __launch_bounds__(256, 1) wg_kernel(const WgArgs A) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  WgSmem& S = *reinterpret_cast<WgSmem*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+  const int tid = threadIdx.x, warp = tid >> 5;
+  const int cnt = *A.count;
+  const int per_stage = (cnt + 31) / 32;
+  const int nslices = A.S * per_stage;
+  if ((int)blockIdx.x >= nslices) return;
+  const int halves = A.H > 128 ? 2 : 1;
+  if (tid == 0) {
+    mbar_init(&S.mb, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+        smem_u32(&S.tmem_base)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const uint32_t tmem = S.tmem_base;
+  const int rows0 = A.H < 128 ? A.H : 128, rows1 = A.H - rows0;
+  const bool two = halves == 2;
+  const WgTiles T{WgTile{A.uT, rows0, -1, A.H, 0, S.au[0][0], S.au[0][1]},
+                  WgTile{A.AT, rows0, 128, A.H, 0, S.ba[0][0], S.ba[0][1]},
+                  WgTile{A.uT, rows1, -1, A.H, 128, S.au[1][0], S.au[1][1]},
+                  WgTile{A.AT, rows1, -1, A.H, 128, S.ba[1][0], S.ba[1][1]},
+                  WgTile{A.gT, kD, -1, kD, 0, S.ag[0], S.ag[1]},
+                  WgTile{A.YT, kD, kD, kD, 0, S.by[0], S.by[1]}};
+  auto slice_cols = [&](int sl, int64_t& c0, int64_t& cmax) {
+    const int s = sl / per_stage;
+    c0 = (int64_t)s * A.pmax + (int64_t)(sl % per_stage) * 32;
+    cmax = (int64_t)s * A.pmax + cnt;
+  };
+  // TMEM: dW1|db1 half h at columns 80 h (M = 128: row = hidden unit);
+  // dW2|db2 at columns 160 (M = 64: row = output; half 0 in lanes 0-15,
+  // half 1 in lanes 16-31 of each quadrant)
+  WgRegs R;
+  {
+    int64_t c0, cmax;
+    slice_cols(blockIdx.x, c0, cmax);
+    wg_fetch_all(T, two, A.ldt, c0, cmax, R);
+  }
+  uint32_t ph = 0;
+  int done = 0;
+  for (int sl = blockIdx.x; sl < nslices; sl += gridDim.x, done++) {
+    wg_store_all(T, two, R);
+    fence_async_smem();
+    fence_before();
+    __syncthreads();
+    if (tid == 0) {
+      fence_after();
+      const int ta[3] = {0, 0, 1}, tb[3] = {0, 1, 0};
+#pragma unroll
+      for (int ks = 0; ks < 4; ks++)
+#pragma unroll
+        for (int term = 0; term < 3; term++) {
+          const uint32_t acc = (done | ks | term) ? 1u : 0u;
+          for (int h = 0; h < halves; h++) {
+            mma_tf32(tmem + kN1 * h, smem_desc(smem_u32(S.au[h][ta[term]]) + 256 * ks, 1024),
+                     smem_desc(smem_u32(S.by[tb[term]]) + 256 * ks, 1024), idesc_mn(128, kN1), acc);
+            mma_tf32(tmem + 2 * kN1 + (h ? (16u << 16) : 0u),
+                     smem_desc(smem_u32(S.ag[ta[term]]) + 256 * ks, 1024),
+                     smem_desc(smem_u32(S.ba[h][tb[term]]) + 256 * ks, 1024),
+                     idesc_mn(64, h ? 128 : kN2), acc);
+          }
+        }
+      mma_commit(&S.mb);
+    }
+    if (sl + (int)gridDim.x < nslices) {  // next slice's loads overlap these MMAs
+      int64_t c0, cmax;
+      slice_cols(sl + gridDim.x, c0, cmax);
+      wg_fetch_all(T, two, A.ldt, c0, cmax, R);
+    }
+    mbar_wait(&S.mb, ph);
+    ph ^= 1;
+    fence_after();
+  }
+  // add this CTA's sums to its partial (the same CTA index every iteration:
+  // a fixed summation order)
+  if (warp < 4) {
+    float* part = A.part + (size_t)blockIdx.x * kPartFloats;
+    const uint32_t lo = (uint32_t)(warp * 32) << 16;
+    const int l = tid & 31;
+    float v[32];
+    for (int h = 0; h < halves; h++) {
+      float* dst = part + (size_t)h * 128 * kN1 + (size_t)tid * kN1;  // row = hidden 128 h + tid
+      for (int c = 0; c < kN1; c += 16) {
+        tmem_ld16(tmem + kN1 * h + lo + c, v);
+        for (int j = 0; j < 16; j++) dst[c + j] += v[j];
+      }
+    }
+    // M = 64 accumulators: lane l < 16 of quadrant w holds output 16 w + l
+    // of half 0, lane 16 + l the same output of half 1
+    const int hh = l >> 4, o = 16 * warp + (l & 15);
+    const int width = hh ? 128 : kN2;
+    float* dst = part + (size_t)2 * 128 * kN1 + ((size_t)hh * 64 + o) * kN2;
+    for (int c = 0; c < kN2; c += 16) {
+      tmem_ld16(tmem + 2 * kN1 + lo + c, v);
+      if (hh < halves)
+        for (int j = 0; j < 16; j++)
+          if (c + j < width) dst[c + j] += v[j];
+    }
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+}
+
+// partials -> gW1 (H, 64), gb1 (H), gW2 (64, H), gb2 (64); fixed order
+__global__ void wg_reduce_kernel(const float* part, int parts, int H, float* gW1, float* gb1,
+                                 float* gW2, float* gb2) {
+  const int total = H * kD + H + kD * H + kD;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x) {
+    size_t off;
+    if (e < H * kD) {
+      const int j = e / kD, c = e % kD;
+      off = (size_t)(j >> 7) * 128 * kN1 + (size_t)(j & 127) * kN1 + c;
+    } else if (e < H * kD + H) {
+      const int j = e - H * kD;
+      off = (size_t)(j >> 7) * 128 * kN1 + (size_t)(j & 127) * kN1 + kD;
+    } else if (e < 2 * H * kD + H) {
+      const int r = e - H * kD - H, o = r / H, j = r % H;
+      off = (size_t)2 * 128 * kN1 + ((size_t)(j >> 7) * 64 + o) * kN2 + (j & 127);
+    } else {
+      const int o = e - 2 * H * kD - H;
+      off = (size_t)2 * 128 * kN1 + (size_t)o * kN2 + 128;
+    }
+    double s = 0.0;
+    for (int b = 0; b < parts; b++) s += (double)part[(size_t)b * kPartFloats + off];
+    const float v = (float)s;
+    if (e < H * kD) {
+      if (gW1) gW1[e] = v;
+    } else if (e < H * kD + H) {
+      if (gb1) gb1[e - H * kD] = v;
+    } else if (e < 2 * H * kD + H) {
+      if (gW2) gW2[e - H * kD - H] = v;
+    } else if (gb2) {
+      gb2[e - 2 * H * kD - H] = v;
+    }
+  }
+}
+
+// ------------------------------------------------------------ workspace ----
+
+struct Layout {
+  size_t total = 0;
+  size_t keys_in, keys, idx_in, order, cub, cub_bytes, count, hi0, hi1, lo, t_old, h, y, k, kb, yb, Ybuf, Ybar,
+      uT, AT, YT, gT, wfwd, wadj, w1t, w2t, part;
+  Layout(int64_t n, int64_t H, int S, int parts) {
+    auto take = [&](size_t bytes) {
+      const size_t o = total;
+      total += (bytes + 255) & ~(size_t)255;
+      return o;
+    };
+    const int64_t pmax = (n + 127) / 128 * 128;
+    cub_bytes = 0;
+    cub::DeviceRadixSort::SortPairsDescending(nullptr, cub_bytes, (const int32_t*)nullptr,
+                                              (int32_t*)nullptr, (const int32_t*)nullptr,
+                                              (int32_t*)nullptr, (int)n);
+    keys_in = take(4 * n), keys = take(4 * n), idx_in = take(4 * n), order = take(4 * n);
+    cub = take(cub_bytes), count = take(8);
+    hi0 = take(8 * n), hi1 = take(8 * n), lo = take(8 * n), t_old = take(8 * n), h = take(8 * n);
+    y = take(8 * n * kD), k = take(4 * (size_t)S * n * kD), kb = take(8 * (size_t)S * n * kD);
+    Ybuf = take(4 * (size_t)S * n * kD), Ybar = take(4 * (size_t)S * n * kD);
+    yb = take(8 * n * kD);
+    uT = take(4 * (size_t)H * S * pmax), AT = take(4 * (size_t)H * S * pmax);
+    YT = take(4 * (size_t)kD * S * pmax), gT = take(4 * (size_t)kD * S * pmax);
+    wfwd = take(mlp_tc_prep_bytes(H)), wadj = take(mlp_tc_prep_bytes(H));
+    w1t = take(4 * H * kD), w2t = take(4 * H * kD);
+    part = take(4 * (size_t)parts * kPartFloats);
+  }
+};
+
+int sm_count() {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  return sms;
+}
+
+template <int M>
+cudaError_t run(AdjParams A, char* ws, cudaStream_t st, int64_t* launches) {
+  constexpr int S = Tab<M>::S;
+  const int64_t n = A.n, H = A.H;
+  const int sms = sm_count();
+  const Layout L(n, H, S, sms);
+  const int64_t pmax = (n + 127) / 128 * 128;
+  auto at = [&](size_t o) { return ws + o; };
+  RowState R;
+  R.n = n;
+  R.pmax = pmax;
+  R.order = (const int32_t*)at(L.order);
+  R.nrec = (const int32_t*)at(L.keys);
+  R.count = (int32_t*)at(L.count);
+  R.hi = (int64_t*)at(L.hi0);
+  R.lo = (int64_t*)at(L.lo);
+  R.t_old = (double*)at(L.t_old);
+  R.h = (double*)at(L.h);
+  R.y = (double*)at(L.y);
+  R.kb = (double*)at(L.kb);
+  R.yb = (double*)at(L.yb);
+  float* k = (float*)at(L.k);
+  float* wfwd = (float*)at(L.wfwd);
+  float* wadj = (float*)at(L.wadj);
+  cudaError_t e;
+  int64_t nl = 0;
+  const unsigned gb = (unsigned)((n * kD + 255) / 256 < sms * 16 ? (n * kD + 255) / 256 : sms * 16);
+  // weights: the forward's pre-split chunks and the adjoint's (W2^T | W1^T)
+  transpose_kernel<<<sms, 256, 0, st>>>(A.W1, (int)H, kD, (float*)at(L.w1t));  // (64, H)
+  transpose_kernel<<<sms, 256, 0, st>>>(A.W2, kD, (int)H, (float*)at(L.w2t));  // (H, 64)
+  if ((e = mlp_tc_prep(A.W1, A.W2, H, wfwd, st)) != cudaSuccess) return e;
+  if ((e = mlp_tc_prep((float*)at(L.w2t), (float*)at(L.w1t), H, wadj, st)) != cudaSuccess) return e;
+  nl += 4;
+  // rows longest trajectory first (stable: ties by index)
+  keys_kernel<<<gb, 256, 0, st>>>(A.traj_offsets, n, (int32_t*)at(L.keys_in), (int32_t*)at(L.idx_in));
+  size_t cb = L.cub_bytes;
+  e = cub::DeviceRadixSort::SortPairsDescending(at(L.cub), cb, (const int32_t*)at(L.keys_in),
+                                                (int32_t*)at(L.keys), (const int32_t*)at(L.idx_in),
+                                                (int32_t*)at(L.order), (int)n, 0, 32, st);
+  if (e != cudaSuccess) return e;
+  nl += 1 + 4;  // keys + the radix sort passes (approximate)
+  int32_t maxn = 0;
+  if ((e = cudaMemcpyAsync(&maxn, at(L.keys), 4, cudaMemcpyDeviceToHost, st)) != cudaSuccess) return e;
+  if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return e;
+  init_kernel<<<gb, 256, 0, st>>>(R, A.n_emitted);
+  if ((e = cudaMemsetAsync(at(L.part), 0, 4 * (size_t)sms * kPartFloats, st)) != cudaSuccess) return e;
+  nl += 1;
+
+  static bool attr = false;
+  const size_t vjp_smem = sizeof(VjpSmem) + 1024, wg_smem = sizeof(WgSmem) + 1024;
+  if (!attr) {
+    if ((e = cudaFuncSetAttribute(vjp_kernel<BODE_METHOD_DOPRI5>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)vjp_smem)) != cudaSuccess) return e;
+    if ((e = cudaFuncSetAttribute(vjp_kernel<BODE_METHOD_TSIT5>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)vjp_smem)) != cudaSuccess) return e;
+    if ((e = cudaFuncSetAttribute(vjp_kernel<BODE_METHOD_HEUN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)vjp_smem)) != cudaSuccess) return e;
+    if ((e = cudaFuncSetAttribute(wg_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wg_smem)) != cudaSuccess) return e;
+    attr = true;
+  }
+  const int max_tiles = (int)((n + kRows - 1) / kRows);
+  const int grid = max_tiles < sms ? max_tiles : sms;
+  VjpArgs V{n, pmax, (int)H, 0, R.count, R.y, k, (const float*)at(L.Ybuf), R.h, R.kb, (float*)at(L.Ybar), wfwd, wadj, A.b1,
+            (float*)at(L.uT), (float*)at(L.AT), (float*)at(L.YT), (float*)at(L.gT)};
+  WgArgs G{(int)H, S, pmax, (int64_t)S * pmax, R.count, V.uT, V.AT, V.YT, V.gT, (float*)at(L.part)};
+  for (int64_t it = 0; it < maxn; it++) {
+    count_kernel<<<1, 1, 0, st>>>(R, it);
+    load_kernel<<<gb, 256, 0, st>>>(R, A.traj, A.traj_offsets, it);
+    // forward recompute of k_0 .. k_{S-2} (the inputs of every stage), the
+    // forward's own MMAs
+    for (int s = 0; s + 1 < S; s++) {
+      MlpTcArgs t{n, (int)H, s, R.y, k, R.h, nullptr, R.count, nullptr, wfwd, A.b1, A.b2,
+                  k + (size_t)s * n * kD, (float*)at(L.Ybuf) + (size_t)s * n * kD};
+      if ((e = mlp_tc_launch<M>(t, max_tiles, st)) != cudaSuccess) return e;
+    }
+    seeds_kernel<M><<<gb, 256, 0, st>>>(R, A.t_eval, A.t_eval_offsets, A.t_eval_len, A.grad_ys);
+    for (int s = S - 1; s >= 0; s--) {
+      V.stage = s;
+      vjp_kernel<M><<<grid, 256, vjp_smem, st>>>(V);
+    }
+    fold_kernel<M><<<gb, 256, 0, st>>>(R, (const float*)at(L.Ybar));
+    wg_kernel<<<sms, 256, wg_smem, st>>>(G);
+    nl += 5 + 2 * S - 1;
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  }
+  finish_kernel<<<gb, 256, 0, st>>>(R, A.grad_ys, A.t_eval_offsets, A.t_eval_len, A.grad_y0);
+  wg_reduce_kernel<<<64, 256, 0, st>>>((const float*)at(L.part), sms, (int)H, A.gW1, A.gb1, A.gW2, A.gb2);
+  nl += 2;
+  *launches += nl;
+  return cudaGetLastError();
+}
+
+}  // namespace adjtc
+
+#ifdef BODE_ADJ_PROF
+extern "C" int bode_debug_adj_prof(long long* out) {
+  cudaMemcpyFromSymbol(out, adjtc::g_adj_prof, sizeof(adjtc::g_adj_prof));
+  int n[2];
+  cudaMemcpyFromSymbol(n, adjtc::g_adj_prof_n, sizeof(n));
+  return n[0] * 1000 + n[1];
+}
+#endif
+
+bool mlp_adjoint_tc_supported(int64_t d, int64_t H) {
+  return d == tc::kD && H % tc::kHc == 0 && H >= 32 && H <= 256;
+}
+
+size_t mlp_adjoint_tc_bytes(int64_t n, int64_t H, int method) {
+  const int S = method == BODE_METHOD_HEUN ? Tab<BODE_METHOD_HEUN>::S
+              : method == BODE_METHOD_TSIT5 ? Tab<BODE_METHOD_TSIT5>::S
+                                            : Tab<BODE_METHOD_DOPRI5>::S;
+  return adjtc::Layout(n, H, S, adjtc::sm_count()).total;
+}
+
+cudaError_t mlp_adjoint_tc_run(int method, AdjParams A, void* ws, cudaStream_t st, int64_t* launches) {
+  switch (method) {
+    case BODE_METHOD_DOPRI5: return adjtc::run<BODE_METHOD_DOPRI5>(A, (char*)ws, st, launches);
+    case BODE_METHOD_TSIT5: return adjtc::run<BODE_METHOD_TSIT5>(A, (char*)ws, st, launches);
+    default: return adjtc::run<BODE_METHOD_HEUN>(A, (char*)ws, st, launches);
+  }
+}
+
+}  // namespace bode

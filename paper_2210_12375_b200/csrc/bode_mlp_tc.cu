@@ -128,6 +128,8 @@ __device__ __forceinline__ void produce_tile(const MlpTcArgs& A, int tile, int c
         }
       }
     }
+    if (A.Yout && lv)
+      *reinterpret_cast<float4*>(A.Yout + (size_t)ir * kD + 4 * q) = make_float4(x[0], x[1], x[2], x[3]);
     float4 hi, lo;
     hi.x = tf32_hi(x[0]), hi.y = tf32_hi(x[1]), hi.z = tf32_hi(x[2]), hi.w = tf32_hi(x[3]);
     lo.x = x[0] - hi.x, lo.y = x[1] - hi.y, lo.z = x[2] - hi.z, lo.w = x[3] - hi.w;

@@ -165,23 +165,27 @@ def _mlp_weights(D, H, seed=3):
     return W1, b1, W2, b2
 
 
-@pytest.mark.parametrize("D,H,method", [(4, 32, "dopri5"), (8, 64, "tsit5"), (16, 48, "heun"),
-                                        (64, 256, "dopri5")])
-def test_mlp_adjoint_matches_autograd_oracle(D, H, method):
+@pytest.mark.parametrize("D,H,method,n", [(4, 32, "dopri5", 12), (8, 64, "tsit5", 12),
+                                          (16, 48, "heun", 12), (64, 256, "dopri5", 12),
+                                          (64, 256, "tsit5", 160), (64, 96, "dopri5", 140),
+                                          (64, 128, "heun", 130)])
+def test_mlp_adjoint_matches_autograd_oracle(D, H, method, n):
     """Neural-ODE gradients (dL/dy0 and the batch-summed dL/dW1, db1, dW2,
     db2) against torch autograd through the fp32-MLP replay of the GPU's own
     accepted steps (fp32 dynamics: tolerance 2e-4 of each gradient's scale).
-    At D=64, H=256 the solve runs the fused tcgen05 kernel and the recording
-    pass the bit-identical lockstep tensor-core path."""
+    At D=64 the solve and its recording run the fused tcgen05 kernel and the
+    backward runs on the tensor cores (bode_mlp_adjoint_tc.cu): n > 128 spans
+    several 128-row tiles, a partial last tile, trajectories of different
+    lengths (y0 scales vary), and H not a multiple of 128."""
     import torch
 
     import paper_2210_12375_b200 as bode
 
     dev = torch.device("cuda:0")
     W = _mlp_weights(D, H)
-    n, m = 12, 6
+    m = 6
     rng = np.random.default_rng(4)
-    y0 = rng.normal(size=(n, D))
+    y0 = rng.normal(size=(n, D)) * rng.uniform(0.2, 3.0, size=(n, 1))
     te = np.linspace(0.0, 1.0, m)
     dyn = bode.mlp_dynamics(*[torch.tensor(w, device=dev) for w in W])
     kw = dict(t_eval=torch.tensor(te, device=dev), method=method, atol=1e-6, rtol=1e-6,
