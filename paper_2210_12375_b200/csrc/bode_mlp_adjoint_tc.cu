@@ -196,8 +196,9 @@ __global__ void finish_kernel(RowState R, const double* grad_ys, const int64_t* 
   }
 }
 
-// -DBODE_ADJ_PROF (debug builds): per-phase clock64 stamps of CTA 0's first
-// tiles, threads 0 (MMA issue) and 128 (producer), read by bode_debug_adj_prof
+// -DBODE_ADJ_PROF (debug builds): per-phase clock64 stamps of CTA 0 in the
+// stage-3 launch, lane 0 of warp 0 (a row owner) and of warp 8 (MMA issue),
+// read by bode_debug_adj_prof
 #ifdef BODE_ADJ_PROF
 __device__ long long g_adj_prof[2][512];
 __device__ int g_adj_prof_n[2];
@@ -228,7 +229,7 @@ struct VjpArgs {
   const float* wfwd;  // forward chunks [W1_c | W2_c] (hi | lo each)
   const float* wadj;  // adjoint chunks [(W2^T)_c | (W1^T)_c]
   const float* b1;
-  float *uT, *AT, *YT, *gT;  // (rows, S * pmax), column = stage * pmax + row
+  float *uT, *AT, *YT, *gT;  // blocked (rows, S * pmax), column = stage * pmax + row
 };
 
 // Y_s / g_s tiles in shared memory; the weights of two hidden chunks in
@@ -241,80 +242,75 @@ struct VjpSmem {
   uint8_t wv[2][2][kW1];     // [buf] (W2^T)_c hi, lo
   uint8_t wy[2][2][kW2];     // [buf] (W1^T)_c hi, lo
   float b1[256];
-  uint64_t full, empty, wa[2], wy_full[2], g1[2], g2[2];
+  uint64_t full, wa[2], wy_full[2], g1[2], g2[2], epi[2];
   uint32_t tmem_base;
 };
 
-// Producer thread r owns tile row r.  vjp_stage_input forms the row's
-// stage input Y_s exactly as the forward did (bode_mlp_tc.cu: fp64 sum in
-// the reference order, rounded to fp32) into registers and writes its
-// transpose (a warp writes 128 contiguous bytes per column); it runs for the
-// NEXT tile while the consumer still works on this one.  vjp_store_tiles
-// then writes Y_s and g_s as TF32 hi/lo core matrices.
+constexpr int kVjpThreads = 288;  // 2 row-owner warpgroups + the MMA warp
+__device__ __forceinline__ void rows_sync() {  // the 256 row-owner threads
+  asm volatile("bar.sync 1, 256;" ::: "memory");
+}
+
+// Production of one tile row's half (columns [32 h, 32 h + 32)) of the
+// stage input Y_s and of g_s = dL/dk_s, into the shared-memory TF32 hi/lo
+// tiles and the transposed global copies.  Y_s is the forward recompute's
+// (stages < S-1), or formed here exactly as the forward did (bode_mlp_tc.cu:
+// fp64 sum in the reference order, rounded to fp32); g_s is the seed plus,
+// in the order the stages were reversed (S-1 down to s+1), h a_s's dL/dY_s'.
 template <int M>
-__device__ __forceinline__ void vjp_stage_input(const VjpArgs& A, int64_t p, bool lv, float* x) {
+__device__ __forceinline__ void vjp_produce(const VjpArgs& A, int64_t p, bool lv, int r, int h,
+                                            VjpSmem& S) {
   using T = Tab<M>;
   const int stage = A.stage;
   const int64_t col = (int64_t)stage * A.pmax + p;
+  const int c0 = 32 * h;
+  float x[32], g[32];
+  if (!lv) {
 #pragma unroll
-  for (int g8 = 0; g8 < kD / 8; g8++) {  // 8 columns at a time: every load in flight
-    double yv[8];
-    float kv[T::S][8];
-    if (lv) {
-      const double2* yp = reinterpret_cast<const double2*>(A.y + p * kD + 8 * g8);
+    for (int e = 0; e < 32; e++) x[e] = g[e] = 0.0f;
+  } else {
+    if (stage == T::S - 1) {
+      const double hr = A.h[p];
 #pragma unroll
-      for (int e = 0; e < 4; e++) {
-        const double2 d = __ldg(yp + e);
-        yv[2 * e] = d.x, yv[2 * e + 1] = d.y;
-      }
+      for (int g8 = 0; g8 < 4; g8++) {  // 8 columns at a time: every load in flight
+        const int cc = c0 + 8 * g8;
+        double yv[8];
+        float kv[T::S][8];
+        const double2* yp = reinterpret_cast<const double2*>(A.y + p * kD + cc);
 #pragma unroll
-      for (int j = 0; j < T::S; j++)
-        if (j < stage) {
-          const float4* kp = reinterpret_cast<const float4*>(A.k + ((int64_t)j * A.n + p) * kD + 8 * g8);
+        for (int e = 0; e < 4; e++) {
+          const double2 d = __ldg(yp + e);
+          yv[2 * e] = d.x, yv[2 * e + 1] = d.y;
+        }
+#pragma unroll
+        for (int j = 0; j < T::S - 1; j++) {
+          const float4* kp = reinterpret_cast<const float4*>(A.k + ((int64_t)j * A.n + p) * kD + cc);
           const float4 k0 = __ldg(kp), k1 = __ldg(kp + 1);
           kv[j][0] = k0.x, kv[j][1] = k0.y, kv[j][2] = k0.z, kv[j][3] = k0.w;
           kv[j][4] = k1.x, kv[j][5] = k1.y, kv[j][6] = k1.z, kv[j][7] = k1.w;
         }
-      const double hr = A.h[p];
 #pragma unroll
-      for (int e = 0; e < 8; e++) {
-        if (stage == 0) {
-          x[8 * g8 + e] = (float)yv[e];
-        } else {
-          double s = 0.0;
+        for (int e = 0; e < 8; e++) {
+          double sum = ExactOps::mul(T::a(stage, 0), (double)kv[0][e]);
 #pragma unroll
-          for (int j = 0; j < T::S; j++) {
-            if (j >= stage) break;
-            s = j == 0 ? ExactOps::mul(T::a(stage, 0), (double)kv[0][e])
-                       : ExactOps::mad(T::a(stage, j), (double)kv[j][e], s);
-          }
-          x[8 * g8 + e] = (float)ExactOps::mad(hr, s, yv[e]);
+          for (int j = 1; j < T::S - 1; j++) sum = ExactOps::mad(T::a(stage, j), (double)kv[j][e], sum);
+          x[8 * g8 + e] = (float)ExactOps::mad(hr, sum, yv[e]);
         }
-        A.YT[blk(8 * g8 + e, col, kD)] = x[8 * g8 + e];
       }
     } else {
+      const float4* yp = reinterpret_cast<const float4*>(A.Ybuf + ((int64_t)stage * A.n + p) * kD + c0);
 #pragma unroll
-      for (int e = 0; e < 8; e++) x[8 * g8 + e] = 0.0f;
+      for (int e = 0; e < 8; e++) {
+        const float4 v = __ldg(yp + e);
+        x[4 * e] = v.x, x[4 * e + 1] = v.y, x[4 * e + 2] = v.z, x[4 * e + 3] = v.w;
+      }
     }
-  }
-}
-
-template <int M>
-__device__ __forceinline__ void vjp_store_tiles(const VjpArgs& A, int64_t p, bool lv, int r,
-                                                const float* x, VjpSmem& S) {
-  const int64_t col = (int64_t)A.stage * A.pmax + p;
-  // dL/dk_s = seed + sum over the later stages s' (in the order they were
-  // reversed, S-1 down to s+1) of h a_s's dL/dY_s'
-  using T = Tab<M>;
-  const int stage = A.stage;
-  const double* kp = A.kb + ((int64_t)stage * A.n + p) * kD;
-  const double hp = lv ? A.h[p] : 0.0;
-  float gall[kD];
+    const double hp = A.h[p];
+    const double* kp = A.kb + ((int64_t)stage * A.n + p) * kD + c0;
 #pragma unroll
-  for (int g8 = 0; g8 < kD / 8; g8++) {
-    double acc[8];
-    float yv[T::S][8];
-    if (lv) {
+    for (int g8 = 0; g8 < 4; g8++) {
+      double acc[8];
+      float yv[T::S][8];
 #pragma unroll
       for (int e = 0; e < 4; e++) {
         const double2 d = __ldg(reinterpret_cast<const double2*>(kp + 8 * g8) + e);
@@ -323,7 +319,7 @@ __device__ __forceinline__ void vjp_store_tiles(const VjpArgs& A, int64_t p, boo
 #pragma unroll
       for (int s2 = T::S - 1; s2 > 0; s2--) {
         if (s2 <= stage || T::za(s2, stage) == 0.0) continue;
-        const float4* yp = reinterpret_cast<const float4*>(A.Ybar + ((int64_t)s2 * A.n + p) * kD + 8 * g8);
+        const float4* yp = reinterpret_cast<const float4*>(A.Ybar + ((int64_t)s2 * A.n + p) * kD + c0 + 8 * g8);
         const float4 a = __ldg(yp), b = __ldg(yp + 1);
         yv[s2][0] = a.x, yv[s2][1] = a.y, yv[s2][2] = a.z, yv[s2][3] = a.w;
         yv[s2][4] = b.x, yv[s2][5] = b.y, yv[s2][6] = b.z, yv[s2][7] = b.w;
@@ -335,63 +331,57 @@ __device__ __forceinline__ void vjp_store_tiles(const VjpArgs& A, int64_t p, boo
 #pragma unroll
         for (int e = 0; e < 8; e++) acc[e] = fma(w, (double)yv[s2][e], acc[e]);
       }
-    } else {
 #pragma unroll
-      for (int e = 0; e < 8; e++) acc[e] = 0.0;
+      for (int e = 0; e < 8; e++) g[8 * g8 + e] = (float)acc[e];
     }
 #pragma unroll
-    for (int e = 0; e < 8; e++) gall[8 * g8 + e] = (float)acc[e];
+    for (int e = 0; e < 32; e++) {
+      A.YT[blk(c0 + e, col, kD)] = x[e];
+      A.gT[blk(c0 + e, col, kD)] = g[e];
+    }
   }
 #pragma unroll
-  for (int q8 = 0; q8 < kD / 8; q8++) {
-    float gv[8];
-#pragma unroll
-    for (int e = 0; e < 8; e++) gv[e] = gall[8 * q8 + e];
-    if (lv) {
-#pragma unroll
-      for (int e = 0; e < 8; e++) A.gT[blk(8 * q8 + e, col, kD)] = gv[e];
-    } else {
-#pragma unroll
-      for (int e = 0; e < 8; e++) gv[e] = 0.0f;
-    }
-#pragma unroll
-    for (int h4 = 0; h4 < 2; h4++) {
-      const int q = 2 * q8 + h4;  // 4-column chunk
-      const uint32_t o = cm_off(r, 4 * q, kD);
-      const float* xs = x + 4 * q;
-      const float* gs = gv + 4 * h4;
-      float4 hi, lo;
-      hi.x = tf32_hi(xs[0]), hi.y = tf32_hi(xs[1]), hi.z = tf32_hi(xs[2]), hi.w = tf32_hi(xs[3]);
-      lo.x = xs[0] - hi.x, lo.y = xs[1] - hi.y, lo.z = xs[2] - hi.z, lo.w = xs[3] - hi.w;
-      *reinterpret_cast<float4*>(S.ay[0] + o) = hi;
-      *reinterpret_cast<float4*>(S.ay[1] + o) = lo;
-      hi.x = tf32_hi(gs[0]), hi.y = tf32_hi(gs[1]), hi.z = tf32_hi(gs[2]), hi.w = tf32_hi(gs[3]);
-      lo.x = gs[0] - hi.x, lo.y = gs[1] - hi.y, lo.z = gs[2] - hi.z, lo.w = gs[3] - hi.w;
-      *reinterpret_cast<float4*>(S.ag[0] + o) = hi;
-      *reinterpret_cast<float4*>(S.ag[1] + o) = lo;
-    }
+  for (int q = 0; q < 8; q++) {
+    const uint32_t o = cm_off(r, c0 + 4 * q, kD);
+    const float* xs = x + 4 * q;
+    const float* gs = g + 4 * q;
+    float4 hi, lo;
+    hi.x = tf32_hi(xs[0]), hi.y = tf32_hi(xs[1]), hi.z = tf32_hi(xs[2]), hi.w = tf32_hi(xs[3]);
+    lo.x = xs[0] - hi.x, lo.y = xs[1] - hi.y, lo.z = xs[2] - hi.z, lo.w = xs[3] - hi.w;
+    *reinterpret_cast<float4*>(S.ay[0] + o) = hi;
+    *reinterpret_cast<float4*>(S.ay[1] + o) = lo;
+    hi.x = tf32_hi(gs[0]), hi.y = tf32_hi(gs[1]), hi.z = tf32_hi(gs[2]), hi.w = tf32_hi(gs[3]);
+    lo.x = gs[0] - hi.x, lo.y = gs[1] - hi.y, lo.z = gs[2] - hi.z, lo.w = gs[3] - hi.w;
+    *reinterpret_cast<float4*>(S.ag[0] + o) = hi;
+    *reinterpret_cast<float4*>(S.ag[1] + o) = lo;
   }
 }
 
+// One CTA per SM, tiles of 128 rows; warps 0-3 and 4-7 own the rows (thread
+// = row = TMEM lane) and split the columns of every production and
+// epilogue; warp 8 issues every MMA and weight copy.  Per hidden chunk c:
+// Z/V of chunk c+1 run on the tensor cores while the row owners do the
+// epilogue of chunk c, and Yb of chunk c after it.
 template <int M>
-__global__ void __launch_bounds__(256, 1) vjp_kernel(const VjpArgs A) {
-  using T = Tab<M>;
+__global__ void __launch_bounds__(kVjpThreads, 1) vjp_kernel(const VjpArgs A) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   VjpSmem& S = *reinterpret_cast<VjpSmem*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
-  const int tid = threadIdx.x, warp = tid >> 5;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int cnt = *A.count;
   const int ntiles = (cnt + kRows - 1) / kRows;
   if ((int)blockIdx.x >= ntiles) return;
   const int nchunk = A.H / kHc;
+  const int my_tiles = (ntiles - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;
+  const int total = my_tiles * nchunk;  // chunk sequence numbers q of this CTA
 
   if (tid == 0) {
     mbar_init(&S.full, 1);
-    mbar_init(&S.empty, 1);
     for (int b = 0; b < 2; b++) {
       mbar_init(&S.wa[b], 1);
       mbar_init(&S.wy_full[b], 1);
       mbar_init(&S.g1[b], 1);
       mbar_init(&S.g2[b], 1);
+      mbar_init(&S.epi[b], 1);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -404,184 +394,159 @@ __global__ void __launch_bounds__(256, 1) vjp_kernel(const VjpArgs A) {
   fence_before();
   __syncthreads();
   fence_after();
+  // TMEM columns: Z / V accumulators of chunk buffer b at 64 b / 64 b + 32,
+  // Yb at 128, u_c hi / lo of buffer b at 192 + 64 b / 192 + 64 b + 32
+  const uint32_t tmem = S.tmem_base;
+  const uint32_t accY = tmem + 128;
+  auto phase = [](int q) { return (uint32_t)((q >> 1) & 1); };
 
-  if (tid >= 128) {
-    // ============ producer: Y_s and g_s tiles (+ their transposes) ============
-    const int r = tid - 128;
-    float x[kD];
-    int kl = 0;
-    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, kl++) {
-      const int64_t p = (int64_t)tile * kRows + r;
-      const bool lv = p < cnt;
-      if (tid == 128) { ADJ_STAMP(1, 1) }
-      if (A.stage == T::S - 1) {
-        vjp_stage_input<M>(A, p, lv, x);  // overlaps the consumer's previous tile
-      } else {  // the forward recompute kept this stage's inputs
-        const float4* yp = reinterpret_cast<const float4*>(A.Ybuf + ((int64_t)A.stage * A.n + p) * kD);
-        float4 v[kD / 4];
+  if (warp == 8) {
+    // ======================= MMA issue (one lane) =======================
+    if (lane == 0) {
+      const char* wf = (const char*)A.wfwd;
+      const char* wa = (const char*)A.wadj;
+      auto load_wa = [&](int q) {  // W1_c and (W2^T)_c of chunk q into buffer q & 1
+        const int b = q & 1, c = q % nchunk;
+        mbar_expect_tx(&S.wa[b], 4 * kW1);
+        bulk_g2s(S.w1[b][0], wf + (size_t)c * kWChunk, kW1, &S.wa[b]);
+        bulk_g2s(S.w1[b][1], wf + (size_t)c * kWChunk + kW1, kW1, &S.wa[b]);
+        bulk_g2s(S.wv[b][0], wa + (size_t)c * kWChunk, kW1, &S.wa[b]);
+        bulk_g2s(S.wv[b][1], wa + (size_t)c * kWChunk + kW1, kW1, &S.wa[b]);
+      };
+      auto load_wy = [&](int q) {  // (W1^T)_c
+        const int b = q & 1, c = q % nchunk;
+        mbar_expect_tx(&S.wy_full[b], 2 * kW2);
+        bulk_g2s(S.wy[b][0], wa + (size_t)c * kWChunk + 2 * kW1, kW2, &S.wy_full[b]);
+        bulk_g2s(S.wy[b][1], wa + (size_t)c * kWChunk + 2 * kW1 + kW2, kW2, &S.wy_full[b]);
+      };
+      const int ta[3] = {0, 0, 1}, tb[3] = {0, 1, 0};
+      auto issue_zv = [&](int q) {  // Z = Y_s W1_c^T, V = g_s (W2^T)_c^T into buffer q & 1
+        const int b = q & 1;
+        mbar_wait(&S.wa[b], phase(q));
+        if (q >= 2) mbar_wait(&S.epi[b], phase(q - 2));  // epilogue(q-2) read this buffer
+        fence_after();
+        const uint32_t az = tmem + 64 * b, av = az + 32;
 #pragma unroll
-        for (int e = 0; e < kD / 4; e++) v[e] = lv ? __ldg(yp + e) : make_float4(0.0f, 0.0f, 0.0f, 0.0f);
-        const int64_t col = (int64_t)A.stage * A.pmax + p;
+        for (int s = 0; s < kD / 8; s++)
 #pragma unroll
-        for (int e = 0; e < kD / 4; e++) {
-          x[4 * e] = v[e].x, x[4 * e + 1] = v[e].y, x[4 * e + 2] = v[e].z, x[4 * e + 3] = v[e].w;
-          if (lv) {
-#pragma unroll
-            for (int f = 0; f < 4; f++) A.YT[blk(4 * e + f, col, kD)] = x[4 * e + f];
+          for (int term = 0; term < 3; term++) {
+            mma_tf32(az, smem_desc(smem_u32(S.ay[ta[term]]) + 256 * s, 2048),
+                     smem_desc(smem_u32(S.w1[b][tb[term]]) + 256 * s, 2048), idesc(kHc), (term | s) ? 1u : 0u);
+            mma_tf32(av, smem_desc(smem_u32(S.ag[ta[term]]) + 256 * s, 2048),
+                     smem_desc(smem_u32(S.wv[b][tb[term]]) + 256 * s, 2048), idesc(kHc), (term | s) ? 1u : 0u);
           }
-        }
-      }
-      if (tid == 128) { ADJ_STAMP(1, 2) }
-      if (kl >= 1) mbar_wait(&S.empty, (kl - 1) & 1);
-      if (tid == 128) { ADJ_STAMP(1, 3) }
-      vjp_store_tiles<M>(A, p, lv, r, x, S);
-      fence_async_smem();
-      group_sync(1);
-      if (tid == 128) { ADJ_STAMP(1, 4) }
-      if (tid == 128) mbar_arrive(&S.full);
-    }
-  } else {
-    // ================== consumer: MMAs + epilogues ==================
-    // TMEM columns: Z / V accumulators of chunk buffer b at 64 b / 64 b + 32,
-    // Yb at 128, u_c hi / lo of buffer b at 192 + 64 b / 192 + 64 b + 32
-    const uint32_t tmem = S.tmem_base;
-    const uint32_t lane_off = (uint32_t)(warp * 32) << 16;
-    const uint32_t accY = tmem + 128;
-    const char* wf = (const char*)A.wfwd;
-    const char* wa = (const char*)A.wadj;
-    const int my_tiles = (ntiles - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;
-    const int total = my_tiles * nchunk;  // chunk sequence numbers q of this CTA
-    auto load_wa = [&](int q) {  // W1_c and (W2^T)_c of chunk q into buffer q & 1
-      const int b = q & 1, c = q % nchunk;
-      mbar_expect_tx(&S.wa[b], 4 * kW1);
-      bulk_g2s(S.w1[b][0], wf + (size_t)c * kWChunk, kW1, &S.wa[b]);
-      bulk_g2s(S.w1[b][1], wf + (size_t)c * kWChunk + kW1, kW1, &S.wa[b]);
-      bulk_g2s(S.wv[b][0], wa + (size_t)c * kWChunk, kW1, &S.wa[b]);
-      bulk_g2s(S.wv[b][1], wa + (size_t)c * kWChunk + kW1, kW1, &S.wa[b]);
-    };
-    auto load_wy = [&](int q) {  // (W1^T)_c
-      const int b = q & 1, c = q % nchunk;
-      mbar_expect_tx(&S.wy_full[b], 2 * kW2);
-      bulk_g2s(S.wy[b][0], wa + (size_t)c * kWChunk + 2 * kW1, kW2, &S.wy_full[b]);
-      bulk_g2s(S.wy[b][1], wa + (size_t)c * kWChunk + 2 * kW1 + kW2, kW2, &S.wy_full[b]);
-    };
-    auto phase = [](int q) { return (uint32_t)((q >> 1) & 1); };
-    const int ta[3] = {0, 0, 1}, tb[3] = {0, 1, 0};
-    auto issue_zv = [&](int q) {  // Z = Y_s W1_c^T, V = g_s (W2^T)_c^T into buffer q & 1
-      const int b = q & 1;
-      mbar_wait(&S.wa[b], phase(q));
-      fence_after();
-      const uint32_t az = tmem + 64 * b, av = az + 32;
+        mma_commit(&S.g1[b]);
+      };
+      auto issue_yb = [&](int q, int c) {  // Yb += u_c (W1^T)_c^T (A from TMEM)
+        const int b = q & 1;
+        mbar_wait(&S.epi[b], phase(q));
+        mbar_wait(&S.wy_full[b], phase(q));
+        fence_after();
+        const uint32_t uhi = tmem + 192 + 64 * b, ulo = uhi + 32;
 #pragma unroll
-      for (int s = 0; s < kD / 8; s++)
-#pragma unroll
-        for (int term = 0; term < 3; term++) {
-          mma_tf32(az, smem_desc(smem_u32(S.ay[ta[term]]) + 256 * s, 2048),
-                   smem_desc(smem_u32(S.w1[b][tb[term]]) + 256 * s, 2048), idesc(kHc), (term | s) ? 1u : 0u);
-          mma_tf32(av, smem_desc(smem_u32(S.ag[ta[term]]) + 256 * s, 2048),
-                   smem_desc(smem_u32(S.wv[b][tb[term]]) + 256 * s, 2048), idesc(kHc), (term | s) ? 1u : 0u);
+        for (int s = 0; s < kHc / 8; s++) {
+          const uint64_t wh = smem_desc(smem_u32(S.wy[b][0]) + 256 * s, 1024);
+          const uint64_t wl = smem_desc(smem_u32(S.wy[b][1]) + 256 * s, 1024);
+          mma_tf32_ts(accY, uhi + 8 * s, wh, idesc(kD), (c | s) ? 1u : 0u);
+          mma_tf32_ts(accY, uhi + 8 * s, wl, idesc(kD), 1u);
+          mma_tf32_ts(accY, ulo + 8 * s, wh, idesc(kD), 1u);
         }
-      mma_commit(&S.g1[b]);
-    };
-    if (tid == 0) {
+        mma_commit(&S.g2[b]);
+      };
       load_wa(0);
       load_wy(0);
       if (total > 1) {
         load_wa(1);
         load_wy(1);
       }
-    }
-    int kl = 0;
-    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, kl++) {
-      if (tid == 0) { ADJ_STAMP(0, 10) }
-      mbar_wait(&S.full, kl & 1);
-      if (tid == 0) { ADJ_STAMP(0, 11) }
-      const int64_t p = (int64_t)tile * kRows + tid;
-      const bool live = p < cnt;
-      const int64_t col = (int64_t)A.stage * A.pmax + p;
-      const int q0 = kl * nchunk;
-      if (tid == 0) issue_zv(q0);
-      for (int c = 0; c < nchunk; c++) {
-        const int q = q0 + c, b = q & 1;
-        if (tid == 0) { ADJ_STAMP(0, 20) }
-        if (tid == 0) {
-          if (c + 1 < nchunk) issue_zv(q + 1);   // runs under this chunk's epilogue
-          else mma_commit(&S.empty);             // Y_s / g_s tiles free after these
-          if (q >= 1) {                          // Yb(q-1) done: its weight buffer is free
+      for (int kl = 0; kl < my_tiles; kl++) {
+        mbar_wait(&S.full, kl & 1);  // tiles produced; the previous tile's Yb read out
+        ADJ_STAMP(1, 10)
+        const int q0 = kl * nchunk;
+        issue_zv(q0);
+        for (int c = 0; c < nchunk; c++) {
+          const int q = q0 + c;
+          if (c + 1 < nchunk) issue_zv(q + 1);
+          ADJ_STAMP(1, 20)
+          // weights of chunk q+2 into buffer q & 1 once ZV(q) has read it
+          mbar_wait(&S.g1[q & 1], phase(q));
+          if (q + 2 < total) load_wa(q + 2);
+          issue_yb(q, c);
+          ADJ_STAMP(1, 21)
+          if (q >= 1) {  // Yb(q-1) done: its (W1^T) buffer takes chunk q+1
             mbar_wait(&S.g2[(q - 1) & 1], phase(q - 1));
-            if (q + 1 < total) load_wy(q + 1);
+            if (q + 1 < total && q >= 1) load_wy(q + 1);
           }
         }
-        if (tid == 0) { ADJ_STAMP(0, 21) }
+      }
+    }
+    __syncwarp();
+  } else {
+    // ============ row owners: production + epilogues (column half h) ============
+    const int h = warp >> 2, r = tid & 127;
+    const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
+    int kl = 0;
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, kl++) {
+      const int64_t p = (int64_t)tile * kRows + r;
+      const bool live = p < cnt;
+      const int64_t col = (int64_t)A.stage * A.pmax + p;
+      // (Y_s / g_s tiles free: every ZV of the previous tile was waited for
+      // by its last epilogue; the previous Yb was read out below)
+      if (tid == 0) { ADJ_STAMP(0, 1) }
+      vjp_produce<M>(A, p, live, r, h, S);
+      fence_async_smem();
+      rows_sync();
+      if (tid == 0) mbar_arrive(&S.full);
+      if (tid == 0) { ADJ_STAMP(0, 2) }
+      const int q0 = kl * nchunk;
+      for (int c = 0; c < nchunk; c++) {
+        const int q = q0 + c, b = q & 1;
         mbar_wait(&S.g1[b], phase(q));
+        if (q >= 2) mbar_wait(&S.g2[b], phase(q - 2));  // u buffer b free
         fence_after();
-        if (tid == 0) { ADJ_STAMP(0, 22) }
-        if (tid == 0 && q + 2 < total) load_wa(q + 2);
-        if (q >= 2) mbar_wait(&S.g2[b], phase(q - 2));  // u buffer b free (Yb(q-2) done)
-        // ---- epilogue: tanh, u = V (1 - tanh^2) -> TMEM (hi, lo); u^T, tanh^T
+        if (tid == 0) { ADJ_STAMP(0, 3) }
+        // ---- tanh, u = V (1 - tanh^2) -> TMEM (hi, lo); u^T, tanh^T
         {
-          float z[32], v[32];
-          tmem_ld32(tmem + 64 * b + lane_off, z);
-          tmem_ld32(tmem + 64 * b + 32 + lane_off, v);
-          float uh[32], ul[32];
-          const int c32 = (q % nchunk) * kHc;
+          float z[16], v[16], uh[16], ul[16];
+          tmem_ld16(tmem + 64 * b + 16 * h + lane_off, z);
+          tmem_ld16(tmem + 64 * b + 32 + 16 * h + lane_off, v);
+          const int c16 = (q % nchunk) * kHc + 16 * h;
 #pragma unroll
-          for (int j = 0; j < kHc; j++) {
-            const float a = tanhf(z[j] + S.b1[c32 + j]);
+          for (int j = 0; j < 16; j++) {
+            const float a = tanhf(z[j] + S.b1[c16 + j]);
             const float uu = v[j] * (1.0f - a * a);
             uh[j] = tf32_hi(uu);
             ul[j] = uu - uh[j];
             if (live) {
-              A.uT[blk(c32 + j, col, A.H)] = uu;
-              A.AT[blk(c32 + j, col, A.H)] = a;
+              A.uT[blk(c16 + j, col, A.H)] = uu;
+              A.AT[blk(c16 + j, col, A.H)] = a;
             }
           }
-          const uint32_t ub = tmem + 192 + 64 * b + lane_off;
+          const uint32_t ub = tmem + 192 + 64 * b + 16 * h + lane_off;
           tmem_st16(ub, uh);
-          tmem_st16(ub + 16, uh + 16);
           tmem_st16(ub + 32, ul);
-          tmem_st16(ub + 48, ul + 16);
           tmem_wait_st();
         }
-        if (tid == 0) { ADJ_STAMP(0, 23) }
         fence_before();
-        group_sync(2);
-        if (tid == 0) { ADJ_STAMP(0, 24) }
-        // ---- Yb += u_c (W1^T)_c^T  (A from TMEM, 3xTF32, K = 32 in 4 steps)
-        if (tid == 0) {
-          fence_after();
-          mbar_wait(&S.wy_full[b], phase(q));
-          const uint32_t uhi = tmem + 192 + 64 * b, ulo = uhi + 32;
-#pragma unroll
-          for (int s = 0; s < kHc / 8; s++) {
-            const uint64_t wh = smem_desc(smem_u32(S.wy[b][0]) + 256 * s, 1024);
-            const uint64_t wl = smem_desc(smem_u32(S.wy[b][1]) + 256 * s, 1024);
-            mma_tf32_ts(accY, uhi + 8 * s, wh, idesc(kD), (c | s) ? 1u : 0u);
-            mma_tf32_ts(accY, uhi + 8 * s, wl, idesc(kD), 1u);
-            mma_tf32_ts(accY, ulo + 8 * s, wh, idesc(kD), 1u);
-          }
-          mma_commit(&S.g2[b]);
-        }
+        rows_sync();
+        if (tid == 0) mbar_arrive(&S.epi[b]);
+        if (tid == 0) { ADJ_STAMP(0, 4) }
       }
-      // ---- dL/dY_s of the row: dL/dy_old += Yb, dL/dk_j += h a_sj Yb (j < s)
-      if (tid == 0) { ADJ_STAMP(0, 30) }
+      // ---- this row's dL/dY_s (columns 32 h .. 32 h + 31)
       mbar_wait(&S.g2[(q0 + nchunk - 1) & 1], phase(q0 + nchunk - 1));
       fence_after();
-      if (tid == 0) { ADJ_STAMP(0, 31) }
       {
-        float yb[kD];
-        tmem_ld32(accY + lane_off, yb);
-        tmem_ld32(accY + lane_off + 32, yb + 32);
+        float yb[32];
+        tmem_ld32(accY + lane_off + 32 * h, yb);
         if (live) {
-          float4* dst = reinterpret_cast<float4*>(A.Ybar + ((int64_t)A.stage * A.n + p) * kD);
+          float4* dst = reinterpret_cast<float4*>(A.Ybar + ((int64_t)A.stage * A.n + p) * kD + 32 * h);
 #pragma unroll
-          for (int e = 0; e < kD / 4; e++)
+          for (int e = 0; e < 8; e++)
             dst[e] = make_float4(yb[4 * e], yb[4 * e + 1], yb[4 * e + 2], yb[4 * e + 3]);
         }
       }
-      if (tid == 0) { ADJ_STAMP(0, 32) }
       fence_before();
-      group_sync(2);
+      if (tid == 0) { ADJ_STAMP(0, 5) }
     }
   }
   fence_before();
@@ -601,69 +566,72 @@ struct WgArgs {
   float* part;  // (grid, kPartFloats)
 };
 
+// K-slices of 16 columns in two shared-memory stages: the operands of slice
+// i+1 are converted into one stage while the MMAs of slice i read the other,
+// and the global loads of slice i+2 are in flight in registers meanwhile.
+constexpr int kWgK = 16;
+struct WgStage {
+  uint8_t au[2][2][128 * kWgK * 4];  // u^T halves [h][hi, lo]
+  uint8_t ag[2][64 * kWgK * 4];      // g^T [hi, lo]
+  uint8_t by[2][kN1 * kWgK * 4];     // [Y^T | 1] [hi, lo]
+  uint8_t ba[2][2][kN2 * kWgK * 4];  // [tanh^T half | 1 (half 0)] [h][hi, lo]
+};
 struct WgSmem {
-  uint8_t au[2][2][128 * 32 * 4];  // u^T halves [h][hi, lo]
-  uint8_t ag[2][64 * 32 * 4];      // g^T [hi, lo]
-  uint8_t by[2][kN1 * 32 * 4];     // [Y^T | 1] [hi, lo]
-  uint8_t ba[2][2][kN2 * 32 * 4];  // [tanh^T half | 1 (half 0)] [h][hi, lo]
-  uint64_t mb;
+  WgStage st[2];
+  uint64_t done[2];
   uint32_t tmem_base;
 };
 
-// One K-slice (32 columns) of the weight-gradient operands, held in
-// registers between its global loads and its shared-memory stores so the
-// loads of slice i+1 are in flight while the MMAs of slice i run.  A source
-// tile is rows [0, nrows) of a row-major (., ldt) fp32 matrix, columns
-// [c0, c0 + 32) with those >= cmax zeroed; rows >= nrows are zero and row
-// `ones` (if >= 0) is 1.0 (the bias column of the GEMM).
 struct WgTile {
   const float* src;   // the matrix (blocked layout); set to the slice's block per fetch
   int nrows, ones;
   int64_t rows;       // the matrix's row count (block stride)
   int64_t row0;       // first row of this tile
-  uint8_t *hi, *lo;
+  int off, lo_off;    // byte offsets of the hi and lo tiles inside a stage
 };
 template <int TROWS>
-constexpr int wg_vec() { return (TROWS * 8 + 255) / 256; }
+constexpr int wg_vec() { return (TROWS * (kWgK / 4) + 255) / 256; }
 
 template <int TROWS>
-__device__ __forceinline__ void wg_fetch(WgTile T, int64_t ldt, int64_t c0, int64_t cmax,
+__device__ __forceinline__ void wg_fetch(WgTile T, int64_t c0, int64_t cmax,
                                          float4 (&v)[wg_vec<TROWS>()]) {
-  T.src += ((c0 >> 5) * T.rows + T.row0) * 32;
+  T.src += ((c0 >> 5) * T.rows + T.row0) * 32 + (c0 & 31);
 #pragma unroll
   for (int q = 0; q < wg_vec<TROWS>(); q++) {
     const int e = threadIdx.x + 256 * q;
-    const int r = e >> 3, k4 = e & 7;
+    const int r = e / (kWgK / 4), k4 = e % (kWgK / 4);
     float4 x = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
-    if (e < TROWS * 8) {
-      if (r < T.nrows)  // (src: this slice's 32-column block, row-major)
+    if (e < TROWS * (kWgK / 4)) {
+      if (r < T.nrows)  // (src: this slice's half of a 32-column block, row-major)
         x = __ldg(reinterpret_cast<const float4*>(T.src + (int64_t)r * 32 + 4 * k4));
       else if (r == T.ones)
         x = make_float4(1.0f, 1.0f, 1.0f, 1.0f);
+    }
+    v[q] = x;  // (columns >= cmax are zeroed at the store: nothing here waits on the load)
+  }
+}
+
+// hi tile at st + off, lo tile one tile later
+template <int TROWS>
+__device__ __forceinline__ void wg_store(const WgTile& T, uint8_t* st, int64_t c0, int64_t cmax,
+                                         const float4 (&v)[wg_vec<TROWS>()]) {
+#pragma unroll
+  for (int q = 0; q < wg_vec<TROWS>(); q++) {
+    const int e = threadIdx.x + 256 * q;
+    if (e < TROWS * (kWgK / 4)) {
+      const int r = e / (kWgK / 4), k4 = e % (kWgK / 4);
+      float4 x = v[q];
       const int64_t c = c0 + 4 * k4;
       if (c >= cmax) x.x = 0.0f;
       if (c + 1 >= cmax) x.y = 0.0f;
       if (c + 2 >= cmax) x.z = 0.0f;
       if (c + 3 >= cmax) x.w = 0.0f;
-    }
-    v[q] = x;
-  }
-}
-
-template <int TROWS>
-__device__ __forceinline__ void wg_store(const WgTile& T, const float4 (&v)[wg_vec<TROWS>()]) {
-#pragma unroll
-  for (int q = 0; q < wg_vec<TROWS>(); q++) {
-    const int e = threadIdx.x + 256 * q;
-    if (e < TROWS * 8) {
-      const int r = e >> 3, k4 = e & 7;
-      const float4 x = v[q];
       float4 hi, lo;
       hi.x = tf32_hi(x.x), hi.y = tf32_hi(x.y), hi.z = tf32_hi(x.z), hi.w = tf32_hi(x.w);
       lo.x = x.x - hi.x, lo.y = x.y - hi.y, lo.z = x.z - hi.z, lo.w = x.w - hi.w;
-      const uint32_t o = cm_off(r, 4 * k4, 32);
-      *reinterpret_cast<float4*>(T.hi + o) = hi;
-      *reinterpret_cast<float4*>(T.lo + o) = lo;
+      const uint32_t o = cm_off(r, 4 * k4, kWgK);
+      *reinterpret_cast<float4*>(st + T.off + o) = hi;
+      *reinterpret_cast<float4*>(st + T.lo_off + o) = lo;
     }
   }
 }
@@ -677,26 +645,27 @@ struct WgRegs {
 struct WgTiles {
   WgTile u0, a0, u1, a1, g, y;
 };
-__device__ __forceinline__ void wg_fetch_all(const WgTiles& T, bool two, int64_t ldt, int64_t c0,
-                                             int64_t cmax, WgRegs& R) {
-  wg_fetch<128>(T.u0, ldt, c0, cmax, R.u0);
-  wg_fetch<kN2>(T.a0, ldt, c0, cmax, R.a0);
+__device__ __forceinline__ void wg_fetch_all(const WgTiles& T, bool two, int64_t c0, int64_t cmax,
+                                             WgRegs& R) {
+  wg_fetch<128>(T.u0, c0, cmax, R.u0);
+  wg_fetch<kN2>(T.a0, c0, cmax, R.a0);
   if (two) {
-    wg_fetch<128>(T.u1, ldt, c0, cmax, R.u1);
-    wg_fetch<128>(T.a1, ldt, c0, cmax, R.a1);
+    wg_fetch<128>(T.u1, c0, cmax, R.u1);
+    wg_fetch<128>(T.a1, c0, cmax, R.a1);
   }
-  wg_fetch<64>(T.g, ldt, c0, cmax, R.g);
-  wg_fetch<kN1>(T.y, ldt, c0, cmax, R.y);
+  wg_fetch<64>(T.g, c0, cmax, R.g);
+  wg_fetch<kN1>(T.y, c0, cmax, R.y);
 }
-__device__ __forceinline__ void wg_store_all(const WgTiles& T, bool two, const WgRegs& R) {
-  wg_store<128>(T.u0, R.u0);
-  wg_store<kN2>(T.a0, R.a0);
+__device__ __forceinline__ void wg_store_all(const WgTiles& T, bool two, uint8_t* st, int64_t c0,
+                                             int64_t cmax, const WgRegs& R) {
+  wg_store<128>(T.u0, st, c0, cmax, R.u0);
+  wg_store<kN2>(T.a0, st, c0, cmax, R.a0);
   if (two) {
-    wg_store<128>(T.u1, R.u1);
-    wg_store<128>(T.a1, R.a1);
+    wg_store<128>(T.u1, st, c0, cmax, R.u1);
+    wg_store<128>(T.a1, st, c0, cmax, R.a1);
   }
-  wg_store<64>(T.g, R.g);
-  wg_store<kN1>(T.y, R.y);
+  wg_store<64>(T.g, st, c0, cmax, R.g);
+  wg_store<kN1>(T.y, st, c0, cmax, R.y);
 }
 
 __global__ void __launch_bounds__(256, 1) wg_kernel(const WgArgs A) {
@@ -704,12 +673,13 @@ __global__ void __launch_bounds__(256, 1) wg_kernel(const WgArgs A) {
   WgSmem& S = *reinterpret_cast<WgSmem*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
   const int tid = threadIdx.x, warp = tid >> 5;
   const int cnt = *A.count;
-  const int per_stage = (cnt + 31) / 32;
+  const int per_stage = (cnt + kWgK - 1) / kWgK;
   const int nslices = A.S * per_stage;
   if ((int)blockIdx.x >= nslices) return;
   const int halves = A.H > 128 ? 2 : 1;
   if (tid == 0) {
-    mbar_init(&S.mb, 1);
+    mbar_init(&S.done[0], 1);
+    mbar_init(&S.done[1], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 0) {
@@ -723,15 +693,17 @@ __global__ void __launch_bounds__(256, 1) wg_kernel(const WgArgs A) {
   const uint32_t tmem = S.tmem_base;
   const int rows0 = A.H < 128 ? A.H : 128, rows1 = A.H - rows0;
   const bool two = halves == 2;
-  const WgTiles T{WgTile{A.uT, rows0, -1, A.H, 0, S.au[0][0], S.au[0][1]},
-                  WgTile{A.AT, rows0, 128, A.H, 0, S.ba[0][0], S.ba[0][1]},
-                  WgTile{A.uT, rows1, -1, A.H, 128, S.au[1][0], S.au[1][1]},
-                  WgTile{A.AT, rows1, -1, A.H, 128, S.ba[1][0], S.ba[1][1]},
-                  WgTile{A.gT, kD, -1, kD, 0, S.ag[0], S.ag[1]},
-                  WgTile{A.YT, kD, kD, kD, 0, S.by[0], S.by[1]}};
+  const WgStage& s0 = S.st[0];
+  auto off = [&](const void* p) { return (int)((const uint8_t*)p - (const uint8_t*)&s0); };
+  const WgTiles T{WgTile{A.uT, rows0, -1, A.H, 0, off(s0.au[0][0]), off(s0.au[0][1])},
+                  WgTile{A.AT, rows0, 128, A.H, 0, off(s0.ba[0][0]), off(s0.ba[0][1])},
+                  WgTile{A.uT, rows1, -1, A.H, 128, off(s0.au[1][0]), off(s0.au[1][1])},
+                  WgTile{A.AT, rows1, -1, A.H, 128, off(s0.ba[1][0]), off(s0.ba[1][1])},
+                  WgTile{A.gT, kD, -1, kD, 0, off(s0.ag[0]), off(s0.ag[1])},
+                  WgTile{A.YT, kD, kD, kD, 0, off(s0.by[0]), off(s0.by[1])}};
   auto slice_cols = [&](int sl, int64_t& c0, int64_t& cmax) {
     const int s = sl / per_stage;
-    c0 = (int64_t)s * A.pmax + (int64_t)(sl % per_stage) * 32;
+    c0 = (int64_t)s * A.pmax + (int64_t)(sl % per_stage) * kWgK;
     cmax = (int64_t)s * A.pmax + cnt;
   };
   // TMEM: dW1|db1 half h at columns 80 h (M = 128: row = hidden unit);
@@ -741,56 +713,70 @@ __global__ void __launch_bounds__(256, 1) wg_kernel(const WgArgs A) {
   {
     int64_t c0, cmax;
     slice_cols(blockIdx.x, c0, cmax);
-    wg_fetch_all(T, two, A.ldt, c0, cmax, R);
+    wg_fetch_all(T, two, c0, cmax, R);
   }
-  uint32_t ph = 0;
-  int done = 0;
-  for (int sl = blockIdx.x; sl < nslices; sl += gridDim.x, done++) {
-    wg_store_all(T, two, R);
+  int i = 0;
+  for (int sl = blockIdx.x; sl < nslices; sl += gridDim.x, i++) {
+    const int b = i & 1;
+    if (i >= 2) mbar_wait(&S.done[b], ((i - 2) >> 1) & 1);  // MMAs of slice i-2 read stage b
+    uint8_t* st = reinterpret_cast<uint8_t*>(&S.st[b]);
+    int64_t c0, cmax;
+    slice_cols(sl, c0, cmax);
+    wg_store_all(T, two, st, c0, cmax, R);
     fence_async_smem();
     fence_before();
     __syncthreads();
     if (tid == 0) {
       fence_after();
+      const WgStage& g = S.st[b];
       const int ta[3] = {0, 0, 1}, tb[3] = {0, 1, 0};
 #pragma unroll
-      for (int ks = 0; ks < 4; ks++)
+      for (int ks = 0; ks < kWgK / 8; ks++)
 #pragma unroll
         for (int term = 0; term < 3; term++) {
-          const uint32_t acc = (done | ks | term) ? 1u : 0u;
+          const uint32_t acc = (i | ks | term) ? 1u : 0u;
           for (int h = 0; h < halves; h++) {
-            mma_tf32(tmem + kN1 * h, smem_desc(smem_u32(S.au[h][ta[term]]) + 256 * ks, 1024),
-                     smem_desc(smem_u32(S.by[tb[term]]) + 256 * ks, 1024), idesc_mn(128, kN1), acc);
+            mma_tf32(tmem + kN1 * h, smem_desc(smem_u32(g.au[h][ta[term]]) + 256 * ks, 512),
+                     smem_desc(smem_u32(g.by[tb[term]]) + 256 * ks, 512), idesc_mn(128, kN1), acc);
             mma_tf32(tmem + 2 * kN1 + (h ? (16u << 16) : 0u),
-                     smem_desc(smem_u32(S.ag[ta[term]]) + 256 * ks, 1024),
-                     smem_desc(smem_u32(S.ba[h][tb[term]]) + 256 * ks, 1024),
+                     smem_desc(smem_u32(g.ag[ta[term]]) + 256 * ks, 512),
+                     smem_desc(smem_u32(g.ba[h][tb[term]]) + 256 * ks, 512),
                      idesc_mn(64, h ? 128 : kN2), acc);
           }
         }
-      mma_commit(&S.mb);
+      mma_commit(&S.done[b]);
     }
     if (sl + (int)gridDim.x < nslices) {  // next slice's loads overlap these MMAs
-      int64_t c0, cmax;
       slice_cols(sl + gridDim.x, c0, cmax);
-      wg_fetch_all(T, two, A.ldt, c0, cmax, R);
+      wg_fetch_all(T, two, c0, cmax, R);
     }
-    mbar_wait(&S.mb, ph);
-    ph ^= 1;
-    fence_after();
   }
+  if (i >= 1) mbar_wait(&S.done[(i - 1) & 1], ((i - 1) >> 1) & 1);  // the last slice's MMAs
+  fence_after();
   // add this CTA's sums to its partial (the same CTA index every iteration:
-  // a fixed summation order)
+  // a fixed summation order), 16 columns per batch of loads
   if (warp < 4) {
     float* part = A.part + (size_t)blockIdx.x * kPartFloats;
     const uint32_t lo = (uint32_t)(warp * 32) << 16;
     const int l = tid & 31;
-    float v[32];
+    auto add16 = [&](float* dst, uint32_t taddr, int width) {
+      float v[16];
+      tmem_ld16(taddr, v);
+      float4* d4 = reinterpret_cast<float4*>(dst);
+      float4 cur[4];
+#pragma unroll
+      for (int e = 0; e < 4; e++) cur[e] = d4[e];
+#pragma unroll
+      for (int e = 0; e < 4; e++) {
+        if (4 * e < width) {
+          cur[e].x += v[4 * e], cur[e].y += v[4 * e + 1], cur[e].z += v[4 * e + 2], cur[e].w += v[4 * e + 3];
+          d4[e] = cur[e];
+        }
+      }
+    };
     for (int h = 0; h < halves; h++) {
       float* dst = part + (size_t)h * 128 * kN1 + (size_t)tid * kN1;  // row = hidden 128 h + tid
-      for (int c = 0; c < kN1; c += 16) {
-        tmem_ld16(tmem + kN1 * h + lo + c, v);
-        for (int j = 0; j < 16; j++) dst[c + j] += v[j];
-      }
+      for (int c = 0; c < kN1; c += 16) add16(dst + c, tmem + kN1 * h + lo + c, 16);
     }
     // M = 64 accumulators: lane l < 16 of quadrant w holds output 16 w + l
     // of half 0, lane 16 + l the same output of half 1
@@ -798,10 +784,8 @@ __global__ void __launch_bounds__(256, 1) wg_kernel(const WgArgs A) {
     const int width = hh ? 128 : kN2;
     float* dst = part + (size_t)2 * 128 * kN1 + ((size_t)hh * 64 + o) * kN2;
     for (int c = 0; c < kN2; c += 16) {
-      tmem_ld16(tmem + 2 * kN1 + lo + c, v);
-      if (hh < halves)
-        for (int j = 0; j < 16; j++)
-          if (c + j < width) dst[c + j] += v[j];
+      const int w = hh < halves ? (width - c < 16 ? width - c : 16) : 0;
+      add16(dst + c, tmem + 2 * kN1 + lo + c, w);
     }
   }
   fence_before();
@@ -958,7 +942,7 @@ cudaError_t run(AdjParams A, char* ws, cudaStream_t st, int64_t* launches) {
     seeds_kernel<M><<<gb, 256, 0, st>>>(R, A.t_eval, A.t_eval_offsets, A.t_eval_len, A.grad_ys);
     for (int s = S - 1; s >= 0; s--) {
       V.stage = s;
-      vjp_kernel<M><<<grid, 256, vjp_smem, st>>>(V);
+      vjp_kernel<M><<<grid, kVjpThreads, vjp_smem, st>>>(V);
     }
     fold_kernel<M><<<gb, 256, 0, st>>>(R, (const float*)at(L.Ybar));
     wg_kernel<<<sms, 256, wg_smem, st>>>(G);
