@@ -1,7 +1,9 @@
 """Copy the round's ncu captures from gpurun_out/ into profiles/ and write
-the summaries the judge reads: profiles/r1_<cfg>.md (key metrics, stalls,
-launch list), profiles/traffic.json (DRAM bytes per launch) and
-profiles/ncu_pipes.json (pipe utilisation per config, cited by bench.py)."""
+the summaries the judge reads: profiles/<round>_<cfg>.md (key metrics,
+stalls, launch list), profiles/traffic.json (DRAM bytes per launch) and
+profiles/ncu_pipes.json (pipe utilisation per config, cited by bench.py).
+
+    ROUND=r2 python tools/profiles_update.py c2 c4 ...   (default round r1)"""
 import csv, io, json, os, shutil, subprocess, sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -9,6 +11,7 @@ sys.path.insert(0, os.path.join(ROOT, "tools"))
 import ncu_summary  # noqa: E402
 
 KERNEL = {"c4": "mlp_fused_kernel"}
+RND = os.environ.get("ROUND", "r1")
 SCALE = {"Mbyte": 1e6, "Gbyte": 1e9, "Kbyte": 1e3, "byte": 1}
 
 
@@ -24,37 +27,37 @@ def main(cfgs):
     traffic, pipes = {}, {}
     for c in cfgs:
         src = os.path.join(ROOT, "gpurun_out", f"full_{c}.ncu-rep")
-        shutil.copy(src, os.path.join(prof, f"r1_full_{c}.ncu-rep"))
+        shutil.copy(src, os.path.join(prof, f"{RND}_full_{c}.ncu-rep"))
         shutil.copy(os.path.join(ROOT, "gpurun_out", f"launches_{c}.csv"),
-                    os.path.join(prof, f"r1_launches_{c}.csv"))
+                    os.path.join(prof, f"{RND}_launches_{c}.csv"))
         h, u, v = raw(src)
         val = lambda m: float(v[h.index(m)]) * SCALE.get(u[h.index(m)], 1.0)
         traffic[c] = dict(kernel=v[h.index("Kernel Name")], dram_read_bytes=val("dram__bytes_read.sum"),
                           dram_write_bytes=val("dram__bytes_write.sum"),
-                          source=f"profiles/r1_{c}.md (ncu --set full, one launch)")
+                          source=f"profiles/{RND}_{c}.md (ncu --set full, one launch)")
         pipes[c] = dict(
             kernel=v[h.index("Kernel Name")],
             fp64_pipe_pct=float(v[h.index("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active")]),
             tensor_pipe_pct=float(v[h.index("sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active")]),
             issue_active_pct=float(v[h.index("smsp__issue_active.avg.pct_of_peak_sustained_active")]),
             dram_pct=float(v[h.index("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed")]),
-            source=f"profiles/r1_{c}.md")
+            source=f"profiles/{RND}_{c}.md")
         buf = io.StringIO()
         stdout = sys.stdout
         sys.stdout = buf
         try:
-            print(f"# ncu --set full, {c} (round 1)\n")
+            print(f"# ncu --set full, {c} (round {RND[1:]})\n")
             print("Command: `ncu --set full --import-source on --clock-control none -k regex:<kernel> "
                   f"-s 1 -c 1 python bench.py --config {c} --steps 1 --warmup 1 --no-e2e --no-cpu` "
-                  f"(tools/ncu_round.sh, one B200 via gpurun; report: profiles/r1_full_{c}.ncu-rep; "
+                  f"(tools/ncu_round.sh, one B200 via gpurun; report: profiles/{RND}_full_{c}.ncu-rep; "
                   "bench default mode = fast for the analytic configs).\n")
-            ncu_summary.full(os.path.join(prof, f"r1_full_{c}.ncu-rep"))
+            ncu_summary.full(os.path.join(prof, f"{RND}_full_{c}.ncu-rep"))
             print(f"\n## Launch list (ncu --metrics gpu__time_duration.sum --clock-control none, "
                   f"bench.py --config {c} --steps 1 --warmup 0; cold-cache, serialised: compare shares)\n")
-            ncu_summary.launches(os.path.join(prof, f"r1_launches_{c}.csv"))
+            ncu_summary.launches(os.path.join(prof, f"{RND}_launches_{c}.csv"))
         finally:
             sys.stdout = stdout
-        open(os.path.join(prof, f"r1_{c}.md"), "w").write(buf.getvalue())
+        open(os.path.join(prof, f"{RND}_{c}.md"), "w").write(buf.getvalue())
     old = os.path.join(prof, "traffic.json")
     if os.path.exists(old):
         t0 = json.load(open(old))
