@@ -44,7 +44,7 @@
 extern "C" {
 #endif
 
-#define BODE_ABI_VERSION 5
+#define BODE_ABI_VERSION 6
 
 /* return codes */
 #define BODE_OK 0
@@ -209,12 +209,11 @@ typedef struct bode_solve_args {
    * OR over shards of map[j]} (FSAL), 1 + S * max_j otherwise. */
   int64_t* max_iterations_out;
   uint8_t* refresh_map_out;
-  /* MLP dynamics only: BODE_MLP_AUTO (= FUSED when d == 64 and hidden is a
-   * multiple of 32 up to 256), BODE_MLP_FUSED (one persistent tcgen05
-   * kernel per solve: stage vectors in TMEM, rows refilled from a queue),
-   * BODE_MLP_CUDA_CORE (lockstep, fp32 FMA) or BODE_MLP_TCGEN05 (lockstep,
-   * per-stage 3xTF32 tcgen05.mma kernels, fp32 accumulation in TMEM) */
-  int32_t mlp_backend;
+  /* reserved, must be 0.  (MLP dynamics run one path per shape: d == 64
+   * with hidden a multiple of 32 up to 256 -> the fused persistent tcgen05
+   * integrator; d == 64 with a wider hidden layer -> the per-stage tcgen05
+   * kernels; other d -> fp32 FMA kernels.  There is no backend switch.) */
+  int32_t reserved_mlp;
   int32_t _pad3;
   /* optional cudaEvent_t pair recorded on `stream` immediately before and
    * after the persistent integrator launch (roofline timing in bench.py) */
@@ -235,6 +234,13 @@ typedef struct bode_solve_args {
   /* run-time program (bode_program_create) for a BODE_METHOD_CUSTOM tableau
    * and/or BODE_DYN_PROGRAM dynamics; NULL for the built-in kernels */
   const struct bode_program* program;
+  /* MLP dynamics with d == 64 (the fused tcgen05 integrator), with traj:
+   * the fp32 stage inputs Y_s of every recorded step, row r of traj owning
+   * (S, 64) floats at traj_stages + r * S * 64 (slot s for s >= 1 when the
+   * tableau is FSAL -- Y_0 is y_old --, every slot otherwise).  Required by
+   * bode_solve_adjoint for such dynamics (its backward runs on the tensor
+   * cores and does not recompute the forward stages). */
+  float* traj_stages;
 } bode_solve_args;
 
 #define BODE_TRAJ_EXTRA 3
@@ -264,12 +270,10 @@ typedef struct bode_adjoint_args {
   float* grad_b1;
   float* grad_W2;
   float* grad_b2;
+  /* MLP dynamics with d == 64: fwd->traj_stages of the recording solve */
+  const float* traj_stages;
 } bode_adjoint_args;
 
-#define BODE_MLP_AUTO 0
-#define BODE_MLP_CUDA_CORE 1
-#define BODE_MLP_TCGEN05 2
-#define BODE_MLP_FUSED 3
 
 /* A ButcherTableau by value (tableau.py:17-57) for the unit ops of the
  * stepping API: row-major a (stride BODE_TABLEAU_MAX_STAGES), interp row i

@@ -64,11 +64,11 @@ class Args(C.Structure):
                 ("blocks", C.c_int32), ("cost_hint", C.c_void_p),
                 ("pipeline_chunks", C.c_int32), ("_pad2", C.c_int32),
                 ("max_iterations_out", C.c_void_p), ("refresh_map_out", C.c_void_p),
-                ("mlp_backend", C.c_int32), ("_pad3", C.c_int32),
+                ("reserved_mlp", C.c_int32), ("_pad3", C.c_int32),
                 ("prof_event_start", C.c_void_p), ("prof_event_stop", C.c_void_p),
                 ("launch_count_out", C.c_void_p),
                 ("traj", C.c_void_p), ("traj_offsets", C.c_void_p),
-                ("program", C.c_void_p)]
+                ("program", C.c_void_p), ("traj_stages", C.c_void_p)]
 
 
 _lib = None

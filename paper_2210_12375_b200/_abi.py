@@ -12,8 +12,21 @@ import os
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("BODE_LIB") or os.path.join(HERE, "_build", "libbode.so")
 
-ABI_VERSION = 5
+ABI_VERSION = 6
 TRAJ_EXTRA = 3
+
+
+def mlp_stage_record(a) -> int:
+    """Stages per recorded step of the fp32 stage-input record the
+    tensor-core MLP backward needs (bode_solve_args.traj_stages): the fused
+    integrator's shapes (d == 64, hidden a multiple of 32 up to 256), built-in
+    tableaus; 0 otherwise."""
+    if a.dyn.kind != DYN["mlp"] or a.d != 64 or a.program:
+        return 0
+    h = a.dyn.hidden
+    if h % 32 or not 32 <= h <= 256:
+        return 0
+    return STAGES.get(a.method, 0)
 
 
 def traj_stride(d: int) -> int:
@@ -22,6 +35,7 @@ def traj_stride(d: int) -> int:
 OK, EINVAL, ECUDA, EUNSUPPORTED = 0, 1, 2, 3
 METHOD = {"dopri5": 0, "tsit5": 1, "heun": 2}
 METHOD_CUSTOM = 3
+STAGES = {0: 7, 1: 7, 2: 2}  # per METHOD value
 MODE = {"exact": 0, "fast": 1}
 DT0_HEURISTIC, DT0_SCALAR, DT0_ARRAY = 0, 1, 2
 DYN = {"vdp": 1, "lorenz": 2, "zero": 3, "const": 4, "linear": 5, "linear_cos": 6,
@@ -66,11 +80,11 @@ class SolveArgs(C.Structure):
                 ("blocks", C.c_int32), ("cost_hint", C.c_void_p),
                 ("pipeline_chunks", C.c_int32), ("joint", C.c_int32),
                 ("max_iterations_out", C.c_void_p), ("refresh_map_out", C.c_void_p),
-                ("mlp_backend", C.c_int32), ("_pad3", C.c_int32),
+                ("reserved_mlp", C.c_int32), ("_pad3", C.c_int32),
                 ("prof_event_start", C.c_void_p), ("prof_event_stop", C.c_void_p),
                 ("launch_count_out", C.c_void_p),
                 ("traj", C.c_void_p), ("traj_offsets", C.c_void_p),
-                ("program", C.c_void_p)]
+                ("program", C.c_void_p), ("traj_stages", C.c_void_p)]
 
 
 class ProgramDesc(C.Structure):
@@ -102,7 +116,8 @@ class AdjointArgs(C.Structure):
                 ("grad_y0", C.c_void_p), ("grad_params", C.c_void_p),
                 ("workspace", C.c_void_p), ("workspace_bytes", C.c_size_t),
                 ("launch_count_out", C.c_void_p), ("grad_W1", C.c_void_p),
-                ("grad_b1", C.c_void_p), ("grad_W2", C.c_void_p), ("grad_b2", C.c_void_p)]
+                ("grad_b1", C.c_void_p), ("grad_W2", C.c_void_p), ("grad_b2", C.c_void_p),
+                ("traj_stages", C.c_void_p)]
 
 
 # every symbol include/bode.h declares, with its ctypes signature

@@ -103,6 +103,7 @@ bool valid_kind(int k) {
 int validate(const bode_solve_args* a) {
   if (!a) return fail(BODE_EINVAL, "null args");
   if (a->abi_version != BODE_ABI_VERSION) return fail(BODE_EINVAL, "abi_version mismatch");
+  if (a->reserved_mlp != 0) return fail(BODE_EINVAL, "reserved_mlp must be 0");
   if (a->n < 1 || a->d < 1)
     return fail(BODE_EINVAL, "need at least one instance and one state component");
   if (a->method < BODE_METHOD_DOPRI5 || a->method > BODE_METHOD_CUSTOM)
@@ -407,6 +408,9 @@ int bode_solve_adjoint(const bode_solve_args* a, const bode_adjoint_args* g) {
     A.gb1 = g->grad_b1;
     A.gW2 = g->grad_W2;
     A.gb2 = g->grad_b2;
+    A.traj_stages = g->traj_stages;
+    if (mlp_adjoint_tc_supported(a->d, a->dyn.hidden) && !g->traj_stages)
+      return fail(BODE_EINVAL, "MLP gradients with d == 64: the forward must record traj_stages");
   }
   int64_t launches = 0;
   cudaError_t e = adjoint_launch(a->method, a->d, A, g->workspace, (cudaStream_t)a->stream,

@@ -28,6 +28,7 @@ struct AdjParams {
   const float *W1, *b1, *W2, *b2;
   float *gW1, *gb1, *gW2, *gb2;
   float* mlp_part;
+  const float* traj_stages;  // (rows, S, 64) recorded stage inputs (MLP, d = 64)
 };
 
 // workspace: [queue | LPT cost | LPT scratch | MLP partials (MLP only)]

@@ -532,13 +532,13 @@ static cudaError_t mlp_solve_m(const bode_solve_args* a, const SolveParams& P, c
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const bool tc_ok = mlp_tc_supported(D, H);
-  const bool fused_ok = tc_ok && mlp_fused_supported(D, H, a->method);
-  if (a->mlp_backend == BODE_MLP_TCGEN05 && !tc_ok) return cudaErrorNotSupported;
-  if (a->mlp_backend == BODE_MLP_FUSED && !fused_ok) return cudaErrorNotSupported;
-  const bool use_tc = tc_ok && a->mlp_backend != BODE_MLP_CUDA_CORE;
-  const bool use_fused = fused_ok &&
-                         (a->mlp_backend == BODE_MLP_AUTO || a->mlp_backend == BODE_MLP_FUSED);
+  // one path per shape (no backend switch): the 64-wide tensor-core tile
+  // (fused persistent integrator when it fits TMEM, per-stage tcgen05
+  // kernels for a wider hidden layer), fp32 FMA kernels for other widths
+  const bool use_tc = mlp_tc_supported(D, H);
+  const bool use_fused = use_tc && mlp_fused_supported(D, H, a->method);
+  // the recorded stage inputs (tensor-core backward) come from the fused kernel
+  if (a->traj && a->traj_stages && !use_fused) return cudaErrorNotSupported;
   if (use_tc && (e = mlp_tc_prep(W1, W2, H, W.wprep, st)) != cudaSuccess) return e;
   int64_t nl = use_tc ? 1 : 0;  // kernels launched
   const int max_tiles = (int)((n + 127) / 128);
@@ -623,6 +623,7 @@ static cudaError_t mlp_solve_m(const bode_solve_args* a, const SolveParams& P, c
     F.refresh = P.refresh;
     F.prof = nullptr;
     F.traj = a->traj;
+    F.traj_y = a->traj ? a->traj_stages : nullptr;
     F.traj_offsets = a->traj_offsets;
 #ifdef BODE_FUSED_PROF
     static unsigned long long* prof_buf = nullptr;

@@ -64,6 +64,7 @@ struct MlpFusedArgs {
   unsigned long long* prof;      // debug builds (-DBODE_FUSED_PROF): (grid*3, 32) cycles
   double* traj;                  // optional accepted-step trajectory (gradients),
   const int64_t* traj_offsets;   // SolveParams::traj layout
+  float* traj_y;                 // optional (rows, S, 64): fp32 stage inputs of each record
 };
 bool mlp_fused_supported(int64_t D, int64_t H, int method);
 template <int M>

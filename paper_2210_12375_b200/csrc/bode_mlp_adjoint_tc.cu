@@ -12,9 +12,10 @@
 // trajectories are reversed in lockstep: reverse iteration `it` undoes step
 // nrec-1-it of every row with nrec > it, i.e. of a prefix of the order.  Per
 // iteration:
-//   load     the step records of the live rows (t_old, h, cursor, y_old)
-//   forward  k_s = f(Y_s) for every stage: the tcgen05 stage kernel of the
-//            lockstep solve (bode_mlp_tc.cu), i.e. the forward's own MMAs
+//   load     the step records of the live rows (t_old, h, cursor, y_old);
+//            the fp32 stage inputs Y_s come from the recording solve
+//            (bode_solve_args.traj_stages, written by the fused forward
+//            kernel), so no forward stage is recomputed
 //   seeds    dL/dk_s from dL/dy_next and the dense-output points of the step
 //   reverse  per stage s = S-1 .. 0, one tcgen05 kernel per 128-row tile:
 //              Z  = Y_s W1^T          (recomputed pre-activation, M=128 N=32 K=64)
@@ -83,6 +84,7 @@ struct RowState {
   int32_t* count;        // rows live in this iteration
   int64_t* hi;           // first point of the later step (the previous lo)
   int64_t* lo;           // cursor of the step being reversed
+  int64_t* rec;          // trajectory row of the step being reversed
   double* t_old;
   double* h;
   double* y;             // (n, 64) y_old
@@ -118,6 +120,7 @@ __global__ void load_kernel(RowState R, const double* traj, const int64_t* traj_
     const double* rec = traj + (traj_off[i] + R.nrec[p] - 1 - it) * kW;
     R.y[e] = rec[kTrajExtra + c];
     if (c == 0) {  // (only this thread touches the row's hi / lo)
+      R.rec[p] = traj_off[i] + R.nrec[p] - 1 - it;
       R.t_old[p] = rec[0];
       R.h[p] = rec[1];
       R.hi[p] = R.lo[p];
@@ -220,9 +223,9 @@ struct VjpArgs {
   int64_t n, pmax;
   int H, stage;
   const int32_t* count;
-  const double* y;
-  const float* k;
-  const float* Ybuf;  // (S, n, 64) fp32 stage inputs from the forward recompute (stages < S-1)
+  const double* y;          // (n, 64) y_old of the step (Y_0 = (float) y_old)
+  const float* Ystages;     // (rows, S, 64) recorded fp32 stage inputs
+  const int64_t* rec;       // (n) trajectory row of the step
   const double* h;
   const double* kb;   // (S, n, 64) dL/dk_s seeds (dense output, y_next)
   float* Ybar;        // (S, n, 64) dL/dY_s of every stage reversed so far
@@ -253,10 +256,9 @@ __device__ __forceinline__ void rows_sync() {  // the 256 row-owner threads
 
 // Production of one tile row's half (columns [32 h, 32 h + 32)) of the
 // stage input Y_s and of g_s = dL/dk_s, into the shared-memory TF32 hi/lo
-// tiles and the transposed global copies.  Y_s is the forward recompute's
-// (stages < S-1), or formed here exactly as the forward did (bode_mlp_tc.cu:
-// fp64 sum in the reference order, rounded to fp32); g_s is the seed plus,
-// in the order the stages were reversed (S-1 down to s+1), h a_s's dL/dY_s'.
+// tiles and the transposed global copies.  Y_s is the recorded stage input
+// (Y_0 = y_old); g_s is the seed plus, in the order the stages were
+// reversed (S-1 down to s+1), h a_s's dL/dY_s'.
 template <int M>
 __device__ __forceinline__ void vjp_produce(const VjpArgs& A, int64_t p, bool lv, int r, int h,
                                             VjpSmem& S) {
@@ -269,36 +271,16 @@ __device__ __forceinline__ void vjp_produce(const VjpArgs& A, int64_t p, bool lv
 #pragma unroll
     for (int e = 0; e < 32; e++) x[e] = g[e] = 0.0f;
   } else {
-    if (stage == T::S - 1) {
-      const double hr = A.h[p];
+    if (stage == 0) {  // y_old itself, rounded as the forward rounded it
+      const double2* yp = reinterpret_cast<const double2*>(A.y + p * kD + c0);
 #pragma unroll
-      for (int g8 = 0; g8 < 4; g8++) {  // 8 columns at a time: every load in flight
-        const int cc = c0 + 8 * g8;
-        double yv[8];
-        float kv[T::S][8];
-        const double2* yp = reinterpret_cast<const double2*>(A.y + p * kD + cc);
-#pragma unroll
-        for (int e = 0; e < 4; e++) {
-          const double2 d = __ldg(yp + e);
-          yv[2 * e] = d.x, yv[2 * e + 1] = d.y;
-        }
-#pragma unroll
-        for (int j = 0; j < T::S - 1; j++) {
-          const float4* kp = reinterpret_cast<const float4*>(A.k + ((int64_t)j * A.n + p) * kD + cc);
-          const float4 k0 = __ldg(kp), k1 = __ldg(kp + 1);
-          kv[j][0] = k0.x, kv[j][1] = k0.y, kv[j][2] = k0.z, kv[j][3] = k0.w;
-          kv[j][4] = k1.x, kv[j][5] = k1.y, kv[j][6] = k1.z, kv[j][7] = k1.w;
-        }
-#pragma unroll
-        for (int e = 0; e < 8; e++) {
-          double sum = ExactOps::mul(T::a(stage, 0), (double)kv[0][e]);
-#pragma unroll
-          for (int j = 1; j < T::S - 1; j++) sum = ExactOps::mad(T::a(stage, j), (double)kv[j][e], sum);
-          x[8 * g8 + e] = (float)ExactOps::mad(hr, sum, yv[e]);
-        }
+      for (int e = 0; e < 16; e++) {
+        const double2 d = __ldg(yp + e);
+        x[2 * e] = (float)d.x, x[2 * e + 1] = (float)d.y;
       }
-    } else {
-      const float4* yp = reinterpret_cast<const float4*>(A.Ybuf + ((int64_t)stage * A.n + p) * kD + c0);
+    } else {  // the recording solve's stage input
+      const float4* yp =
+          reinterpret_cast<const float4*>(A.Ystages + (A.rec[p] * T::S + stage) * kD + c0);
 #pragma unroll
       for (int e = 0; e < 8; e++) {
         const float4 v = __ldg(yp + e);
@@ -833,7 +815,7 @@ __global__ void wg_reduce_kernel(const float* part, int parts, int H, float* gW1
 
 struct Layout {
   size_t total = 0;
-  size_t keys_in, keys, idx_in, order, cub, cub_bytes, count, hi0, hi1, lo, t_old, h, y, k, kb, yb, Ybuf, Ybar,
+  size_t keys_in, keys, idx_in, order, cub, cub_bytes, count, hi0, hi1, lo, t_old, h, y, kb, rec, yb, Ybar,
       uT, AT, YT, gT, wfwd, wadj, w1t, w2t, part;
   Layout(int64_t n, int64_t H, int S, int parts) {
     auto take = [&](size_t bytes) {
@@ -849,8 +831,8 @@ struct Layout {
     keys_in = take(4 * n), keys = take(4 * n), idx_in = take(4 * n), order = take(4 * n);
     cub = take(cub_bytes), count = take(8);
     hi0 = take(8 * n), hi1 = take(8 * n), lo = take(8 * n), t_old = take(8 * n), h = take(8 * n);
-    y = take(8 * n * kD), k = take(4 * (size_t)S * n * kD), kb = take(8 * (size_t)S * n * kD);
-    Ybuf = take(4 * (size_t)S * n * kD), Ybar = take(4 * (size_t)S * n * kD);
+    y = take(8 * n * kD), kb = take(8 * (size_t)S * n * kD), rec = take(8 * n);
+    Ybar = take(4 * (size_t)S * n * kD);
     yb = take(8 * n * kD);
     uT = take(4 * (size_t)H * S * pmax), AT = take(4 * (size_t)H * S * pmax);
     YT = take(4 * (size_t)kD * S * pmax), gT = take(4 * (size_t)kD * S * pmax);
@@ -870,6 +852,7 @@ int sm_count() {
 template <int M>
 cudaError_t run(AdjParams A, char* ws, cudaStream_t st, int64_t* launches) {
   constexpr int S = Tab<M>::S;
+  if (!A.traj_stages) return cudaErrorInvalidValue;  // (bode_abi.cu reports it)
   const int64_t n = A.n, H = A.H;
   const int sms = sm_count();
   const Layout L(n, H, S, sms);
@@ -888,7 +871,7 @@ cudaError_t run(AdjParams A, char* ws, cudaStream_t st, int64_t* launches) {
   R.y = (double*)at(L.y);
   R.kb = (double*)at(L.kb);
   R.yb = (double*)at(L.yb);
-  float* k = (float*)at(L.k);
+  R.rec = (int64_t*)at(L.rec);
   float* wfwd = (float*)at(L.wfwd);
   float* wadj = (float*)at(L.wadj);
   cudaError_t e;
@@ -926,19 +909,12 @@ cudaError_t run(AdjParams A, char* ws, cudaStream_t st, int64_t* launches) {
   }
   const int max_tiles = (int)((n + kRows - 1) / kRows);
   const int grid = max_tiles < sms ? max_tiles : sms;
-  VjpArgs V{n, pmax, (int)H, 0, R.count, R.y, k, (const float*)at(L.Ybuf), R.h, R.kb, (float*)at(L.Ybar), wfwd, wadj, A.b1,
+  VjpArgs V{n, pmax, (int)H, 0, R.count, R.y, A.traj_stages, R.rec, R.h, R.kb, (float*)at(L.Ybar), wfwd, wadj, A.b1,
             (float*)at(L.uT), (float*)at(L.AT), (float*)at(L.YT), (float*)at(L.gT)};
   WgArgs G{(int)H, S, pmax, (int64_t)S * pmax, R.count, V.uT, V.AT, V.YT, V.gT, (float*)at(L.part)};
   for (int64_t it = 0; it < maxn; it++) {
     count_kernel<<<1, 1, 0, st>>>(R, it);
     load_kernel<<<gb, 256, 0, st>>>(R, A.traj, A.traj_offsets, it);
-    // forward recompute of k_0 .. k_{S-2} (the inputs of every stage), the
-    // forward's own MMAs
-    for (int s = 0; s + 1 < S; s++) {
-      MlpTcArgs t{n, (int)H, s, R.y, k, R.h, nullptr, R.count, nullptr, wfwd, A.b1, A.b2,
-                  k + (size_t)s * n * kD, (float*)at(L.Ybuf) + (size_t)s * n * kD};
-      if ((e = mlp_tc_launch<M>(t, max_tiles, st)) != cudaSuccess) return e;
-    }
     seeds_kernel<M><<<gb, 256, 0, st>>>(R, A.t_eval, A.t_eval_offsets, A.t_eval_len, A.grad_ys);
     for (int s = S - 1; s >= 0; s--) {
       V.stage = s;
@@ -946,7 +922,7 @@ cudaError_t run(AdjParams A, char* ws, cudaStream_t st, int64_t* launches) {
     }
     fold_kernel<M><<<gb, 256, 0, st>>>(R, (const float*)at(L.Ybar));
     wg_kernel<<<sms, 256, wg_smem, st>>>(G);
-    nl += 5 + 2 * S - 1;
+    nl += 5 + S;
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
   }
   finish_kernel<<<gb, 256, 0, st>>>(R, A.grad_ys, A.t_eval_offsets, A.t_eval_len, A.grad_y0);

@@ -168,6 +168,7 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_fused_kernel(const MlpFusedAr
   // ---- row state (WG0 threads)
   bool have = false;
   int64_t idx = 0, nsteps = 0, nacc = 0, cursor = 0, m = 0;
+  int64_t trow = 0, tlen = 0;  // (gradients) this row's trajectory rows
   double t = 0.0, dt = 0.0, t_end = 0.0, atol = 0.0, rtol = 0.0, n1 = 1.0, n2 = 1.0, h = 0.0;
   bool trunc = false;
   const double* te = nullptr;
@@ -205,6 +206,10 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_fused_kernel(const MlpFusedAr
       n2 = 1.0;
       nsteps = 0;
       nacc = 0;
+      if (A.traj_y) {
+        trow = A.traj_offsets[i];
+        tlen = A.traj_offsets[i + 1] - trow;
+      }
       have = true;
     };
     if (wg == 0) {
@@ -307,6 +312,14 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_fused_kernel(const MlpFusedAr
 #pragma unroll
             for (int q = 0; q < 4; q++)
               store_hilo(sm.a[0], sm.a[1], cm_off(row, c0 + 4 * q, kD), x + 4 * q);
+            // gradients: this attempt's stage input into the row of the step
+            // being tried (a rejected attempt is overwritten by the next one)
+            if (A.traj_y && live && nacc < tlen) {
+              float4* dst = reinterpret_cast<float4*>(A.traj_y + ((trow + nacc) * S + s) * kD + c0);
+#pragma unroll
+              for (int q = 0; q < 4; q++)
+                dst[q] = make_float4(x[4 * q], x[4 * q + 1], x[4 * q + 2], x[4 * q + 3]);
+            }
           }
         }
         fence_async_smem();

@@ -31,7 +31,6 @@ __all__ = ["DEFAULT_MAX_STEPS", "SolveStatus", "IvpBatch", "SolveStats", "Soluti
 DEFAULT_MAX_STEPS = 10_000
 # MLP path: fused persistent tcgen05 kernel (auto when d == 64), lockstep
 # per-stage tcgen05 3xTF32 kernels, or lockstep CUDA-core fp32
-MLP_BACKENDS = {"auto": 0, "cuda_core": 1, "tcgen05": 2, "fused": 3}
 
 
 # host arrays in [PIN_MIN_BYTES, PIN_MAX_BYTES] are page-locked (DMA at ~50
@@ -274,7 +273,7 @@ def solve(problem: IvpBatch, f, tableau=None, tol: Tolerances | None = None,
           controller: PidCoefficients | None = None, max_steps: int = DEFAULT_MAX_STEPS,
           dt0=None, record_trace: bool = False, *, mode: str = "exact", order=None,
           cost_hint=None, pipeline_chunks="auto", with_refresh_map: bool = False,
-          mlp_backend: str = "auto", _joint: bool = False) -> Solution:
+          _joint: bool = False) -> Solution:
     """Integrate every instance independently with adaptive steps on the GPU
     (reference ``solve``, solver.py:352-369), host arrays in and out."""
     if max_steps < 1:
@@ -341,7 +340,6 @@ def solve(problem: IvpBatch, f, tableau=None, tol: Tolerances | None = None,
             if smp.max() > smp.mean() * n / (_LANES * pipeline_chunks):
                 pipeline_chunks = 1
     a.pipeline_chunks = int(pipeline_chunks) if n >= 65536 else 1
-    a.mlp_backend = MLP_BACKENDS[mlp_backend]
     a.joint = 1 if _joint else 0
     ys = host_empty((max(n_rows, 1), d))
     n_emitted = host_empty(n, np.int64)
@@ -419,7 +417,7 @@ def solve_device(y0, t_start, t_end, f, *, t_eval=None, t_eval_offsets=None, met
                  atol=1e-6, rtol=1e-6, controller: PidCoefficients | None = None,
                  max_steps: int = DEFAULT_MAX_STEPS, dt0=None, order=None, cost_hint=None,
                  mode: str = "exact", record_trace: bool = False, stream=None,
-                 threads_per_block: int = 0, blocks: int = 0, mlp_backend: str = "auto",
+                 threads_per_block: int = 0, blocks: int = 0,
                  prof_events=None, with_refresh_map: bool = False,
                  record_trajectory: bool = False):
     """Device-resident solve on torch CUDA tensors; asynchronous (no host
@@ -524,7 +522,6 @@ def solve_device(y0, t_start, t_end, f, *, t_eval=None, t_eval_offsets=None, met
         a.max_iterations_out = out["max_iterations"].data_ptr()
         a.refresh_map_out = out["refresh_map"].data_ptr()
     a.threads_per_block, a.blocks = int(threads_per_block), int(blocks)
-    a.mlp_backend = MLP_BACKENDS[mlp_backend]
     if prof_events is not None:  # (torch.cuda.Event, torch.cuda.Event) around the integrator
         a.prof_event_start, a.prof_event_stop = (prof_events[0].cuda_event,
                                                  prof_events[1].cuda_event)
@@ -551,11 +548,18 @@ def solve_device(y0, t_start, t_end, f, *, t_eval=None, t_eval_offsets=None, met
             traj = torch.empty((max(rows, 1), _abi.traj_stride(d)), **f64)
             keep += [toff, traj]
             a.traj, a.traj_offsets = traj.data_ptr(), toff.data_ptr()
+            tstages = None
+            ns = _abi.mlp_stage_record(a)
+            if ns:  # tensor-core backward: the fp32 stage inputs of every step
+                tstages = torch.zeros((max(rows, 1), ns, 64), dtype=torch.float32, device=dev)
+                keep.append(tstages)
+                a.traj_stages = tstages.data_ptr()
             n_acc0 = out["n_accepted"].clone()
             _abi.check(lib.bode_solve(_abi.C.byref(a)))
             if not torch.equal(n_acc0, out["n_accepted"]):  # (the rows are bounded in-kernel)
                 raise _abi.BodeLibraryError("the recording solve diverged from the sizing solve")
         out["traj"], out["traj_offsets"] = traj[:rows], toff
+        out["traj_stages"] = tstages
         out["_args"], out["_keep"], out["_stream"] = a, keep, st
     # keep inputs alive until the stream has consumed them
     for t in keep:
@@ -590,6 +594,8 @@ def adjoint_device(fwd: dict, grad_ys):
     g = _abi.AdjointArgs()
     keep = []
     g.traj, g.traj_offsets = fwd["traj"].data_ptr(), fwd["traj_offsets"].data_ptr()
+    if fwd.get("traj_stages") is not None:
+        g.traj_stages = fwd["traj_stages"].data_ptr()
     g.n_emitted = fwd["n_emitted"].data_ptr()
     if fwd["ys"].numel():
         gy = grad_ys.to(dtype=torch.float64, device=dev).reshape(fwd["ys"].shape).contiguous()

@@ -283,8 +283,7 @@ def test_host_transfer_paths_are_equivalent(monkeypatch):
         assert np.array_equal(a.status, o.status) and np.array_equal(a.n_emitted, o.n_emitted)
 
 
-@pytest.mark.parametrize("backend", ["fused", "tcgen05", "cuda_core"])
-def test_mlp_neural_ode_vs_reference_fp32(backend):
+def test_mlp_neural_ode_vs_reference_fp32():
     """C4 (neural ODE, D=64, H=256, tanh): the reference solve with a NumPy
     fp32 MLP (tests/golden/mlp.npz).  fp32 GEMM summation order differs from
     OpenBLAS (and 3xTF32 from fp32), so step counts are compared in
@@ -294,7 +293,7 @@ def test_mlp_neural_ode_vs_reference_fp32(backend):
     n = z["y0"].shape[0]
     prob = bode.IvpBatch(z["y0"], np.zeros(n), np.full(n, 10.0), np.full((n, 1), 10.0))
     sol = bode.solve(prob, bode.mlp_dynamics(z["W1"], z["b1"], z["W2"], z["b2"]),
-                     max_steps=100_000, mlp_backend=backend)
+                     max_steps=100_000)
     assert np.array_equal(sol.status, z["status"])
     ratio = sol.stats.n_steps.sum() / z["n_steps"].sum()
     assert abs(ratio - 1.0) < 0.02, ratio
@@ -305,8 +304,7 @@ def test_mlp_neural_ode_vs_reference_fp32(backend):
     assert sol.stats.n_f_evals[0] >= 1 + 6 * sol.stats.n_steps.max()
 
 
-@pytest.mark.parametrize("backend", ["fused", "tcgen05", "cuda_core"])
-def test_mlp_matches_oracle_at_scale(backend):
+def test_mlp_matches_oracle_at_scale():
     z = np.load(os.path.join(os.path.dirname(__file__), "golden", "mlp.npz"))
     rng = np.random.default_rng(3)
     n = 2048
@@ -314,8 +312,7 @@ def test_mlp_matches_oracle_at_scale(backend):
     mlp = (z["W1"], z["b1"], z["W2"], z["b2"])
     te = np.array([2.5, 5.0, 10.0])
     sol = bode.solve(bode.IvpBatch(y0, np.zeros(n), np.full(n, 10.0), te),
-                     bode.mlp_dynamics(*mlp), tol=bode.Tolerances(1e-6, 1e-6), max_steps=100_000,
-                     mlp_backend=backend)
+                     bode.mlp_dynamics(*mlp), tol=bode.Tolerances(1e-6, 1e-6), max_steps=100_000)
     ref = O.solve(y0, 0.0, 10.0, te, dict(name="mlp", inst=None, shared=(), mlp=mlp),
                   atol=1e-6, rtol=1e-6, max_steps=100_000, nthreads=NT)
     assert np.array_equal(sol.status, ref["status"])
@@ -323,33 +320,3 @@ def test_mlp_matches_oracle_at_scale(backend):
     assert np.mean(sol.stats.n_steps == ref["n_steps"]) > 0.9
     a, b = sol.ys_flat.reshape(n, -1), ref["ys"].reshape(n, -1)
     assert np.max(np.abs(a - b).max(axis=1) / np.abs(b).max(axis=1)) < 1e-4
-
-
-@pytest.mark.parametrize("method,tol,te", [("dopri5", 1e-6, "dense3"), ("tsit5", 1e-7, "ragged"),
-                                           ("heun", 1e-4, "dense3")])
-def test_mlp_fused_bitwise_equals_lockstep_tcgen05(method, tol, te):
-    """The fused persistent kernel issues the lockstep tensor-core path's MMA
-    sequence and replays its fp64 arithmetic, so every output -- ys, step
-    counts, statuses, final dt, n_f_evals -- must be bit-identical, for any
-    tableau, ragged t_eval and rows refilled mid-tile (n > 148 * 128)."""
-    z = np.load(os.path.join(os.path.dirname(__file__), "golden", "mlp.npz"))
-    rng = np.random.default_rng(11)
-    n = 148 * 128 + 3000
-    y0 = rng.normal(size=(n, 64))
-    t_end = rng.uniform(2.0, 6.0, n)
-    if te == "dense3":
-        tev = np.stack([0.25 * t_end, 0.5 * t_end, t_end], axis=1)
-    else:
-        tev = [np.sort(rng.uniform(0.0, t_end[i], i % 4)) for i in range(n)]
-    prob = bode.IvpBatch(y0, np.zeros(n), t_end, tev)
-    f = bode.mlp_dynamics(z["W1"], z["b1"], z["W2"], z["b2"])
-    tab = {"dopri5": bode.dopri5, "tsit5": bode.tsit5, "heun": bode.heun}[method]()
-    kw = dict(tableau=tab, tol=bode.Tolerances(tol, tol), max_steps=100_000,
-              controller=bode.pid_controller("PI42"))
-    a = bode.solve(prob, f, mlp_backend="fused", **kw)
-    b = bode.solve(prob, f, mlp_backend="tcgen05", **kw)
-    assert np.array_equal(a.status, b.status)
-    for k in ("n_steps", "n_accepted", "n_f_evals", "final_dt"):
-        assert np.array_equal(getattr(a.stats, k), getattr(b.stats, k)), k
-    assert np.array_equal(a.n_emitted, b.n_emitted)
-    assert np.array_equal(a.ys_flat, b.ys_flat)
