@@ -525,9 +525,7 @@ def run_bode(args, rank, world, local_rank):
                         global_instances=n if strong else n * world, method=cfg["method"],
                         controller="PI42" if cfg["ctrl"] is PI42 else "I",
                         tol=cfg["tol"],
-                        # the MLP path has one arithmetic mode: the reference's
-                        # operation order in its fp64 control (bode_mlp*.cu)
-                        mode=args.mode if cfg["dyn"] != "mlp" else "exact (MLP control)",
+                        mode=args.mode,
                         lpt_order=bool(args.lpt),
                         parallelism=(f"shard{world}: one {n}-instance batch, cost-balanced "
                                      "device partition, NCCL gather of all results to rank 0 "

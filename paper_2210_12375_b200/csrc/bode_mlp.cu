@@ -624,6 +624,7 @@ static cudaError_t mlp_solve_m(const bode_solve_args* a, const SolveParams& P, c
     F.prof = nullptr;
     F.traj = a->traj;
     F.traj_y = a->traj ? a->traj_stages : nullptr;
+    F.fast = a->mode == BODE_MODE_FAST;
     F.traj_offsets = a->traj_offsets;
 #ifdef BODE_FUSED_PROF
     static unsigned long long* prof_buf = nullptr;

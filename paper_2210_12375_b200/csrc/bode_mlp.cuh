@@ -34,6 +34,7 @@ cudaError_t mlp_tc_launch(const MlpTcArgs& A, int max_tiles, cudaStream_t st);
 // launch runs every running instance to termination
 struct MlpFusedArgs {
   int H;
+  int fast;                      // BODE_MODE_FAST: fused arithmetic, squared-norm I / PI control
   int64_t max_steps;
   const int32_t* act;            // running instances after the init pass
   const int32_t* count;          // their number (device)

@@ -33,6 +33,8 @@
 // stage combination, control and dense output replay the reference order.
 #include <cuda_runtime.h>
 
+#include <type_traits>
+
 #include "bode_mlp.cuh"
 #include "bode_tc.cuh"
 
@@ -107,9 +109,17 @@ __device__ __forceinline__ void store_hilo(uint8_t* hi_base, uint8_t* lo_base, u
   *reinterpret_cast<float4*>(lo_base + off) = lo;
 }
 
-template <int M>
+// FAST (bode_solve_args.mode == BODE_MODE_FAST): the fp64 stage
+// combinations, error estimate and dense output fuse where written
+// (FastOps), the error ratio multiplies by a reciprocal, and an I / PI
+// controller runs on the squared norm with one exp (adapt_pi_ms) -- the
+// analytic kernels' fast mode.  The MLP itself is fp32 either way, so its
+// stage values already differ from the reference at fp32-ulp level; the
+// MLP parity bar (aggregate step counts 2%, y(T) 1e-4) holds for both.
+template <int M, bool FAST>
 __global__ void __launch_bounds__(kThreads, 1) mlp_fused_kernel(const MlpFusedArgs A) {
   using T = Tab<M>;
+  using O = typename std::conditional<FAST, FastOps, ExactOps>::type;
   constexpr int S = T::S;
   constexpr int S0 = T::FSAL ? 1 : 0;
   extern __shared__ __align__(16) uint8_t smem_raw[];
@@ -170,6 +180,7 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_fused_kernel(const MlpFusedAr
   int64_t idx = 0, nsteps = 0, nacc = 0, cursor = 0, m = 0;
   int64_t trow = 0, tlen = 0;  // (gradients) this row's trajectory rows
   double t = 0.0, dt = 0.0, t_end = 0.0, atol = 0.0, rtol = 0.0, n1 = 1.0, n2 = 1.0, h = 0.0;
+  LogCache L1{0.0, 0.0, true};  // (FAST I / PI) log of the previous norm: log(1) = 0
   bool trunc = false;
   const double* te = nullptr;
   double* yout = nullptr;
@@ -204,6 +215,7 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_fused_kernel(const MlpFusedAr
       }
       n1 = 1.0;
       n2 = 1.0;
+      L1 = LogCache{0.0, 0.0, true};
       nsteps = 0;
       nacc = 0;
       if (A.traj_y) {
@@ -300,14 +312,14 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_fused_kernel(const MlpFusedAr
               const double aj = T::a(s, j);
 #pragma unroll
               for (int e = 0; e < 16; e++)
-                acc[e] = j == 0 ? ExactOps::mul(aj, (double)kv[e])
-                                : ExactOps::mad(aj, (double)kv[e], acc[e]);
+                acc[e] = j == 0 ? O::mul(aj, (double)kv[e])
+                                : O::mad(aj, (double)kv[e], acc[e]);
             }
             float x[16];
 #pragma unroll
             for (int e = 0; e < 16; e++) {
               const double y = sm.ys[c0 + e][row];
-              x[e] = live ? (float)(s > 0 ? ExactOps::mad(hr, acc[e], y) : y) : 0.0f;
+              x[e] = live ? (float)(s > 0 ? O::mad(hr, acc[e], y) : y) : 0.0f;
             }
 #pragma unroll
             for (int q = 0; q < 4; q++)
@@ -328,18 +340,18 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_fused_kernel(const MlpFusedAr
         // ============ tanh epilogues of the hidden chunks
         int Wd;
         const bool htm = h_in_tmem(s, A.H, &Wd);
-        const int spu = Wd / kHc;
+        const int spu = Wd / kHc, lspu = 31 - __clz(spu);  // (a power of two: shifts, not divisions)
         const uint32_t acc1_base = 512 - 2 * Wd, h_base = acc1_base - 64;
         for (int c = 0; c < nc; c++) {
-          const int u = c / spu, b = u & 1;
-          if (c % spu == 0) {
+          const int u = c >> lspu, b = u & 1;
+          if ((c & (spu - 1)) == 0) {
             mbar_wait(&sm.g1done[b], ph_g1[b]);
             ph_g1[b] ^= 1;
             fence_after();
           }
           PROF_MARK(3)
           float v[16];
-          tmem_ld16(lrow + acc1_base + Wd * b + 32 * (c % spu) + 16 * wg, v);
+          tmem_ld16(lrow + acc1_base + Wd * b + 32 * (c & (spu - 1)) + 16 * wg, v);
           const float* b1 = A.b1 + c * kHc + 16 * wg;
 #pragma unroll
           for (int j = 0; j < 16; j++) v[j] = tanhf(v[j] + __ldg(b1 + j));
@@ -407,7 +419,7 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_fused_kernel(const MlpFusedAr
         const uint64_t dW2 = smem_desc(smem_u32(sm.w[0]), 1024);
         int Wd;
         const bool htm = h_in_tmem(s, A.H, &Wd);
-        const int spu = Wd / kHc, nu = A.H / Wd;
+        const int spu = Wd / kHc, nu = A.H / Wd, lspu = 31 - __clz(spu);
         const int KS = 2048 / Wd;                     // K per 16 KB item
         const uint32_t acc1_base = 512 - 2 * Wd, h_base = acc1_base - 64;
         // GEMM1 unit u: acc1[u&1] (N = Wd) = Y_s W1[u Wd .. u Wd + Wd)^T,
@@ -489,7 +501,7 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_fused_kernel(const MlpFusedAr
             gemm2_half(c, g, sl);
           }
           ph_epi ^= 1;
-          if (c % spu == spu - 1 && c / spu + 2 < nu) gemm1(c / spu + 2);
+          if ((c & (spu - 1)) == spu - 1 && (c >> lspu) + 2 < nu) gemm1((c >> lspu) + 2);
         }
         PROF_MARK(20)
       } else if (s == S0) {
@@ -535,19 +547,19 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_fused_kernel(const MlpFusedAr
 #pragma unroll
           for (int e = 0; e < 16; e++) {
             const double kd = (double)kv[e];
-            sb[e] = j == 0 ? ExactOps::mul(bj, kd) : ExactOps::mad(bj, kd, sb[e]);
-            se[e] = j == 0 ? ExactOps::mul(ej, kd) : ExactOps::mad(ej, kd, se[e]);
+            sb[e] = j == 0 ? O::mul(bj, kd) : O::mad(bj, kd, sb[e]);
+            se[e] = j == 0 ? O::mul(ej, kd) : O::mad(ej, kd, se[e]);
           }
         }
 #pragma unroll
         for (int e = 0; e < 16; e++) {
           const int c = c0 + e;
           const double y = sm.ys[c][row];
-          const double yn = ExactOps::mad(h, sb[e], y);
-          const double err = ExactOps::mul(h, se[e]);
-          const double scale = ExactOps::mad(rtol, np_max(fabs(y), fabs(yn)), atol);
-          const double r = ddiv(err, scale);
-          const double q = ExactOps::mul(r, r);
+          const double yn = O::mad(h, sb[e], y);
+          const double err = O::mul(h, se[e]);
+          const double scale = O::mad(rtol, np_max(fabs(y), fabs(yn)), atol);
+          const double r = FAST ? __dmul_rn(err, fast_rcp1(scale)) : ddiv(err, scale);
+          const double q = O::mul(r, r);
           if (wg == 0) {
             sq[c & 7] = c < 8 ? q : ExactOps::add(sq[c & 7], q);  // NumPy pairwise, n = 64
           } else {
@@ -567,11 +579,17 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_fused_kernel(const MlpFusedAr
       for (int c = 32; c < kD; c++) sq[c & 7] = ExactOps::add(sq[c & 7], q1[(c - 32) * kRows + row]);
       double nrm = ExactOps::add(ExactOps::add(ExactOps::add(sq[0], sq[1]), ExactOps::add(sq[2], sq[3])),
                                  ExactOps::add(ExactOps::add(sq[4], sq[5]), ExactOps::add(sq[6], sq[7])));
-      nrm = dsqrt(ddiv(nrm, (double)kD));
-      if (!isfinite(nrm)) nrm = __longlong_as_double(0x7ff0000000000000LL);
       bool accept = false;
       double dtn = h;
-      if (have) accept = adapt(A.ctrl, nrm, n1, n2, dtn);
+      if (FAST && A.ctrl.plain_pi) {  // squared norm, one exp (bode_device.cuh)
+        double ms = __dmul_rn(nrm, 1.0 / kD);  // (exact: kD is a power of two)
+        ms = ms < INFINITY ? ms : __longlong_as_double(0x7ff0000000000000LL);  // NaN -> inf
+        if (have) accept = adapt_pi_ms(A.ctrl, ms, L1, dtn, g_pow_tables);
+      } else {
+        nrm = dsqrt(ddiv(nrm, (double)kD));
+        if (!isfinite(nrm)) nrm = __longlong_as_double(0x7ff0000000000000LL);
+        if (have) accept = adapt(A.ctrl, nrm, n1, n2, dtn);
+      }
       const int64_t cursor_before = cursor;
       // dense output for every crossed point (solver.py:284-322), pre-commit state
       bool pend = have && accept && cursor < m && h != 0.0;
@@ -588,8 +606,8 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_fused_kernel(const MlpFusedAr
         for (int q = 0; q < S; q++) {
           double v = T::w(q, T::NI - 1);
 #pragma unroll
-          for (int r = T::NI - 2; r >= 0; r--) v = ExactOps::mad(v, th, T::w(q, r));
-          w[q] = ExactOps::mul(v, th);
+          for (int r = T::NI - 2; r >= 0; r--) v = O::mad(v, th, T::w(q, r));
+          w[q] = O::mul(v, th);
         }
 #pragma unroll
         for (int ch = 0; ch < 2; ch++) {
@@ -601,13 +619,13 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_fused_kernel(const MlpFusedAr
             tmem_ld16(lrow + 64 * j + c0, kv);
 #pragma unroll
             for (int e = 0; e < 16; e++)
-              sa[e] = j == 0 ? ExactOps::mul(w[0], (double)kv[e])
-                             : ExactOps::mad(w[j], (double)kv[e], sa[e]);
+              sa[e] = j == 0 ? O::mul(w[0], (double)kv[e])
+                             : O::mad(w[j], (double)kv[e], sa[e]);
           }
           if (pend && yout) {
 #pragma unroll
             for (int e = 0; e < 16; e++)
-              yout[cursor * kD + c0 + e] = ExactOps::mad(h, sa[e], sm.ys[c0 + e][row]);
+              yout[cursor * kD + c0 + e] = O::mad(h, sa[e], sm.ys[c0 + e][row]);
           }
         }
         if (pend) {
@@ -720,15 +738,21 @@ cudaError_t mlp_fused_launch(const MlpFusedArgs& A, cudaStream_t st) {
   const size_t smem = sizeof(fused::Smem);
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(fused::mlp_fused_kernel<M>,
+    cudaError_t e = cudaFuncSetAttribute(fused::mlp_fused_kernel<M, false>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(fused::mlp_fused_kernel<M, true>,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     attr = true;
   }
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  fused::mlp_fused_kernel<M><<<sms, fused::kThreads, smem, st>>>(A);
+  if (A.fast)
+    fused::mlp_fused_kernel<M, true><<<sms, fused::kThreads, smem, st>>>(A);
+  else
+    fused::mlp_fused_kernel<M, false><<<sms, fused::kThreads, smem, st>>>(A);
   return cudaGetLastError();
 }
 

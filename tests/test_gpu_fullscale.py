@@ -132,8 +132,9 @@ def test_c3_lorenz_full_scale_fast_mode():
     print(f"C3 2^18 x 1000 points fast: scaled ys err {err:.2e}")
 
 
-def test_c4_mlp_full_scale_fused():
-    cfg, sol, ref = _solve_both("c4")
+@pytest.mark.parametrize("mode", ["fast", "exact"])
+def test_c4_mlp_full_scale_fused(mode):
+    cfg, sol, ref = _solve_both("c4", mode=mode)
     assert cfg["n"] == 65536
     assert np.array_equal(sol.status, ref["status"]), "status"
     ratio = sol.stats.n_steps.sum() / ref["n_steps"].sum()
@@ -141,5 +142,5 @@ def test_c4_mlp_full_scale_fused():
     err = _scaled_ys_err(sol, ref, cfg["n"])
     assert err < 1e-4, err
     same = float(np.mean(sol.stats.n_steps == ref["n_steps"]))
-    print(f"C4 64K fused: sum n_steps ratio {ratio:.5f}, per-instance identical {same:.1%}, "
+    print(f"C4 64K fused ({mode}): sum n_steps ratio {ratio:.5f}, per-instance identical {same:.1%}, "
           f"scaled y(T) err {err:.2e}")
