@@ -158,14 +158,20 @@ int validate(const bode_solve_args* a) {
 // chunk's tail leaves idle; each slot has its own queue and LPT scratch, and
 // f0 rows are indexed by absolute instance.
 struct Layout {
-  size_t f0, tn, lpt, lpt_slot, mlp, total;
+  size_t f0, tn, rec, lpt, lpt_slot, mlp, total;
 };
+
+// resume records (bode_solver.cuh) for the persistent analytic kernels
+bool use_records(const bode_solve_args* a) { return a->dyn.kind != BODE_DYN_MLP && !a->joint; }
 
 Layout layout(const bode_solve_args* a, int64_t n_chunk, int slots) {
   Layout L;
   L.f0 = Workspace::f0_offset(a->max_steps);
   L.tn = L.f0 + ((8 * (size_t)a->n * (size_t)a->d + 255) & ~(size_t)255);
-  L.lpt = L.tn + ((8 * (size_t)a->n + 255) & ~(size_t)255);
+  L.rec = L.tn + ((8 * (size_t)a->n + 255) & ~(size_t)255);
+  const size_t rec_bytes =
+      use_records(a) ? 8 * (size_t)a->n * rec_stride(a->d, inst_cols(a->dyn, a->program)) : 0;
+  L.lpt = L.rec + ((rec_bytes + 255) & ~(size_t)255);
   L.lpt_slot = a->cost_hint && !a->order ? ((lpt_workspace_bytes(n_chunk) + 255) & ~(size_t)255) : 0;
   L.mlp = L.lpt + L.lpt_slot * slots;
   L.total = L.mlp + (a->dyn.kind == BODE_DYN_MLP ? mlp_workspace_bytes(a) : 0);
@@ -236,6 +242,10 @@ int run_chunk(const bode_solve_args* a, int64_t lo, int64_t hi, const Layout& L,
   P.smem_words = words * 4 <= 32 * 1024 ? (int32_t)words : 0;  // per-block shared bitmap
   P.f0 = (double*)(ws + L.f0) + lo * d;
   P.te_next = (double*)(ws + L.tn) + lo;
+  if (use_records(a)) {
+    P.rec_stride = rec_stride(d, n_inst);
+    P.rec = (double*)(ws + L.rec) + lo * P.rec_stride;
+  }
   P.ev_start = a->prof_event_start;
   P.ev_stop = a->prof_event_stop;
   if (a->order) {

@@ -60,9 +60,23 @@ struct SolveParams {
   int32_t smem_words;          // >0: per-block shared bitmap of this many words
   double* f0;                  // (n, D) FSAL seeds from the init pass
   double* te_next;             // (n) first pending output time from the init pass
+  // optional: the init pass's resume records in QUEUE order (kRec* slots,
+  // rec_stride doubles per position) -- a refill reads one contiguous
+  // record at its queue position instead of gathering a dozen scattered
+  // per-instance fields through the order permutation
+  double* rec;
+  int32_t rec_stride;
   void* ev_start;              // host side only: optional cudaEvent_t around
   void* ev_stop;               // the persistent launch (bench roofline)
 };
+
+// resume record slots (doubles; integers stored by bit pattern), then
+// y0 (D), f0 (D) and the instance's per-instance parameters
+enum : int { kRecT = 0, kRecTEnd, kRecDt, kRecTeNext, kRecIdx, kRecCursor, kRecM, kRecStatus,
+             kRecTeOff, kRecY };
+__host__ __device__ __forceinline__ int rec_stride(int64_t d, int n_inst) {
+  return (int)((kRecY + 2 * d + n_inst + 3) / 4 * 4);
+}
 
 constexpr int kTrajExtra = BODE_TRAJ_EXTRA;
 template <int D>
@@ -173,15 +187,75 @@ struct Lane {
       cursor++;
     }
     if (status == BODE_RUNNING) {
+      if (!P.rec) {
 #pragma unroll
-      for (int c = 0; c < D; c++) P.f0[i * D + c] = k[0][c];
-      P.te_next[i] = cursor < m ? te[cursor] : 0.0;
+        for (int c = 0; c < D; c++) P.f0[i * D + c] = k[0][c];
+        P.te_next[i] = cursor < m ? te[cursor] : 0.0;
+      }
       P.final_dt[i] = dt;
       P.n_emitted[i] = cursor;
       P.status[i] = BODE_RUNNING;
     } else {
       finish(P);
     }
+  }
+
+  // the resume record of queue position pos (P.rec), after initialize()
+  __device__ __forceinline__ void write_record(const SolveParams& P, int64_t pos) const {
+    double* r = P.rec + pos * P.rec_stride;
+    const double* te = te_of(P);
+    r[kRecT] = t;
+    r[kRecTEnd] = t_end;
+    r[kRecDt] = dt;
+    r[kRecTeNext] = cursor < m ? te[cursor] : 0.0;
+    r[kRecIdx] = __longlong_as_double(idx);
+    r[kRecCursor] = __longlong_as_double((int64_t)cursor);
+    r[kRecM] = __longlong_as_double((int64_t)m);
+    r[kRecStatus] = __longlong_as_double((int64_t)status);
+    r[kRecTeOff] = __longlong_as_double(P.t_eval_offsets ? P.t_eval_offsets[idx]
+                                                         : idx * P.t_eval_len);
+#pragma unroll
+    for (int c = 0; c < D; c++) {
+      r[kRecY + c] = y[c];
+      r[kRecY + D + c] = k[0][c];
+    }
+    for (int q = 0; q < P.dyn.n_inst; q++) r[kRecY + 2 * D + q] = P.dyn.inst[idx * P.dyn.n_inst + q];
+  }
+
+  // pick up the row of queue position pos from its record; returns the
+  // row's t_eval / ys offset and status
+  __device__ __forceinline__ int64_t resume_record(const SolveParams& P, int64_t pos,
+                                                   int64_t& st) {
+    const double* r = P.rec + pos * P.rec_stride;
+    // every load at once: the record is 16-byte aligned (rec_stride % 4 == 0)
+    constexpr int NV = (kRecY + 2 * D + 1) / 2;
+    double2 v[NV];
+#pragma unroll
+    for (int q = 0; q < NV; q++) v[q] = reinterpret_cast<const double2*>(r)[q];
+    const double* x = reinterpret_cast<const double*>(v);
+    t = x[kRecT];
+    t_end = x[kRecTEnd];
+    dt = x[kRecDt];
+    te_next = x[kRecTeNext];
+    idx = __double_as_longlong(x[kRecIdx]);
+    cursor = (int32_t)__double_as_longlong(x[kRecCursor]);
+    m = (int32_t)__double_as_longlong(x[kRecM]);
+    st = __double_as_longlong(x[kRecStatus]);
+#pragma unroll
+    for (int c = 0; c < D; c++) {
+      y[c] = x[kRecY + c];
+      k[0][c] = x[kRecY + D + c];
+    }
+    DynParams pr = P.dyn;  // per-instance parameters from the record (row 0)
+    pr.inst = r + kRecY + 2 * D;
+    f.load(pr, 0);
+    n1 = 1.0;
+    n2 = 1.0;
+    nsteps = 0;
+    nacc = 0;
+    status = BODE_RUNNING;
+    L1.ok = cr_log(1.0, g_pow_tables, L1.h, L1.l);  // log(1) = 0 exactly (both modes)
+    return __double_as_longlong(x[kRecTeOff]);
   }
 
   // pick up a row prepared by the init pass
@@ -369,12 +443,20 @@ __global__ void __launch_bounds__(128, ((F::D <= 2 && (!REC || PI)) ? BODE_BLOCK
         if (pos >= (unsigned long long)P.n) {
           done = true;
         } else {
-          const int64_t i = P.order ? P.order[pos] : (int64_t)pos;
-          // every load of the refill issues at once (one round trip after
-          // the order lookup); a row the init pass finalised is dropped
-          const int64_t st = P.status[i];
-          L.resume(P, i);
-          s_eb[threadIdx.x] = EmitBase{L.te_of(P), L.ys_of(P)};
+          int64_t st;
+          if (P.rec) {  // one contiguous record in queue order
+            const int64_t off = L.resume_record(P, (int64_t)pos, st);
+            s_eb[threadIdx.x] = EmitBase{P.t_eval_offsets ? P.t_eval + off : P.t_eval,
+                                         P.ys ? P.ys + off * F::D : nullptr};
+          } else {
+            const int64_t i = P.order ? P.order[pos] : (int64_t)pos;
+            // every load of the refill issues at once (one round trip after
+            // the order lookup); a row the init pass finalised is dropped
+            st = P.status[i];
+            L.resume(P, i);
+            s_eb[threadIdx.x] = EmitBase{L.te_of(P), L.ys_of(P)};
+          }
+          const int64_t i = L.idx;
           if (st == BODE_RUNNING) {
             if constexpr (REC)
               s_trec[threadIdx.x] = TrajRows{P.traj + P.traj_offsets[i] * kTrajStride<F::D>,
@@ -429,9 +511,13 @@ __global__ void __launch_bounds__(128, ((F::D <= 2 && (!REC || PI)) ? BODE_BLOCK
 template <int M, class F, class O>
 __global__ void __launch_bounds__(128) bode_init_kernel(const SolveParams P) {
   Lane<M, F, O> L;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < P.n;
-       i += (int64_t)gridDim.x * blockDim.x)
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < P.n;
+       q += (int64_t)gridDim.x * blockDim.x) {
+    // with resume records: queue position q (records written in queue order)
+    const int64_t i = (P.rec && P.order) ? P.order[q] : q;
     L.initialize(P, i);
+    if (P.rec) L.write_record(P, q);
+  }
 }
 
 #if BODE_HOST_CODE
