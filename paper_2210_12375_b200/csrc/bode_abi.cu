@@ -138,6 +138,11 @@ int validate(const bode_solve_args* a) {
   if (a->dyn.kind == BODE_DYN_MLP &&
       (!a->dyn.W1 || !a->dyn.b1 || !a->dyn.W2 || !a->dyn.b2 || a->dyn.hidden < 1))
     return fail(BODE_EINVAL, "MLP weights required");
+  // one MLP path: the fused tcgen05 integrator's 64-wide tile (narrower
+  // networks are zero-padded by the caller -- the Python facade does it)
+  if (a->dyn.kind == BODE_DYN_MLP && (a->d != 64 || a->dyn.hidden % 32 || a->dyn.hidden > 256))
+    return fail(BODE_EUNSUPPORTED,
+                "MLP dynamics: d == 64 and hidden a multiple of 32 up to 256 (zero-pad narrower networks)");
   if (a->pipeline_chunks < 0) return fail(BODE_EINVAL, "pipeline_chunks must be >= 0");
   if (a->traj && !a->traj_offsets) return fail(BODE_EINVAL, "traj needs traj_offsets");
   if (a->traj && a->joint)
@@ -384,12 +389,11 @@ int bode_solve_adjoint(const bode_solve_args* a, const bode_adjoint_args* g) {
   if (!g) return fail(BODE_EINVAL, "null adjoint args");
   if (a->joint) return fail(BODE_EUNSUPPORTED, "gradients: independent solve only");
   if (a->program) return fail(BODE_EUNSUPPORTED, "gradients: built-in methods and dynamics only");
-  if (a->dyn.kind == BODE_DYN_MLP &&
-      !((a->d == 4 || a->d == 8 || a->d == 16 || a->d == 32 || a->d == 64) &&
-        a->dyn.hidden <= 256 && a->dyn.hidden % 16 == 0))
-    return fail(BODE_EUNSUPPORTED, "MLP gradients: d in {4, 8, 16, 32, 64}, hidden <= 256, multiple of 16");
+
   if (!g->traj || !g->traj_offsets || !g->n_emitted || !g->grad_y0)
     return fail(BODE_EINVAL, "adjoint needs traj, traj_offsets, n_emitted and grad_y0");
+  if (a->dyn.kind == BODE_DYN_MLP && !g->traj_stages)
+    return fail(BODE_EINVAL, "MLP gradients: the forward must record traj_stages");
   if ((a->t_eval_offsets || a->t_eval_len > 0) && !g->grad_ys)
     return fail(BODE_EINVAL, "adjoint needs grad_ys");
   if (!g->workspace ||
@@ -419,8 +423,6 @@ int bode_solve_adjoint(const bode_solve_args* a, const bode_adjoint_args* g) {
     A.gW2 = g->grad_W2;
     A.gb2 = g->grad_b2;
     A.traj_stages = g->traj_stages;
-    if (mlp_adjoint_tc_supported(a->d, a->dyn.hidden) && !g->traj_stages)
-      return fail(BODE_EINVAL, "MLP gradients with d == 64: the forward must record traj_stages");
   }
   int64_t launches = 0;
   cudaError_t e = adjoint_launch(a->method, a->d, A, g->workspace, (cudaStream_t)a->stream,

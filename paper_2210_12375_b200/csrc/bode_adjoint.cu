@@ -217,15 +217,14 @@ static size_t adjoint_lpt_end(int64_t n) {
 
 // workspace: [queue counter | cost (n doubles) | LPT scratch | MLP partials]
 size_t adjoint_workspace_bytes(int64_t n, int64_t d, int kind, int64_t H) {
-  if (kind == BODE_DYN_MLP && mlp_adjoint_tc_supported(d, H))
-    return mlp_adjoint_tc_bytes(n, H, BODE_METHOD_DOPRI5);  // (7 stages: the widest)
-  return adjoint_lpt_end(n) + (kind == BODE_DYN_MLP ? mlp_adjoint_part_bytes(d, H) : 0);
+  (void)d;
+  if (kind == BODE_DYN_MLP) return mlp_adjoint_tc_bytes(n, H, BODE_METHOD_DOPRI5);  // (7 stages: the widest)
+  return adjoint_lpt_end(n);
 }
 
 cudaError_t adjoint_launch(int method, int64_t d, AdjParams A, void* ws, cudaStream_t st,
                            int64_t* launches) {
-  if (A.dyn.kind == BODE_DYN_MLP && mlp_adjoint_tc_supported(d, A.H))
-    return mlp_adjoint_tc_run(method, A, ws, st, launches);
+  if (A.dyn.kind == BODE_DYN_MLP) return mlp_adjoint_tc_run(method, A, ws, st, launches);
   char* w = (char*)ws;
   cudaError_t e = cudaMemsetAsync(w, 0, 8, st);
   if (e != cudaSuccess) return e;
@@ -239,10 +238,6 @@ cudaError_t adjoint_launch(int method, int64_t d, AdjParams A, void* ws, cudaStr
   if (e != cudaSuccess) return e;
   A.order = order;
   *launches += 4;  // cost + 3 LPT passes
-  if (A.dyn.kind == BODE_DYN_MLP) {
-    A.mlp_part = (float*)(w + adjoint_lpt_end(A.n));
-    return mlp_adjoint_run(method, d, A, st, launches);
-  }
   *launches += 1;
   switch (method) {
     case BODE_METHOD_DOPRI5: return dispatch_adjoint<BODE_METHOD_DOPRI5>(A.dyn.kind, d, A, st);

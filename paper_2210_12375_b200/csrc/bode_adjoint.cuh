@@ -27,14 +27,11 @@ struct AdjParams {
   int64_t H;
   const float *W1, *b1, *W2, *b2;
   float *gW1, *gb1, *gW2, *gb2;
-  float* mlp_part;
   const float* traj_stages;  // (rows, S, 64) recorded stage inputs (MLP, d = 64)
 };
 
 // workspace: [queue | LPT cost | LPT scratch | MLP partials (MLP only)]
 size_t adjoint_workspace_bytes(int64_t n, int64_t d, int kind, int64_t H);
-size_t mlp_adjoint_part_bytes(int64_t d, int64_t H);
-cudaError_t mlp_adjoint_run(int method, int64_t d, AdjParams A, cudaStream_t st, int64_t* launches);
 // tensor-core backward for D = 64 (bode_mlp_adjoint_tc.cu); the workspace
 // of adjoint_workspace_bytes is sized for 7 stages (the widest tableau)
 bool mlp_adjoint_tc_supported(int64_t d, int64_t H);

@@ -2,20 +2,14 @@
 // fp32 on an fp64 state (the C4 oracle is the reference
 // solve with a NumPy fp32 MLP callable).
 //
-// Unlike the analytic path, the dynamics here is a dense contraction over
-// the whole batch, so the loop runs in lockstep like the reference's
-// step_once (solver.py:208-282): every iteration evaluates the six FSAL
-// stages for all *running* instances as batched MLPs, then one control
-// kernel (a warp per instance) forms y_next / err, the NumPy-order RMS
-// norm, the PID update, accept/reject, dense output and statuses, and
-// compacts the running set for the next iteration.  Finished instances drop
-// out of the GEMMs (the reference keeps them in as "overhanging" rows,
-// Appendix B; results are identical, the work is not).  Stage values are
-// stored as fp32 -- exactly the values the reference's float64 cast of the
-// fp32 MLP output holds -- and combined in fp64 in the reference order.
-//
-// Stage evaluation kernel: see mlp_eval_* below (CUDA-core fp32 here; the
-// tcgen05 path lives in bode_mlp_tc.cu).
+// One path: BatchSolver.__init__ for every row as a batched init pass (f0,
+// the Hairer probe evaluation, dt0, INFINITE_DYNAMICS, points at t_start;
+// the two MLP evaluations on the tensor cores, bode_mlp_tc.cu), then ONE
+// launch of the fused persistent tcgen05 integrator (bode_mlp_fused.cu) that
+// runs every running row to termination.  The network must fill the 64-wide
+// tensor-core tile (d == 64, hidden a multiple of 32 up to 256; bode_abi.cu
+// validates it): narrower networks are zero-padded by the caller (the
+// Python facade does it, dynamics.mlp_pad).
 #include <cstdio>
 
 #include "bode_mlp.cuh"
@@ -73,92 +67,6 @@ size_t carve(const bode_solve_args* a, char* base, MlpWs* w) {
   return off;
 }
 
-// ---------------------------------------------------------------- MLP ----
-// out[row of active[p]] = W2 tanh(W1 Y[p] + b1) + b2, p < count.  Y rows are
-// compacted (position p), outputs scattered to the instance row.
-// CUDA-core fp32 version: persistent blocks (one per SM) keep both weight
-// matrices transposed in shared memory and stream tiles of kTile rows.
-__global__ void __launch_bounds__(256) mlp_eval_cc_kernel(const float* __restrict__ Y,
-                                                          const int32_t* __restrict__ act,
-                                                          const int32_t* __restrict__ count,
-                                                          const float* __restrict__ W1,
-                                                          const float* __restrict__ b1,
-                                                          const float* __restrict__ W2,
-                                                          const float* __restrict__ b2,
-                                                          int D, int H, float* __restrict__ out) {
-  extern __shared__ float sm[];
-  float* W1t = sm;               // D x H  (W1t[c*H + j] = W1[j][c])
-  float* W2t = W1t + D * H;      // H x D  (W2t[j*D + o] = W2[o][j])
-  float* Ys = W2t + H * D;       // kTile x D
-  float* Hs = Ys + kTile * D;    // kTile x H
-  const int cnt = *count;
-  if ((int)blockIdx.x * kTile >= cnt) return;
-  for (int e = threadIdx.x; e < D * H; e += blockDim.x) {
-    const int j = e / D, c = e % D;  // coalesced read of W1[j][c] and W2[c][j]
-    W1t[c * H + j] = W1[e];
-    const int o = e / H, jj = e % H;
-    W2t[jj * D + o] = W2[e];
-  }
-  for (int tile = blockIdx.x; tile * kTile < cnt; tile += gridDim.x) {
-    const int p0 = tile * kTile;
-    const int rows = cnt - p0 < kTile ? cnt - p0 : kTile;
-    __syncthreads();
-    for (int e = threadIdx.x; e < kTile * D; e += blockDim.x) {
-      const int r = e / D;
-      Ys[e] = r < rows ? Y[(size_t)(p0 + r) * D + e % D] : 0.0f;
-    }
-    __syncthreads();
-    for (int j = threadIdx.x; j < H; j += blockDim.x) {
-      float acc[kTile];
-#pragma unroll
-      for (int r = 0; r < kTile; r++) acc[r] = 0.0f;
-      for (int c = 0; c < D; c++) {
-        const float w = W1t[c * H + j];
-#pragma unroll
-        for (int r = 0; r < kTile; r++) acc[r] = fmaf(Ys[r * D + c], w, acc[r]);
-      }
-      const float bj = b1[j];
-#pragma unroll
-      for (int r = 0; r < kTile; r++) Hs[r * H + j] = tanhf(acc[r] + bj);
-    }
-    __syncthreads();
-    for (int e = threadIdx.x; e < rows * D; e += blockDim.x) {
-      const int r = e / D, o = e % D;
-      const float* hr = Hs + r * H;
-      float acc = 0.0f;
-      for (int j = 0; j < H; j++) acc = fmaf(hr[j], W2t[j * D + o], acc);
-      out[(size_t)act[p0 + r] * D + o] = acc + b2[o];
-    }
-  }
-}
-
-// ------------------------------------------------------ stage inputs ----
-// Y[p] = fp32( y + h * sum_{j<i} a_ij k_j )  in the reference order
-// (stepper.py:81-89), for p < count.
-template <int M>
-__global__ void mlp_stage_input_kernel(MlpWs W, int64_t n, int D, int stage) {
-  using T = Tab<M>;
-  const int cnt = W.cnt[0];
-  const int64_t total = (int64_t)cnt * D;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
-       e += (int64_t)gridDim.x * blockDim.x) {
-    const int p = (int)(e / D), c = (int)(e % D);
-    const int64_t i = W.act[0][p];
-    double y = W.y[i * D + c];
-    if (stage > 0) {
-      double s = 0.0;
-#pragma unroll
-      for (int j = 0; j < T::S; j++) {
-        if (j >= stage) break;
-        const double kj = (double)W.k[((int64_t)j * n + i) * D + c];
-        s = j == 0 ? ExactOps::mul(T::a(stage, 0), kj) : ExactOps::mad(T::a(stage, j), kj, s);
-      }
-      y = ExactOps::mad(W.h[i], s, y);
-    }
-    W.Y[(int64_t)p * D + c] = (float)y;
-  }
-}
-
 // ---------------------------------------------------------- control ----
 struct CtrlArgs {
   CtrlParams ctrl;
@@ -194,141 +102,6 @@ __device__ __forceinline__ void te_of(const CtrlArgs& A, int64_t i, int D, const
     te = A.t_eval;
     m = A.t_eval_len;
     ys = A.ys ? A.ys + i * A.t_eval_len * D : nullptr;
-  }
-}
-
-// one warp per running instance: the rest of step_once after the stages
-template <int M>
-__global__ void __launch_bounds__(128) mlp_control_kernel(MlpWs W, CtrlArgs A, int64_t n, int D) {
-  using T = Tab<M>;
-  __shared__ double sq[4][kMaxD];
-  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  const int cnt = W.cnt[0];
-  const int p = blockIdx.x * 4 + wib;
-  if (p >= cnt) return;
-  const int64_t i = W.act[0][p];
-  const double h = W.h[i], y_t = W.t[i], t_end = A.t_end[i];
-  const double atol = A.atol_v ? A.atol_v[i] : A.atol, rtol = A.rtol_v ? A.rtol_v[i] : A.rtol;
-  const int nslot = (D + 31) / 32;
-  const int64_t nacc_before = A.n_accepted[i];  // (read before lane 0 updates it)
-  double yv[4], yn[4];
-  for (int s = 0; s < nslot; s++) {
-    const int c = lane + 32 * s;
-    if (c >= D) break;
-    const double y = W.y[i * D + c];
-    double sb = 0.0, se = 0.0;
-#pragma unroll
-    for (int j = 0; j < T::S; j++) {
-      const double kj = (double)W.k[((int64_t)j * n + i) * D + c];
-      sb = j == 0 ? ExactOps::mul(T::b(0), kj) : ExactOps::mad(T::b(j), kj, sb);
-      se = j == 0 ? ExactOps::mul(T::e(0), kj) : ExactOps::mad(T::e(j), kj, se);
-    }
-    yv[s] = y;
-    yn[s] = ExactOps::mad(h, sb, y);
-    const double err = ExactOps::mul(h, se);
-    const double scale = ExactOps::mad(rtol, np_max(fabs(y), fabs(yn[s])), atol);
-    const double r = ddiv(err, scale);
-    sq[wib][c] = ExactOps::mul(r, r);
-  }
-  __syncwarp();
-  int acc_i = 0;
-  double dtn = 0.0;
-  if (lane == 0) {
-    double nrm = dsqrt(ddiv(pairwise_sum_rt<ExactOps>(sq[wib], D), (double)D));
-    if (!isfinite(nrm)) nrm = __longlong_as_double(0x7ff0000000000000LL);
-    double a1 = W.n1[i], a2 = W.n2[i];
-    dtn = h;
-    acc_i = adapt(A.ctrl, nrm, a1, a2, dtn);
-    W.n1[i] = a1;
-    W.n2[i] = a2;
-  }
-  acc_i = __shfl_sync(0xffffffffu, acc_i, 0);
-  dtn = __shfl_sync(0xffffffffu, dtn, 0);
-  const bool trunc = W.trunc[i] != 0;
-  const int64_t j_iter = A.n_steps[i];
-  int64_t cursor = A.n_emitted[i];
-  int status = BODE_RUNNING;
-  double t_new = y_t;
-  if (acc_i && A.traj && nacc_before < A.traj_offsets[i + 1] - A.traj_offsets[i]) {
-    // record (t_old, h, cursor, y_old) for the adjoint (rows bounded: they
-    // were sized by an identical solve)
-    const int W = BODE_TRAJ_STRIDE(D);
-    double* rec = A.traj + (A.traj_offsets[i] + nacc_before) * W;
-    if (lane == 0) {
-      rec[0] = y_t;
-      rec[1] = h;
-      rec[2] = (double)cursor;
-    }
-    for (int s = 0; s < nslot; s++) {
-      const int c = lane + 32 * s;
-      if (c < D) rec[kTrajRowExtra + c] = yv[s];
-    }
-  }
-  if (acc_i) {
-    // dense output (solver.py:284-322) from the pre-commit state
-    const double* te;
-    int64_t m;
-    double* ys;
-    te_of(A, i, D, te, m, ys);
-    if (cursor < m && h != 0.0) {
-      while (cursor < m) {
-        double th = ddiv(ExactOps::sub(te[cursor], y_t), h);
-        if (!(th <= 1.0)) break;
-        th = np_max(th, 0.0);
-        double w[7];
-#pragma unroll
-        for (int q = 0; q < T::S; q++) {
-          double v = T::w(q, T::NI - 1);
-          for (int r = T::NI - 2; r >= 0; r--) v = ExactOps::mad(v, th, T::w(q, r));
-          w[q] = ExactOps::mul(v, th);
-        }
-        for (int s = 0; s < nslot; s++) {
-          const int c = lane + 32 * s;
-          if (c >= D) break;
-          double sacc = 0.0;
-#pragma unroll
-          for (int q = 0; q < T::S; q++) {
-            const double kq = (double)W.k[((int64_t)q * n + i) * D + c];
-            sacc = q == 0 ? ExactOps::mul(w[0], kq) : ExactOps::mad(w[q], kq, sacc);
-          }
-          if (ys) ys[cursor * D + c] = ExactOps::mad(h, sacc, yv[s]);
-        }
-        cursor++;
-      }
-    }
-    for (int s = 0; s < nslot; s++) {
-      const int c = lane + 32 * s;
-      if (c >= D) break;
-      W.y[i * D + c] = yn[s];
-      if (T::FSAL) W.k[i * D + c] = W.k[((int64_t)(T::S - 1) * n + i) * D + c];
-    }
-    t_new = trunc ? t_end : ExactOps::add(y_t, h);
-    if (trunc) status = BODE_SUCCESS;
-  }
-  if (lane == 0) {
-    const int64_t ns = j_iter + 1;
-    if (status == BODE_RUNNING && ExactOps::add(t_new, dtn) == t_new) status = BODE_STEP_UNDERFLOW;
-    if (status == BODE_RUNNING && ns >= A.max_steps) status = BODE_MAX_STEPS_EXCEEDED;
-    A.n_steps[i] = ns;
-    if (acc_i) A.n_accepted[i] += 1;
-    A.n_emitted[i] = cursor;
-    W.t[i] = t_new;
-    W.dt[i] = dtn;
-    A.final_dt[i] = dtn;
-    A.status[i] = status;
-    if (!acc_i && status == BODE_RUNNING) {
-      const uint64_t bit = (uint64_t)j_iter + 1;
-      atomicOr(&A.refresh[bit >> 5], 1u << (bit & 31));
-    }
-    if (status == BODE_RUNNING) {
-      const double rem = ExactOps::sub(t_end, t_new);
-      const bool tr = fabs(dtn) >= fabs(rem);
-      W.h[i] = tr ? rem : dtn;
-      W.trunc[i] = tr;
-      W.act[1][atomicAdd(&W.cnt[1], 1)] = (int32_t)i;
-    } else {
-      atomicMax(A.max_n, (unsigned long long)ns);
-    }
   }
 }
 
@@ -496,15 +269,6 @@ __global__ void __launch_bounds__(128) mlp_init_c_kernel(MlpWs W, InitArgs I, Ct
   }
 }
 
-// the first stage of every attempt for non-FSAL tableaus: Y = y
-__global__ void mlp_state_input_kernel(MlpWs W, int D) {
-  const int cnt = W.cnt[0];
-  const int64_t total = (int64_t)cnt * D;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
-       e += (int64_t)gridDim.x * blockDim.x)
-    W.Y[e] = (float)W.y[(int64_t)W.act[0][e / D] * D + e % D];
-}
-
 inline unsigned grid_for(int64_t work, int per = 256, unsigned cap = 148 * 16) {
   const int64_t g = (work + per - 1) / per;
   return (unsigned)(g < 1 ? 1 : (g > cap ? cap : g));
@@ -520,56 +284,19 @@ static cudaError_t mlp_solve_m(const bode_solve_args* a, const SolveParams& P, c
   using T = Tab<M>;
   const int64_t n = a->n;
   const int D = (int)a->d, H = (int)a->dyn.hidden;
-  if (D > kMaxD || H > 1024) return cudaErrorNotSupported;
+  if (!mlp_fused_supported(D, H, a->method)) return cudaErrorNotSupported;  // (validated)
   MlpWs W;
   carve(a, wsb, &W);
   const float *W1 = a->dyn.W1, *b1 = a->dyn.b1, *W2 = a->dyn.W2, *b2 = a->dyn.b2;
-  const size_t smem = sizeof(float) * ((size_t)2 * D * H + (size_t)kTile * (D + H));
-  if (smem > 227 * 1024) return cudaErrorNotSupported;
-  cudaError_t e = cudaFuncSetAttribute(mlp_eval_cc_kernel,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = mlp_tc_prep(W1, W2, H, W.wprep, st);
   if (e != cudaSuccess) return e;
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  // one path per shape (no backend switch): the 64-wide tensor-core tile
-  // (fused persistent integrator when it fits TMEM, per-stage tcgen05
-  // kernels for a wider hidden layer), fp32 FMA kernels for other widths
-  const bool use_tc = mlp_tc_supported(D, H);
-  const bool use_fused = use_tc && mlp_fused_supported(D, H, a->method);
-  // the recorded stage inputs (tensor-core backward) come from the fused kernel
-  if (a->traj && a->traj_stages && !use_fused) return cudaErrorNotSupported;
-  if (use_tc && (e = mlp_tc_prep(W1, W2, H, W.wprep, st)) != cudaSuccess) return e;
-  int64_t nl = use_tc ? 1 : 0;  // kernels launched
+  int64_t nl = 1;  // kernels launched
   const int max_tiles = (int)((n + 127) / 128);
   // f(Y) for the compacted fp32 rows in W.Y (init evaluations)
   auto eval = [&](float* out) {
-    if (use_tc) {
-      MlpTcArgs t{n, H, 0, W.y, W.k, W.h, W.act[0], W.cnt, W.Y, W.wprep, b1, b2, out};
-      mlp_tc_launch<M>(t, max_tiles, st);
-      nl += 1;
-      return;
-    }
+    MlpTcArgs t{n, H, 0, W.y, W.k, W.h, W.act[0], W.cnt, W.Y, W.wprep, b1, b2, out};
+    mlp_tc_launch<M>(t, max_tiles, st);
     nl += 1;
-    // one persistent block per SM; blocks past the live tile count exit
-    const unsigned g = grid_for(n, kTile, (unsigned)sms);
-    mlp_eval_cc_kernel<<<g, 256, smem, st>>>(W.Y, W.act[0], W.cnt, W1, b1, W2, b2, D, H, out);
-  };
-  // stage s of the current attempt: input formed from y, h and k_0..k_{s-1}
-  auto stage = [&](int s) {
-    if (use_tc) {  // prologue fused into the tensor-core kernel
-      MlpTcArgs t{n, H, s, W.y, W.k, W.h, W.act[0], W.cnt, nullptr, W.wprep, b1, b2,
-                  W.k + (size_t)s * n * D};
-      mlp_tc_launch<M>(t, max_tiles, st);
-      nl += 1;
-      return;
-    }
-    nl += 1;
-    if (s == 0)
-      mlp_state_input_kernel<<<grid_for(n * D), 256, 0, st>>>(W, D);
-    else
-      mlp_stage_input_kernel<M><<<grid_for(n * D), 256, 0, st>>>(W, n, D, s);
-    eval(W.k + (size_t)s * n * D);
   };
   InitArgs I{a->y0, a->t_start, a->t_end, a->atol_v, a->rtol_v, a->atol, a->rtol,
              a->dt0_mode, a->dt0, a->dt0_v, T::ORDER};
@@ -590,7 +317,7 @@ static cudaError_t mlp_solve_m(const bode_solve_args* a, const SolveParams& P, c
   nl += heur ? 5 : 4;
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
 
-  if (use_fused) {  // one persistent launch runs every running instance to the end
+  {  // one persistent launch runs every running instance to the end
     MlpFusedArgs F;
     F.H = H;
     F.max_steps = a->max_steps;
@@ -655,29 +382,6 @@ static cudaError_t mlp_solve_m(const bode_solve_args* a, const SolveParams& P, c
     return e;
   }
 
-  // lockstep iterations in bursts; each burst ends with one host read of the
-  // running count (kernels of a drained batch exit immediately)
-  int32_t* h_cnt = nullptr;
-  if ((e = cudaMallocHost((void**)&h_cnt, sizeof(int32_t))) != cudaSuccess) return e;
-  int64_t iters = 0;
-  int burst = 4;
-  while (true) {
-    for (int b = 0; b < burst; b++) {
-      for (int s = T::FSAL ? 1 : 0; s < T::S; s++) stage(s);
-      mlp_control_kernel<M><<<(unsigned)((n + 3) / 4), 128, 0, st>>>(W, A, n, D);
-      mlp_copy_list_kernel<<<grid_for(n), 256, 0, st>>>(W);
-      mlp_swap_kernel<<<1, 32, 0, st>>>(W);
-      nl += 3;
-    }
-    iters += burst;
-    if ((e = cudaMemcpyAsync(h_cnt, W.cnt, sizeof(int32_t), cudaMemcpyDeviceToHost, st)) != cudaSuccess) break;
-    if ((e = cudaStreamSynchronize(st)) != cudaSuccess) break;
-    if (*h_cnt == 0 || iters >= a->max_steps + 1) break;
-    burst = burst < 32 ? burst * 2 : 32;
-  }
-  cudaFreeHost(h_cnt);
-  if (launches) *launches += nl;
-  return e == cudaSuccess ? cudaGetLastError() : e;
 }
 
 cudaError_t mlp_solve(const bode_solve_args* a, const SolveParams& P, char* ws, cudaStream_t st,

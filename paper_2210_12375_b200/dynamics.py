@@ -245,6 +245,42 @@ def damped_dynamics() -> DeviceDynamics:
     return DeviceDynamics("damped")
 
 
+MLP_TILE = 64   # state width of the tensor-core tile (csrc/bode_tc.cuh kD)
+MLP_HMAX = 256  # hidden width the fused kernel keeps in TMEM
+
+
+def mlp_pad(dyn: DeviceDynamics):
+    """The MLP zero-padded to the tensor-core tile: D -> 64, H -> a multiple
+    of 32.  Returns (padded dynamics, D, H), or None when it already fits.
+    Padded hidden units have zero weights and bias (tanh(0) = 0 feeds zero
+    columns of W2), padded outputs have zero rows of W2 and zero bias, so
+    f of a zero-padded state is the zero-padded f exactly and padded state
+    components stay exactly 0.  solve / solve_device scale the tolerances by
+    sqrt(D/64) so the 64-wide RMS error norm equals the D-wide one."""
+    W1, b1, W2, b2 = dyn.mlp
+    H, D = W1.shape
+    if D > MLP_TILE or H > MLP_HMAX:
+        raise NotImplementedError(f"MLP dynamics run on the 64-wide tensor-core tile: need "
+                                  f"D <= {MLP_TILE} and hidden <= {MLP_HMAX}, got D={D}, H={H}")
+    Hp = (H + 31) // 32 * 32
+    if D == MLP_TILE and Hp == H:
+        return None
+    if _is_tensor(W1):
+        import torch
+
+        def z(*shape):
+            return torch.zeros(shape, dtype=torch.float32, device=W1.device)
+    else:
+        def z(*shape):
+            return np.zeros(shape, dtype=np.float32)
+    W1p, b1p, W2p, b2p = z(Hp, MLP_TILE), z(Hp), z(MLP_TILE, Hp), z(MLP_TILE)
+    W1p[:H, :D] = W1
+    b1p[:H] = b1
+    W2p[:D, :H] = W2
+    b2p[:D] = b2
+    return DeviceDynamics("mlp", {}, mlp=(W1p, b1p, W2p, b2p)), D, H
+
+
 def mlp_dynamics(W1, b1, W2, b2) -> DeviceDynamics:
     """Neural-ODE dynamics W2 tanh(W1 y + b1) + b2 evaluated in fp32 on the
     tensor cores; the state stays fp64.  Weights as

@@ -22,7 +22,7 @@ import numpy as np
 
 from . import _abi
 from .controller import PidCoefficients, Tolerances, integral_controller
-from .dynamics import DeviceDynamics, as_device_dynamics, build_struct
+from .dynamics import MLP_TILE, DeviceDynamics, as_device_dynamics, build_struct, mlp_pad
 from .tableau import is_custom, method_of
 
 __all__ = ["DEFAULT_MAX_STEPS", "SolveStatus", "IvpBatch", "SolveStats", "Solution",
@@ -283,6 +283,11 @@ def solve(problem: IvpBatch, f, tableau=None, tol: Tolerances | None = None,
     dyn = as_device_dynamics(f, n, d)
     method = method_of(tableau)
     tol = tol if tol is not None else Tolerances()
+    if dyn.kind == "mlp" and (pad := mlp_pad(dyn)) is not None:
+        return _solve_mlp_padded(problem, pad, tableau, tol, controller, max_steps, dt0,
+                                 record_trace, mode=mode, order=order, cost_hint=cost_hint,
+                                 pipeline_chunks=pipeline_chunks,
+                                 with_refresh_map=with_refresh_map)
     controller = controller if controller is not None else integral_controller()
     keep = []
     a = _abi.SolveArgs()
@@ -382,6 +387,35 @@ def solve(problem: IvpBatch, f, tableau=None, tol: Tolerances | None = None,
                     status, d)
 
 
+def _pad_scale(D: int) -> float:
+    """Tolerance factor making the RMS error norm over the zero-padded
+    64-wide state equal the norm over the D real components."""
+    return float(np.sqrt(D / MLP_TILE))
+
+
+def _pad_tol(v, D: int, positive: bool = False):
+    if positive and np.any(np.asarray(v.cpu() if hasattr(v, "cpu") else v) <= 0):
+        raise ValueError("MLP dynamics narrower than 64 need atol > 0 (the zero-padded "
+                         "components would divide 0 by 0 in the error norm)")
+    return v * _pad_scale(D)
+
+
+def _solve_mlp_padded(problem, pad, tableau, tol, controller, max_steps, dt0, record_trace, **kw):
+    """solve() for an MLP narrower than the tensor-core tile: the same
+    solve on the zero-padded 64-wide state with sqrt(D/64)-scaled
+    tolerances (dynamics.mlp_pad), outputs sliced back to D."""
+    import copy
+
+    dyn64, D, _ = pad
+    p64 = copy.copy(problem)
+    p64.y0 = np.zeros((problem.batch_size, MLP_TILE))
+    p64.y0[:, :D] = problem.y0
+    tol64 = Tolerances(_pad_tol(tol.atol, D, positive=True), _pad_tol(tol.rtol, D))
+    sol = solve(p64, dyn64, tableau, tol64, controller, max_steps, dt0, record_trace, **kw)
+    ys = np.ascontiguousarray(sol.ys_flat.reshape(-1, MLP_TILE)[:, :D]).reshape(-1)
+    return Solution(ys, sol.offsets, sol.shared_len, sol.n_emitted, sol.stats, sol.status, D)
+
+
 def solve_joint(problem: IvpBatch, f, tableau=None, tol: Tolerances | None = None,
                 controller: PidCoefficients | None = None, max_steps: int = DEFAULT_MAX_STEPS,
                 dt0=None, record_trace: bool = False, *, mode: str = "exact") -> Solution:
@@ -443,6 +477,21 @@ def solve_device(y0, t_start, t_end, f, *, t_eval=None, t_eval_offsets=None, met
     y0 = y0.to(**f64).contiguous()
     n, d = y0.shape
     dyn = as_device_dynamics(f, n, d)
+    if dyn.kind == "mlp" and (pad := mlp_pad(dyn)) is not None:
+        # the zero-padded 64-wide solve (dynamics.mlp_pad), outputs sliced to D
+        dyn64, D, H = pad
+        y64 = torch.zeros((n, MLP_TILE), **f64)
+        y64[:, :D] = y0
+        out = solve_device(y64, t_start, t_end, dyn64, t_eval=t_eval, t_eval_offsets=t_eval_offsets,
+                           method=method, atol=_pad_tol(atol, D, positive=True), rtol=_pad_tol(rtol, D),
+                           controller=controller, max_steps=max_steps, dt0=dt0, order=order,
+                           cost_hint=cost_hint, mode=mode, record_trace=record_trace,
+                           stream=stream, threads_per_block=threads_per_block, blocks=blocks,
+                           prof_events=prof_events, with_refresh_map=with_refresh_map,
+                           record_trajectory=record_trajectory)
+        out["ys"] = out["ys"][:, :D].contiguous()
+        out["_mlp_pad"] = (D, H)
+        return out
     t_start = torch.as_tensor(t_start, **f64).expand(n).contiguous()
     t_end = torch.as_tensor(t_end, **f64).expand(n).contiguous()
     keep = [y0, t_start, t_end]
@@ -588,6 +637,18 @@ def adjoint_device(fwd: dict, grad_ys):
     lib = _abi.load()
     if "_args" not in fwd:
         raise ValueError("the forward solve was not recorded (record_trajectory=True)")
+    if "_mlp_pad" in fwd:  # the forward ran zero-padded to 64 (dynamics.mlp_pad)
+        D, H = fwd["_mlp_pad"]
+        g64 = torch.zeros((fwd["ys"].shape[0], MLP_TILE), dtype=torch.float64,
+                          device=fwd["n_emitted"].device)
+        g64[:, :D] = grad_ys.reshape(-1, D)
+        inner = {k: v for k, v in fwd.items() if k not in ("_mlp_pad", "ys")}
+        inner["ys"] = g64  # (only its shape is used)
+        gy0, gw = adjoint_device(inner, g64)
+        return gy0[:, :D].contiguous(), {"W1": gw["W1"][:H, :D].contiguous(),
+                                         "b1": gw["b1"][:H].contiguous(),
+                                         "W2": gw["W2"][:D, :H].contiguous(),
+                                         "b2": gw["b2"][:D].contiguous()}
     a = fwd["_args"]
     n, d = int(a.n), int(a.d)
     dev = fwd["n_emitted"].device

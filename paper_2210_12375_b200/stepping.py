@@ -89,7 +89,7 @@ class Stepper:
         S, fsal = int(tab.stages), bool(tab.fsal)
         prog = get_program("dopri5", dyn, d, UNITS)  # dynamics only; the tableau is data
         keep = []
-        dev = lambda a: (keep.append(torch.as_tensor(np.ascontiguousarray(a, dtype=np.float64))  # noqa: E731
+        dev = lambda a: (keep.append(torch.tensor(np.asarray(a, dtype=np.float64))  # noqa: E731
                                      .to("cuda")), keep[-1].data_ptr())[1]
         ds = build_struct(dyn, n, keep, device_arrays=dev)
         tt = dev(np.broadcast_to(np.asarray(t if t is not None else 0.0, dtype=float), (n,)))

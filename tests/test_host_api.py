@@ -180,11 +180,16 @@ def test_adjoint_abi_validation_without_gpu():
     a.joint = 1
     with pytest.raises(NotImplementedError):
         _abi.check(lib.bode_solve_adjoint(C.byref(a), C.byref(g)))
-    m = _valid_args("mlp", d=6, hidden=32)  # MLP widths outside the compiled set
-    with pytest.raises(NotImplementedError, match="MLP gradients"):
-        _abi.check(lib.bode_solve_adjoint(C.byref(m), C.byref(g)))
-    m = _valid_args("mlp", d=8, hidden=40)  # hidden not a multiple of 16
-    with pytest.raises(NotImplementedError, match="MLP gradients"):
+    # one MLP path: the 64-wide tensor-core tile (the facade zero-pads
+    # narrower networks, dynamics.mlp_pad); anything else is unsupported
+    for d, hidden in ((6, 32), (64, 40), (64, 288)):
+        m = _valid_args("mlp", d=d, hidden=hidden)
+        with pytest.raises(NotImplementedError, match="MLP dynamics"):
+            _abi.check(lib.bode_solve(C.byref(m)))
+        with pytest.raises(NotImplementedError, match="MLP dynamics"):
+            _abi.check(lib.bode_solve_adjoint(C.byref(m), C.byref(g)))
+    m = _valid_args("mlp", d=64, hidden=64)  # gradients need the recorded stage inputs
+    with pytest.raises(ValueError, match="traj_stages"):
         _abi.check(lib.bode_solve_adjoint(C.byref(m), C.byref(g)))
     r = _valid_args()
     r.traj = 0x1000  # recording without offsets

@@ -58,3 +58,13 @@ if which in ("all", "adjoint"):
     g0, gp = bode.adjoint_device(fwd, torch.ones_like(fwd["ys"]))
     torch.cuda.synchronize()
     print("adjoint ok", float(g0.abs().sum()))
+if which in ("all", "mlp_adjoint"):
+    # tensor-core MLP backward (D=64): fused recording with stage inputs,
+    # the VJP kernels and the split-K weight-gradient GEMM over 3 tiles
+    cfg = bench.make_config("c4", 0, n_override=300)
+    W = [torch.tensor(w, device="cuda") for w in cfg["mlp"]]
+    fwd = bode.solve_device(torch.tensor(cfg["y0"], **f64), 0.0, 1.0, bode.mlp_dynamics(*W),
+                            t_eval=torch.tensor([0.5, 1.0], **f64), record_trajectory=True)
+    g0, gw = bode.adjoint_device(fwd, torch.ones_like(fwd["ys"]))
+    torch.cuda.synchronize()
+    print("mlp adjoint ok", float(g0.abs().sum()), float(gw["W1"].abs().sum()))
