@@ -691,19 +691,21 @@ __global__ void __launch_bounds__(256, 1) wg_kernel(const WgArgs A) {
   // TMEM: dW1|db1 half h at columns 80 h (M = 128: row = hidden unit);
   // dW2|db2 at columns 160 (M = 64: row = output; half 0 in lanes 0-15,
   // half 1 in lanes 16-31 of each quadrant)
-  WgRegs R;
-  {
+  // slice i of this CTA = blockIdx.x + i * gridDim.x; the loads of slices
+  // i+1 and i+2 are in flight (two register sets) while slice i is stored
+  auto fetch = [&](int i, WgRegs& R) {
+    const int sl = (int)blockIdx.x + i * (int)gridDim.x;
+    if (sl >= nslices) return;
     int64_t c0, cmax;
-    slice_cols(blockIdx.x, c0, cmax);
+    slice_cols(sl, c0, cmax);
     wg_fetch_all(T, two, c0, cmax, R);
-  }
-  int i = 0;
-  for (int sl = blockIdx.x; sl < nslices; sl += gridDim.x, i++) {
+  };
+  auto step = [&](int i, WgRegs& R) {
     const int b = i & 1;
     if (i >= 2) mbar_wait(&S.done[b], ((i - 2) >> 1) & 1);  // MMAs of slice i-2 read stage b
     uint8_t* st = reinterpret_cast<uint8_t*>(&S.st[b]);
     int64_t c0, cmax;
-    slice_cols(sl, c0, cmax);
+    slice_cols((int)blockIdx.x + i * (int)gridDim.x, c0, cmax);
     wg_store_all(T, two, st, c0, cmax, R);
     fence_async_smem();
     fence_before();
@@ -728,10 +730,17 @@ __global__ void __launch_bounds__(256, 1) wg_kernel(const WgArgs A) {
         }
       mma_commit(&S.done[b]);
     }
-    if (sl + (int)gridDim.x < nslices) {  // next slice's loads overlap these MMAs
-      slice_cols(sl + gridDim.x, c0, cmax);
-      wg_fetch_all(T, two, c0, cmax, R);
-    }
+    fetch(i + 2, R);  // (the register set just stored)
+  };
+  const int mine = (nslices - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;
+  WgRegs R0, R1;
+  fetch(0, R0);
+  fetch(1, R1);
+  int i = 0;
+  while (i < mine) {
+    step(i++, R0);
+    if (i >= mine) break;
+    step(i++, R1);
   }
   if (i >= 1) mbar_wait(&S.done[(i - 1) & 1], ((i - 1) >> 1) & 1);  // the last slice's MMAs
   fence_after();
