@@ -500,6 +500,25 @@ def run_bode(args, rank, world, local_rank):
                    d2h_bytes_per_step=int(d2h), ms_per_step=1e3 * tot / len(e2e_t),
                    path="paper_2210_12375_b200.solve -> bode_solve_host (NumPy arrays in "
                         "page-locked host memory, outputs page-locked)")
+        if not strong and 8 * pts * d > 1e9:
+            # the same call with ys left on the device (solve(..., device_ys=True)):
+            # inputs up, statistics down -- for callers that consume the dense
+            # output on the GPU (C3: 6.3 GB of ys otherwise cross PCIe)
+            dv_t = []
+            for _ in range(max(1, min(args.steps, 3))):
+                flush.zero_()
+                torch.cuda.synchronize(dev)
+                t0 = time.perf_counter()
+                sol = bode.solve(prob, dyn_h, device_ys=True, **kw)
+                acc_dv = int(sol.stats.n_accepted.sum())
+                dv_t.append(time.perf_counter() - t0)
+                del sol
+            e2e["device_ys"] = dict(value=acc_dv / float(np.mean(dv_t)), unit="instance-steps/s",
+                                    ms_per_step=1e3 * float(np.mean(dv_t)),
+                                    h2d_bytes_per_step=int(h2d),
+                                    d2h_bytes_per_step=int(n * 40 + 8),
+                                    path="paper_2210_12375_b200.solve(device_ys=True) -> "
+                                         "solve_device (ys stay in HBM)")
 
     # ---- CPU baseline (rank 0, N=1 only)
     cpu = None

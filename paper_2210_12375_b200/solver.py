@@ -273,11 +273,20 @@ def solve(problem: IvpBatch, f, tableau=None, tol: Tolerances | None = None,
           controller: PidCoefficients | None = None, max_steps: int = DEFAULT_MAX_STEPS,
           dt0=None, record_trace: bool = False, *, mode: str = "exact", order=None,
           cost_hint=None, pipeline_chunks="auto", with_refresh_map: bool = False,
-          _joint: bool = False) -> Solution:
+          device_ys: bool = False, _joint: bool = False) -> Solution:
     """Integrate every instance independently with adaptive steps on the GPU
-    (reference ``solve``, solver.py:352-369), host arrays in and out."""
+    (reference ``solve``, solver.py:352-369), host arrays in and out.
+    ``device_ys=True``: the same solve, but ``Solution.ys_flat`` (and the
+    ``ys`` rows) stay on the GPU as a torch tensor -- only the inputs go up
+    and the statistics / statuses come back (for callers that consume the
+    dense output on the device; torchode's semantics)."""
     if max_steps < 1:
         raise ValueError("max_steps must be at least 1")
+    if device_ys:
+        if _joint or record_trace or with_refresh_map:
+            raise ValueError("device_ys: independent solve without trace / refresh map")
+        return _solve_device_ys(problem, f, tableau, tol, controller, max_steps, dt0, mode,
+                                order, cost_hint)
     lib = _abi.load()
     n, d = problem.batch_size, problem.n_features
     dyn = as_device_dynamics(f, n, d)
@@ -385,6 +394,38 @@ def solve(problem: IvpBatch, f, tableau=None, tol: Tolerances | None = None,
         offs = None
     return Solution(ys[:n_rows], offs, te.size if problem.te_shared else 0, n_emitted, stats,
                     status, d)
+
+
+def _solve_device_ys(problem, f, tableau, tol, controller, max_steps, dt0, mode, order,
+                     cost_hint) -> Solution:
+    """solve(..., device_ys=True): host inputs uploaded, solve_device, the
+    statistics downloaded, ys left on the device."""
+    import torch
+
+    dev = torch.device("cuda", torch.cuda.current_device())
+    T = lambda x: None if x is None else torch.as_tensor(np.asarray(x)).to(dev, non_blocking=True)  # noqa: E731
+    n, d = problem.batch_size, problem.n_features
+    tol = tol if tol is not None else Tolerances()
+    tv = T(problem.te_values) if problem.te_values.size else None
+    offs = None if problem.te_shared or tv is None else T(problem.te_offsets)
+    tv2 = tv
+    atol = tol.atol if np.ndim(tol.atol) == 0 else T(np.asarray(tol.atol, dtype=float))
+    rtol = tol.rtol if np.ndim(tol.rtol) == 0 else T(np.asarray(tol.rtol, dtype=float))
+    d0 = dt0 if dt0 is None or np.ndim(dt0) == 0 else T(np.asarray(dt0, dtype=float))
+    out = solve_device(T(problem.y0), T(problem.t_start), T(problem.t_end), f, t_eval=tv2,
+                       t_eval_offsets=offs, method=tableau if tableau is not None else "dopri5",
+                       atol=atol, rtol=rtol, controller=controller, max_steps=max_steps, dt0=d0,
+                       order=None if order is None else T(np.asarray(order, dtype=np.int64)),
+                       cost_hint=None if cost_hint is None else T(np.asarray(cost_hint, dtype=float)),
+                       mode=mode)
+    h = {k: out[k].cpu().numpy() for k in ("n_emitted", "n_steps", "n_accepted", "final_dt",
+                                           "status", "n_f_evals")}
+    stats = SolveStats(n_steps=h["n_steps"], n_accepted=h["n_accepted"],
+                       n_f_evals=np.broadcast_to(h["n_f_evals"], (n,)), final_dt=h["final_dt"],
+                       extra={})
+    shared = problem.te_values.size if problem.te_shared else 0
+    return Solution(out["ys"].reshape(-1), None if problem.te_shared or tv is None
+                    else problem.te_offsets, shared, h["n_emitted"], stats, h["status"], d)
 
 
 def _pad_scale(D: int) -> float:

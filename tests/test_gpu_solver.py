@@ -320,3 +320,30 @@ def test_mlp_matches_oracle_at_scale():
     assert np.mean(sol.stats.n_steps == ref["n_steps"]) > 0.9
     a, b = sol.ys_flat.reshape(n, -1), ref["ys"].reshape(n, -1)
     assert np.max(np.abs(a - b).max(axis=1) / np.abs(b).max(axis=1)) < 1e-4
+
+
+@pytest.mark.parametrize("te", ["shared", "ragged"])
+def test_solve_device_ys_equals_host_ys(te):
+    """solve(..., device_ys=True) is the same solve with ys left on the
+    device: ys bitwise equal to the host-buffer solve, same statistics."""
+    import torch
+
+    rng = np.random.default_rng(21)
+    n = 3000
+    mu = rng.uniform(1.0, 10.0, n)
+    t1 = rng.uniform(3.0, 8.0, n)
+    tev = (np.linspace(0.0, 3.0, 7) if te == "shared"
+           else [np.sort(rng.uniform(0.0, t1[i], i % 5)) for i in range(n)])
+    prob = bode.IvpBatch(np.tile([2.0, 0.0], (n, 1)), np.zeros(n), t1, tev)
+    f = bode.vdp_dynamics(bode.VdpParams(mu))
+    kw = dict(controller=bode.pid_controller("PI42"), mode="fast", cost_hint=mu * t1)
+    a = bode.solve(prob, f, **kw)
+    b = bode.solve(prob, f, device_ys=True, **kw)
+    assert isinstance(b.ys_flat, torch.Tensor) and b.ys_flat.is_cuda
+    assert np.array_equal(a.ys_flat.reshape(-1), b.ys_flat.cpu().numpy().reshape(-1))
+    for k in ("n_steps", "n_accepted", "final_dt"):
+        assert np.array_equal(getattr(a.stats, k), getattr(b.stats, k)), k
+    assert np.array_equal(a.status, b.status) and np.array_equal(a.n_emitted, b.n_emitted)
+    assert np.array_equal(a.stats.n_f_evals, b.stats.n_f_evals)
+    i = int(np.argmax(a.n_emitted))
+    assert np.array_equal(a.ys[i], b.ys[i].cpu().numpy())
