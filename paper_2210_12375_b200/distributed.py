@@ -57,14 +57,31 @@ def combine_f_evals(max_iterations, refresh_maps, stages: int, fsal: bool) -> in
     return int(1 + (stages - 1) * mx + union[1:mx].sum())
 
 
+def _csr_rows(offs: np.ndarray, idx: np.ndarray):
+    """Row indices (into a CSR array with offsets ``offs``) of instances
+    ``idx`` in that order, and the shard's own offsets -- vectorised."""
+    counts = offs[idx + 1] - offs[idx]
+    sub = np.zeros(len(idx) + 1, np.int64)
+    np.cumsum(counts, out=sub[1:])
+    rows = np.repeat(offs[idx] - sub[:-1], counts) + np.arange(int(sub[-1]), dtype=np.int64)
+    return rows, sub
+
+
 def subset_problem(problem: IvpBatch, idx) -> IvpBatch:
-    idx = np.asarray(idx)
+    """The instances ``idx`` of a validated batch (no per-instance Python
+    work: the evaluation points are sliced as CSR rows)."""
+    idx = np.asarray(idx, dtype=np.int64)
+    sub = IvpBatch.__new__(IvpBatch)
+    sub.y0 = problem.y0[idx]
+    sub.t_start, sub.t_end = problem.t_start[idx], problem.t_end[idx]
+    sub._te_list = None
+    sub.te_shared = problem.te_shared
     if problem.te_shared:
-        te = problem.te_values
+        sub.te_values, sub.te_offsets = problem.te_values, None
     else:
-        o = problem.te_offsets
-        te = [problem.te_values[o[i]:o[i + 1]] for i in idx]
-    return IvpBatch(problem.y0[idx], problem.t_start[idx], problem.t_end[idx], te)
+        rows, offs = _csr_rows(problem.te_offsets, idx)
+        sub.te_values, sub.te_offsets = problem.te_values[rows], offs
+    return sub
 
 
 def solve_sharded(problem: IvpBatch, f, *, group=None, cost_hint=None, gather_to: int | None = 0,
@@ -106,43 +123,44 @@ def solve_sharded(problem: IvpBatch, f, *, group=None, cost_hint=None, gather_to
     if gather_to is None:
         return idx, sol
     # results travel as tensors (NCCL on the GPU box, gloo on CPU): one
-    # (rows, 6) record per instance and the shard's flat ys rows
+    # (rows, 6) record per instance and the shard's flat ys rows (its CSR
+    # layout; rows past an instance's n_emitted are never read)
     k, d = len(idx), problem.n_features
     rec = np.empty((k, 6), np.int64)
     rec[:, 0] = idx
     rec[:, 1], rec[:, 2] = sol.stats.n_steps, sol.stats.n_accepted
     rec[:, 3] = np.asarray(sol.stats.final_dt, np.float64).view(np.int64)
     rec[:, 4], rec[:, 5] = sol.status, sol.n_emitted
-    flat = np.zeros((0, d)) if k == 0 else np.concatenate(
-        [np.asarray(y, np.float64).reshape(-1, d) for y in sol.ys])
+    flat = np.ascontiguousarray(np.asarray(sol.ys_flat, np.float64).reshape(-1, d))
     recs = gather_rows(torch.from_numpy(rec).to(dev), gather_to, group)
-    ys_all = gather_rows(torch.from_numpy(np.ascontiguousarray(flat)).to(dev), gather_to, group)
+    ys_all = gather_rows(torch.from_numpy(flat).to(dev), gather_to, group)
     if rank != gather_to:
         return None
-    recs = [r.cpu().numpy() for r in recs]
-    ys_all = [y.cpu().numpy() for y in ys_all]
-    ys = [None] * n
+    counts = problem.eval_counts()
+    offs = np.zeros(n + 1, np.int64)
+    np.cumsum(counts, out=offs[1:])
+    out = np.empty((int(offs[-1]), d))
     n_steps = np.zeros(n, np.int64)
     n_acc = np.zeros(n, np.int64)
     fdt = np.zeros(n)
     status = np.zeros(n, np.int64)
     n_emit = np.zeros(n, np.int64)
-    for r, y in zip(recs, ys_all):
+    for r, y in zip(recs, ys_all):  # one vectorised scatter per rank
+        r, y = r.cpu().numpy(), y.cpu().numpy()
         ids = r[:, 0]
         n_steps[ids], n_acc[ids], status[ids], n_emit[ids] = r[:, 1], r[:, 2], r[:, 4], r[:, 5]
         fdt[ids] = r[:, 3].view(np.float64)
-        o = np.concatenate([[0], np.cumsum(r[:, 5])])
-        for j, i in enumerate(ids):
-            ys[i] = y[o[j]:o[j + 1]]
-    counts = problem.eval_counts()
-    offs = np.zeros(n + 1, np.int64)
-    np.cumsum(counts, out=offs[1:])
-    flat = np.full((int(offs[-1]), d), np.nan)
-    for i in range(n):
-        flat[offs[i]:offs[i] + len(ys[i])] = ys[i]
+        if problem.te_shared:
+            m = counts[0] if n else 0
+            out.reshape(n, m, d)[ids] = y.reshape(len(ids), m, d)
+        elif len(ids):
+            rows, _ = _csr_rows(offs, ids)
+            out[rows] = y[:len(rows)]
     stats = SolveStats(n_steps=n_steps, n_accepted=n_acc,
                        n_f_evals=np.full(n, nfe, dtype=np.int64), final_dt=fdt)
-    return Solution(flat, offs, 0, n_emit, stats, status, d)
+    if problem.te_shared:
+        return Solution(out.reshape(-1), None, int(counts[0]) if n else 0, n_emit, stats, status, d)
+    return Solution(out, offs, 0, n_emit, stats, status, d)
 
 
 def gather_rows(t, dst: int = 0, group=None):
