@@ -235,12 +235,17 @@ struct VjpArgs {
   float *uT, *AT, *YT, *gT;  // blocked (rows, S * pmax), column = stage * pmax + row
 };
 
-// Y_s / g_s tiles in shared memory; the weights of two hidden chunks in
-// flight (buffer = chunk sequence number & 1); u_c lives in TMEM (the A
-// operand of the Yb GEMM), so the epilogue never writes shared memory
+// Every A operand lives in tensor memory (tcgen05.mma's A-from-TMEM form:
+// one row per lane, K along the columns), so the MMAs read only the weights
+// from shared memory -- N = 32 MMAs with both operands in shared memory are
+// bound by its operand bandwidth.  TMEM columns (512):
+//   0 / 64      Y_s hi / lo          128 / 192   g_s hi / lo
+//   256 + 64 b  chunk buffer b: Z | V accumulators (32 + 32), overwritten
+//               by the epilogue with u_c hi | lo (the A of the Yb GEMM)
+//   384         Yb accumulator (64)
+// Shared memory holds the weights of two hidden chunks in flight (buffer =
+// chunk sequence number & 1).
 struct VjpSmem {
-  uint8_t ay[2][kATile];     // Y_s hi, lo
-  uint8_t ag[2][kATile];     // g_s hi, lo
   uint8_t w1[2][2][kW1];     // [buf] W1_c hi, lo
   uint8_t wv[2][2][kW1];     // [buf] (W2^T)_c hi, lo
   uint8_t wy[2][2][kW2];     // [buf] (W1^T)_c hi, lo
@@ -255,13 +260,13 @@ __device__ __forceinline__ void rows_sync() {  // the 256 row-owner threads
 }
 
 // Production of one tile row's half (columns [32 h, 32 h + 32)) of the
-// stage input Y_s and of g_s = dL/dk_s, into the shared-memory TF32 hi/lo
-// tiles and the transposed global copies.  Y_s is the recorded stage input
+// stage input Y_s and of g_s = dL/dk_s, into the TMEM TF32 hi/lo operand
+// columns of the row's lane (trow) and the transposed global copies.  Y_s is the recorded stage input
 // (Y_0 = y_old); g_s is the seed plus, in the order the stages were
 // reversed (S-1 down to s+1), h a_s's dL/dY_s'.
 template <int M>
-__device__ __forceinline__ void vjp_produce(const VjpArgs& A, int64_t p, bool lv, int r, int h,
-                                            VjpSmem& S) {
+__device__ __forceinline__ void vjp_produce(const VjpArgs& A, int64_t p, bool lv, int h,
+                                            uint32_t trow) {
   using T = Tab<M>;
   const int stage = A.stage;
   const int64_t col = (int64_t)stage * A.pmax + p;
@@ -322,21 +327,21 @@ __device__ __forceinline__ void vjp_produce(const VjpArgs& A, int64_t p, bool lv
       A.gT[blk(c0 + e, col, kD)] = g[e];
     }
   }
+  // TF32 hi / lo of this half into the A-operand columns (lane = row)
 #pragma unroll
-  for (int q = 0; q < 8; q++) {
-    const uint32_t o = cm_off(r, c0 + 4 * q, kD);
-    const float* xs = x + 4 * q;
-    const float* gs = g + 4 * q;
-    float4 hi, lo;
-    hi.x = tf32_hi(xs[0]), hi.y = tf32_hi(xs[1]), hi.z = tf32_hi(xs[2]), hi.w = tf32_hi(xs[3]);
-    lo.x = xs[0] - hi.x, lo.y = xs[1] - hi.y, lo.z = xs[2] - hi.z, lo.w = xs[3] - hi.w;
-    *reinterpret_cast<float4*>(S.ay[0] + o) = hi;
-    *reinterpret_cast<float4*>(S.ay[1] + o) = lo;
-    hi.x = tf32_hi(gs[0]), hi.y = tf32_hi(gs[1]), hi.z = tf32_hi(gs[2]), hi.w = tf32_hi(gs[3]);
-    lo.x = gs[0] - hi.x, lo.y = gs[1] - hi.y, lo.z = gs[2] - hi.z, lo.w = gs[3] - hi.w;
-    *reinterpret_cast<float4*>(S.ag[0] + o) = hi;
-    *reinterpret_cast<float4*>(S.ag[1] + o) = lo;
+  for (int q = 0; q < 4; q++) {
+    const float* v = q < 2 ? x + 16 * q : g + 16 * (q - 2);
+    float hi[16], lo[16];
+#pragma unroll
+    for (int e = 0; e < 16; e++) {
+      hi[e] = tf32_hi(v[e]);
+      lo[e] = v[e] - hi[e];
+    }
+    const uint32_t col = (q < 2 ? 0 : 128) + c0 + 16 * (q & 1);
+    tmem_st16(trow + col, hi);
+    tmem_st16(trow + col + 64, lo);
   }
+  tmem_wait_st();
 }
 
 // One CTA per SM, tiles of 128 rows; warps 0-3 and 4-7 own the rows (thread
@@ -379,7 +384,7 @@ __global__ void __launch_bounds__(kVjpThreads, 1) vjp_kernel(const VjpArgs A) {
   // TMEM columns: Z / V accumulators of chunk buffer b at 64 b / 64 b + 32,
   // Yb at 128, u_c hi / lo of buffer b at 192 + 64 b / 192 + 64 b + 32
   const uint32_t tmem = S.tmem_base;
-  const uint32_t accY = tmem + 128;
+  const uint32_t accY = tmem + 384;
   auto phase = [](int q) { return (uint32_t)((q >> 1) & 1); };
 
   if (warp == 8) {
@@ -401,21 +406,22 @@ __global__ void __launch_bounds__(kVjpThreads, 1) vjp_kernel(const VjpArgs A) {
         bulk_g2s(S.wy[b][0], wa + (size_t)c * kWChunk + 2 * kW1, kW2, &S.wy_full[b]);
         bulk_g2s(S.wy[b][1], wa + (size_t)c * kWChunk + 2 * kW1 + kW2, kW2, &S.wy_full[b]);
       };
-      const int ta[3] = {0, 0, 1}, tb[3] = {0, 1, 0};
+      const int tb[3] = {0, 1, 0};
       auto issue_zv = [&](int q) {  // Z = Y_s W1_c^T, V = g_s (W2^T)_c^T into buffer q & 1
         const int b = q & 1;
         mbar_wait(&S.wa[b], phase(q));
-        if (q >= 2) mbar_wait(&S.epi[b], phase(q - 2));  // epilogue(q-2) read this buffer
+        if (q >= 2) mbar_wait(&S.g2[b], phase(q - 2));  // Yb(q-2) read u from this buffer
         fence_after();
-        const uint32_t az = tmem + 64 * b, av = az + 32;
+        const uint32_t az = tmem + 256 + 64 * b, av = az + 32;
+        const uint32_t ya[3] = {tmem, tmem, tmem + 64}, ga[3] = {tmem + 128, tmem + 128, tmem + 192};
 #pragma unroll
         for (int s = 0; s < kD / 8; s++)
 #pragma unroll
           for (int term = 0; term < 3; term++) {
-            mma_tf32(az, smem_desc(smem_u32(S.ay[ta[term]]) + 256 * s, 2048),
-                     smem_desc(smem_u32(S.w1[b][tb[term]]) + 256 * s, 2048), idesc(kHc), (term | s) ? 1u : 0u);
-            mma_tf32(av, smem_desc(smem_u32(S.ag[ta[term]]) + 256 * s, 2048),
-                     smem_desc(smem_u32(S.wv[b][tb[term]]) + 256 * s, 2048), idesc(kHc), (term | s) ? 1u : 0u);
+            mma_tf32_ts(az, ya[term] + 8 * s, smem_desc(smem_u32(S.w1[b][tb[term]]) + 256 * s, 2048),
+                        idesc(kHc), (term | s) ? 1u : 0u);
+            mma_tf32_ts(av, ga[term] + 8 * s, smem_desc(smem_u32(S.wv[b][tb[term]]) + 256 * s, 2048),
+                        idesc(kHc), (term | s) ? 1u : 0u);
           }
         mma_commit(&S.g1[b]);
       };
@@ -424,7 +430,7 @@ __global__ void __launch_bounds__(kVjpThreads, 1) vjp_kernel(const VjpArgs A) {
         mbar_wait(&S.epi[b], phase(q));
         mbar_wait(&S.wy_full[b], phase(q));
         fence_after();
-        const uint32_t uhi = tmem + 192 + 64 * b, ulo = uhi + 32;
+        const uint32_t uhi = tmem + 256 + 64 * b, ulo = uhi + 32;
 #pragma unroll
         for (int s = 0; s < kHc / 8; s++) {
           const uint64_t wh = smem_desc(smem_u32(S.wy[b][0]) + 256 * s, 1024);
@@ -475,23 +481,22 @@ __global__ void __launch_bounds__(kVjpThreads, 1) vjp_kernel(const VjpArgs A) {
       // (Y_s / g_s tiles free: every ZV of the previous tile was waited for
       // by its last epilogue; the previous Yb was read out below)
       if (tid == 0) { ADJ_STAMP(0, 1) }
-      vjp_produce<M>(A, p, live, r, h, S);
-      fence_async_smem();
+      vjp_produce<M>(A, p, live, h, tmem + lane_off);
+      fence_before();
       rows_sync();
       if (tid == 0) mbar_arrive(&S.full);
       if (tid == 0) { ADJ_STAMP(0, 2) }
       const int q0 = kl * nchunk;
       for (int c = 0; c < nchunk; c++) {
         const int q = q0 + c, b = q & 1;
-        mbar_wait(&S.g1[b], phase(q));
-        if (q >= 2) mbar_wait(&S.g2[b], phase(q - 2));  // u buffer b free
+        mbar_wait(&S.g1[b], phase(q));  // Z / V of this chunk (Yb(q-2) had left the buffer)
         fence_after();
         if (tid == 0) { ADJ_STAMP(0, 3) }
         // ---- tanh, u = V (1 - tanh^2) -> TMEM (hi, lo); u^T, tanh^T
         {
           float z[16], v[16], uh[16], ul[16];
-          tmem_ld16(tmem + 64 * b + 16 * h + lane_off, z);
-          tmem_ld16(tmem + 64 * b + 32 + 16 * h + lane_off, v);
+          tmem_ld16(tmem + 256 + 64 * b + 16 * h + lane_off, z);
+          tmem_ld16(tmem + 256 + 64 * b + 32 + 16 * h + lane_off, v);
           const int c16 = (q % nchunk) * kHc + 16 * h;
 #pragma unroll
           for (int j = 0; j < 16; j++) {
@@ -504,7 +509,8 @@ __global__ void __launch_bounds__(kVjpThreads, 1) vjp_kernel(const VjpArgs A) {
               A.AT[blk(c16 + j, col, A.H)] = a;
             }
           }
-          const uint32_t ub = tmem + 192 + 64 * b + 16 * h + lane_off;
+          // u hi / lo over this thread's own Z / V columns (read above)
+          const uint32_t ub = tmem + 256 + 64 * b + 16 * h + lane_off;
           tmem_st16(ub, uh);
           tmem_st16(ub + 32, ul);
           tmem_wait_st();
