@@ -263,6 +263,12 @@ int run_chunk(const bode_solve_args* a, int64_t lo, int64_t hi, const Layout& L,
     if (e != cudaSuccess) return cuda_fail(e, "LPT order");
     P.order = order;
   }
+  if (P.rec && P.order) {  // record positions (the te_next buffer is unused with records)
+    int64_t* inv = reinterpret_cast<int64_t*>(P.te_next);
+    if ((e = inverse_order(P.order, n, inv, st)) != cudaSuccess) return cuda_fail(e, "record order");
+    P.rec_pos = inv;
+    g_launches += 1;
+  }
   if (a->joint) {
     g_launches += 1;
     e = joint_solve(a->method, a->mode, a->dyn.kind, d, P, ws + L.f0, a->n_f_evals, st,

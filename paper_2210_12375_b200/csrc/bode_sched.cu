@@ -153,4 +153,18 @@ cudaError_t shard_partition(const double* cost, int64_t n, int32_t world, int64_
   return cudaGetLastError();
 }
 
+namespace {
+__global__ void inverse_order_kernel(const int64_t* order, int64_t n, int64_t* inv) {
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n;
+       q += (int64_t)gridDim.x * blockDim.x)
+    inv[order[q]] = q;
+}
+}  // namespace
+
+cudaError_t inverse_order(const int64_t* order, int64_t n, int64_t* inv, cudaStream_t st) {
+  const int64_t nb = (n + 255) / 256;
+  inverse_order_kernel<<<(unsigned)(nb < 148 * 16 ? nb : 148 * 16), 256, 0, st>>>(order, n, inv);
+  return cudaGetLastError();
+}
+
 }  // namespace bode

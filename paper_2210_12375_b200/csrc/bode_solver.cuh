@@ -66,6 +66,7 @@ struct SolveParams {
   // per-instance fields through the order permutation
   double* rec;
   int32_t rec_stride;
+  const int64_t* rec_pos;      // queue position of instance i (NULL: i)
   void* ev_start;              // host side only: optional cudaEvent_t around
   void* ev_stop;               // the persistent launch (bench roofline)
 };
@@ -200,9 +201,12 @@ struct Lane {
     }
   }
 
-  // the resume record of queue position pos (P.rec), after initialize()
+  // the resume record of queue position pos (P.rec), after initialize():
+  // assembled in registers and written as whole 32-byte sectors (256-bit
+  // stores) -- the positions are scattered, partial-sector writes are not
   __device__ __forceinline__ void write_record(const SolveParams& P, int64_t pos) const {
-    double* r = P.rec + pos * P.rec_stride;
+    constexpr int NR = (kRecY + 2 * D + 8 + 3) / 4 * 4;  // (n_inst <= 8)
+    double r[NR];
     const double* te = te_of(P);
     r[kRecT] = t;
     r[kRecTEnd] = t_end;
@@ -219,7 +223,21 @@ struct Lane {
       r[kRecY + c] = y[c];
       r[kRecY + D + c] = k[0][c];
     }
-    for (int q = 0; q < P.dyn.n_inst; q++) r[kRecY + 2 * D + q] = P.dyn.inst[idx * P.dyn.n_inst + q];
+#pragma unroll
+    for (int q = 0; q < 8; q++)
+      r[kRecY + 2 * D + q] = q < P.dyn.n_inst ? P.dyn.inst[idx * P.dyn.n_inst + q] : 0.0;
+    double* dst = P.rec + pos * P.rec_stride;
+#pragma unroll
+    for (int q = 0; q < NR; q += 4)
+      if (q < P.rec_stride) {
+#ifdef __CUDACC_RTC__  // (run-time programs: the runtime NVRTC's PTX has no 256-bit vectors)
+        reinterpret_cast<double2*>(dst + q)[0] = make_double2(r[q], r[q + 1]);
+        reinterpret_cast<double2*>(dst + q)[1] = make_double2(r[q + 2], r[q + 3]);
+#else
+        asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(dst + q), "d"(r[q]),
+                     "d"(r[q + 1]), "d"(r[q + 2]), "d"(r[q + 3]) : "memory");
+#endif
+      }
   }
 
   // pick up the row of queue position pos from its record; returns the
@@ -511,12 +529,12 @@ __global__ void __launch_bounds__(128, ((F::D <= 2 && (!REC || PI)) ? BODE_BLOCK
 template <int M, class F, class O>
 __global__ void __launch_bounds__(128) bode_init_kernel(const SolveParams P) {
   Lane<M, F, O> L;
-  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < P.n;
-       q += (int64_t)gridDim.x * blockDim.x) {
-    // with resume records: queue position q (records written in queue order)
-    const int64_t i = (P.rec && P.order) ? P.order[q] : q;
+  // instances in their natural order (coalesced per-instance reads and
+  // writes); each resume record goes to its queue position (whole sectors)
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < P.n;
+       i += (int64_t)gridDim.x * blockDim.x) {
     L.initialize(P, i);
-    if (P.rec) L.write_record(P, q);
+    if (P.rec) L.write_record(P, P.rec_pos ? P.rec_pos[i] : i);
   }
 }
 
