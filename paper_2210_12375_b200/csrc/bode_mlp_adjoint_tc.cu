@@ -591,7 +591,11 @@ __device__ __forceinline__ void wg_fetch(WgTile T, int64_t c0, int64_t cmax,
     float4 x = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
     if (e < TROWS * (kWgK / 4)) {
       if (r < T.nrows)  // (src: this slice's half of a 32-column block, row-major)
-        x = __ldg(reinterpret_cast<const float4*>(T.src + (int64_t)r * 32 + 4 * k4));
+        // (.L2::128B: the whole 128-byte block row comes into L2 -- this
+        // CTA reads its other half in the next slice)
+        asm volatile("ld.global.nc.L2::128B.v4.f32 {%0, %1, %2, %3}, [%4];"
+                     : "=f"(x.x), "=f"(x.y), "=f"(x.z), "=f"(x.w)
+                     : "l"(T.src + (int64_t)r * 32 + 4 * k4));
       else if (r == T.ones)
         x = make_float4(1.0f, 1.0f, 1.0f, 1.0f);
     }
@@ -663,7 +667,12 @@ __global__ void __launch_bounds__(256, 1) wg_kernel(const WgArgs A) {
   const int cnt = *A.count;
   const int per_stage = (cnt + kWgK - 1) / kWgK;
   const int nslices = A.S * per_stage;
-  if ((int)blockIdx.x >= nslices) return;
+  // this CTA's slices: a contiguous range (consecutive slices are the two
+  // halves of one 32-column block)
+  const int per_cta = (nslices + (int)gridDim.x - 1) / (int)gridDim.x;
+  const int first = (int)blockIdx.x * per_cta;
+  const int last = first + per_cta < nslices ? first + per_cta : nslices;
+  if (first >= nslices) return;
   const int halves = A.H > 128 ? 2 : 1;
   if (tid == 0) {
     mbar_init(&S.done[0], 1);
@@ -700,8 +709,8 @@ __global__ void __launch_bounds__(256, 1) wg_kernel(const WgArgs A) {
   // slice i of this CTA = blockIdx.x + i * gridDim.x; the loads of slices
   // i+1 and i+2 are in flight (two register sets) while slice i is stored
   auto fetch = [&](int i, WgRegs& R) {
-    const int sl = (int)blockIdx.x + i * (int)gridDim.x;
-    if (sl >= nslices) return;
+    const int sl = first + i;
+    if (sl >= last) return;
     int64_t c0, cmax;
     slice_cols(sl, c0, cmax);
     wg_fetch_all(T, two, c0, cmax, R);
@@ -711,7 +720,7 @@ __global__ void __launch_bounds__(256, 1) wg_kernel(const WgArgs A) {
     if (i >= 2) mbar_wait(&S.done[b], ((i - 2) >> 1) & 1);  // MMAs of slice i-2 read stage b
     uint8_t* st = reinterpret_cast<uint8_t*>(&S.st[b]);
     int64_t c0, cmax;
-    slice_cols((int)blockIdx.x + i * (int)gridDim.x, c0, cmax);
+    slice_cols(first + i, c0, cmax);
     wg_store_all(T, two, st, c0, cmax, R);
     fence_async_smem();
     fence_before();
@@ -738,7 +747,7 @@ __global__ void __launch_bounds__(256, 1) wg_kernel(const WgArgs A) {
     }
     fetch(i + 2, R);  // (the register set just stored)
   };
-  const int mine = (nslices - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;
+  const int mine = last - first;
   WgRegs R0, R1;
   fetch(0, R0);
   fetch(1, R1);
