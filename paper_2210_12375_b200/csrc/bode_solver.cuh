@@ -396,8 +396,12 @@ struct Lane {
       double out[D];
       interpolate<T, D, O>(k, y, h, theta, out);
       if (ys) {
+        if (D == 2 && (reinterpret_cast<unsigned long long>(ys) & 15) == 0) {  // one 16-byte store
+          reinterpret_cast<double2*>(ys)[cursor] = make_double2(out[0], out[D - 1]);
+        } else {
 #pragma unroll
-        for (int c = 0; c < D; c++) ys[cursor * D + c] = out[c];
+          for (int c = 0; c < D; c++) ys[cursor * D + c] = out[c];
+        }
       }
       cursor++;
       if (cursor < m) te_next = te[cursor];
