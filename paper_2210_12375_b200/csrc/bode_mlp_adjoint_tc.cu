@@ -2,10 +2,11 @@
 // torchode's AutoDiffAdjoint for f(y) = W2 tanh(W1 y + b1) + b2) with every
 // contraction on the 5th-generation tensor cores.
 //
-// Same definition as the CUDA-core kernel (bode_mlp_adjoint.cu): reverse mode
+// Same definition as the analytic adjoint (bode_adjoint.cu): reverse mode
 // through the recorded accepted steps -- stages, solution update, dense
 // output -- with step sizes and accept decisions held fixed; outputs dL/dy0
-// per instance and dL/dW1, db1, dW2, db2 summed over the batch.
+// per instance and dL/dW1, db1, dW2, db2 summed over the batch.  The network
+// fills the 64-wide tile (narrower ones are zero-padded by the caller).
 //
 // The rows are ordered by trajectory length, longest first (a stable radix
 // sort, so the order -- and every sum below -- is deterministic), and the
@@ -22,9 +23,12 @@
 //              V  = g_s W2            (W2^T pre-split chunks, M=128 N=32 K=64)
 //              u  = V (1 - tanh(Z + b1)^2)         (epilogue, CUDA cores)
 //              Yb = sum_c u_c W1_c    (W1^T pre-split chunks, M=128 N=64 K=32)
-//            then dL/dk_j += h a_sj Yb (j < s), dL/dy_old += Yb;
-//            u^T, tanh^T, Y_s^T, g_s^T are written to global memory
-//            transposed (a warp of row threads writes 128 contiguous bytes)
+//            Y_s, g_s and u_c are the MMAs' A operands in TMEM; each stage's
+//            Yb is stored, and the later launches' producers form
+//            dL/dk_j = seed + sum h a_sj Yb (j < s); a fold pass adds the
+//            Yb to dL/dy_old; u^T, tanh^T, Y_s^T, g_s^T are written to global
+//            memory transposed (slice-contiguous blocks, 128 contiguous
+//            bytes per warp store)
 //   weights  one split-K tcgen05 GEMM over the iteration's (stage, row)
 //            columns: dW1 | db1 = u^T [Y | 1] (M=128 per half of H, N=80),
 //            dW2 | db2 = g^T [tanh | 1] (M=64, both halves interleaved in
@@ -839,7 +843,7 @@ __global__ void wg_reduce_kernel(const float* part, int parts, int H, float* gW1
 
 struct Layout {
   size_t total = 0;
-  size_t keys_in, keys, idx_in, order, cub, cub_bytes, count, hi0, hi1, lo, t_old, h, y, kb, rec, yb, Ybar,
+  size_t keys_in, keys, idx_in, order, cub, cub_bytes, count, hi, lo, t_old, h, y, kb, rec, yb, Ybar,
       uT, AT, YT, gT, wfwd, wadj, w1t, w2t, part;
   Layout(int64_t n, int64_t H, int S, int parts) {
     auto take = [&](size_t bytes) {
@@ -854,7 +858,7 @@ struct Layout {
                                               (int32_t*)nullptr, (int)n);
     keys_in = take(4 * n), keys = take(4 * n), idx_in = take(4 * n), order = take(4 * n);
     cub = take(cub_bytes), count = take(8);
-    hi0 = take(8 * n), hi1 = take(8 * n), lo = take(8 * n), t_old = take(8 * n), h = take(8 * n);
+    hi = take(8 * n), lo = take(8 * n), t_old = take(8 * n), h = take(8 * n);
     y = take(8 * n * kD), kb = take(8 * (size_t)S * n * kD), rec = take(8 * n);
     Ybar = take(4 * (size_t)S * n * kD);
     yb = take(8 * n * kD);
@@ -888,7 +892,7 @@ cudaError_t run(AdjParams A, char* ws, cudaStream_t st, int64_t* launches) {
   R.order = (const int32_t*)at(L.order);
   R.nrec = (const int32_t*)at(L.keys);
   R.count = (int32_t*)at(L.count);
-  R.hi = (int64_t*)at(L.hi0);
+  R.hi = (int64_t*)at(L.hi);
   R.lo = (int64_t*)at(L.lo);
   R.t_old = (double*)at(L.t_old);
   R.h = (double*)at(L.h);
