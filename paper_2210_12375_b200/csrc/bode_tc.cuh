@@ -54,6 +54,16 @@ __device__ __forceinline__ float tf32_hi(float x) {
   asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
   return __uint_as_float(r);
 }
+// tanh(x) = 1 - 2 / (e^{2x} + 1) on ex2.approx / rcp.approx (fast mode):
+// absolute error ~2e-7 over the whole range (libdevice tanhf: ~1 ulp
+// relative, a polynomial branch for |x| < 0.6 and saturation tests); +-inf
+// e^{2x} saturates to +-1 without a branch, NaN propagates
+__device__ __forceinline__ float tanh_fast(float x) {
+  float e, r;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(x * 2.8853900817779268f));
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(e + 1.0f));
+  return fmaf(-2.0f, r, 1.0f);
+}
 __device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count));
 }
