@@ -392,87 +392,102 @@ __global__ void __launch_bounds__(kVjpThreads, 1) vjp_kernel(const VjpArgs A) {
   auto phase = [](int q) { return (uint32_t)((q >> 1) & 1); };
 
   if (warp == 8) {
-    // ======================= MMA issue (one lane) =======================
-    if (lane == 0) {
-      const char* wf = (const char*)A.wfwd;
-      const char* wa = (const char*)A.wadj;
-      auto load_wa = [&](int q) {  // W1_c and (W2^T)_c of chunk q into buffer q & 1
-        const int b = q & 1, c = q % nchunk;
+    // ======================= MMA issue =======================
+    // The whole warp runs the control flow, so the descriptors and TMEM
+    // addresses are warp-uniform values in uniform registers; one elected
+    // lane issues each batch of MMAs / copies.  (Issuing from a single-lane
+    // branch makes the compiler move every operand into uniform registers
+    // through a per-MMA R2UR.BROADCAST loop: ~60 cycles per MMA against
+    // 16 / 33 for an N = 32 / 64 TS MMA, tools/mma_cost.cu.)
+    const char* wf = (const char*)A.wfwd;
+    const char* wa = (const char*)A.wadj;
+    auto load_wa = [&](int q) {  // W1_c and (W2^T)_c of chunk q into buffer q & 1
+      const int b = q & 1, c = q % nchunk;
+      if (elect_one()) {
         mbar_expect_tx(&S.wa[b], 4 * kW1);
         bulk_g2s(S.w1[b][0], wf + (size_t)c * kWChunk, kW1, &S.wa[b]);
         bulk_g2s(S.w1[b][1], wf + (size_t)c * kWChunk + kW1, kW1, &S.wa[b]);
         bulk_g2s(S.wv[b][0], wa + (size_t)c * kWChunk, kW1, &S.wa[b]);
         bulk_g2s(S.wv[b][1], wa + (size_t)c * kWChunk + kW1, kW1, &S.wa[b]);
-      };
-      auto load_wy = [&](int q) {  // (W1^T)_c
-        const int b = q & 1, c = q % nchunk;
+      }
+      __syncwarp();
+    };
+    auto load_wy = [&](int q) {  // (W1^T)_c
+      const int b = q & 1, c = q % nchunk;
+      if (elect_one()) {
         mbar_expect_tx(&S.wy_full[b], 2 * kW2);
         bulk_g2s(S.wy[b][0], wa + (size_t)c * kWChunk + 2 * kW1, kW2, &S.wy_full[b]);
         bulk_g2s(S.wy[b][1], wa + (size_t)c * kWChunk + 2 * kW1 + kW2, kW2, &S.wy_full[b]);
-      };
-      const int tb[3] = {0, 1, 0};
-      auto issue_zv = [&](int q) {  // Z = Y_s W1_c^T, V = g_s (W2^T)_c^T into buffer q & 1
-        const int b = q & 1;
-        mbar_wait(&S.wa[b], phase(q));
-        if (q >= 2) mbar_wait(&S.g2[b], phase(q - 2));  // Yb(q-2) read u from this buffer
+      }
+      __syncwarp();
+    };
+    auto issue_zv = [&](int q) {  // Z = Y_s W1_c^T, V = g_s (W2^T)_c^T into buffer q & 1
+      const int b = q & 1;
+      mbar_wait(&S.wa[b], phase(q));
+      if (q >= 2) mbar_wait(&S.g2[b], phase(q - 2));  // Yb(q-2) read u from this buffer
+      const uint32_t az = tmem + 256 + 64 * b, av = az + 32;
+      const uint64_t w1[2] = {smem_desc(smem_u32(S.w1[b][0]), 2048), smem_desc(smem_u32(S.w1[b][1]), 2048)};
+      const uint64_t wv[2] = {smem_desc(smem_u32(S.wv[b][0]), 2048), smem_desc(smem_u32(S.wv[b][1]), 2048)};
+      if (elect_one()) {
         fence_after();
-        const uint32_t az = tmem + 256 + 64 * b, av = az + 32;
+        const int tb[3] = {0, 1, 0};
         const uint32_t ya[3] = {tmem, tmem, tmem + 64}, ga[3] = {tmem + 128, tmem + 128, tmem + 192};
 #pragma unroll
         for (int s = 0; s < kD / 8; s++)
 #pragma unroll
           for (int term = 0; term < 3; term++) {
-            mma_tf32_ts(az, ya[term] + 8 * s, smem_desc(smem_u32(S.w1[b][tb[term]]) + 256 * s, 2048),
-                        idesc(kHc), (term | s) ? 1u : 0u);
-            mma_tf32_ts(av, ga[term] + 8 * s, smem_desc(smem_u32(S.wv[b][tb[term]]) + 256 * s, 2048),
-                        idesc(kHc), (term | s) ? 1u : 0u);
+            mma_tf32_ts(az, ya[term] + 8 * s, w1[tb[term]] + 16 * s, idesc(kHc), (term | s) ? 1u : 0u);
+            mma_tf32_ts(av, ga[term] + 8 * s, wv[tb[term]] + 16 * s, idesc(kHc), (term | s) ? 1u : 0u);
           }
         mma_commit(&S.g1[b]);
-      };
-      auto issue_yb = [&](int q, int c) {  // Yb += u_c (W1^T)_c^T (A from TMEM)
-        const int b = q & 1;
-        mbar_wait(&S.epi[b], phase(q));
-        mbar_wait(&S.wy_full[b], phase(q));
+      }
+      __syncwarp();
+    };
+    auto issue_yb = [&](int q, int c) {  // Yb += u_c (W1^T)_c^T (A from TMEM)
+      const int b = q & 1;
+      mbar_wait(&S.epi[b], phase(q));
+      mbar_wait(&S.wy_full[b], phase(q));
+      const uint32_t uhi = tmem + 256 + 64 * b, ulo = uhi + 32;
+      const uint64_t wh = smem_desc(smem_u32(S.wy[b][0]), 1024);
+      const uint64_t wl = smem_desc(smem_u32(S.wy[b][1]), 1024);
+      if (elect_one()) {
         fence_after();
-        const uint32_t uhi = tmem + 256 + 64 * b, ulo = uhi + 32;
 #pragma unroll
         for (int s = 0; s < kHc / 8; s++) {
-          const uint64_t wh = smem_desc(smem_u32(S.wy[b][0]) + 256 * s, 1024);
-          const uint64_t wl = smem_desc(smem_u32(S.wy[b][1]) + 256 * s, 1024);
-          mma_tf32_ts(accY, uhi + 8 * s, wh, idesc(kD), (c | s) ? 1u : 0u);
-          mma_tf32_ts(accY, uhi + 8 * s, wl, idesc(kD), 1u);
-          mma_tf32_ts(accY, ulo + 8 * s, wh, idesc(kD), 1u);
+          mma_tf32_ts(accY, uhi + 8 * s, wh + 16 * s, idesc(kD), (c | s) ? 1u : 0u);
+          mma_tf32_ts(accY, uhi + 8 * s, wl + 16 * s, idesc(kD), 1u);
+          mma_tf32_ts(accY, ulo + 8 * s, wh + 16 * s, idesc(kD), 1u);
         }
         mma_commit(&S.g2[b]);
-      };
-      load_wa(0);
-      load_wy(0);
-      if (total > 1) {
-        load_wa(1);
-        load_wy(1);
       }
-      for (int kl = 0; kl < my_tiles; kl++) {
-        mbar_wait(&S.full, kl & 1);  // tiles produced; the previous tile's Yb read out
-        ADJ_STAMP(1, 10)
-        const int q0 = kl * nchunk;
-        issue_zv(q0);
-        for (int c = 0; c < nchunk; c++) {
-          const int q = q0 + c;
-          if (c + 1 < nchunk) issue_zv(q + 1);
-          ADJ_STAMP(1, 20)
-          // weights of chunk q+2 into buffer q & 1 once ZV(q) has read it
-          mbar_wait(&S.g1[q & 1], phase(q));
-          if (q + 2 < total) load_wa(q + 2);
-          issue_yb(q, c);
-          ADJ_STAMP(1, 21)
-          if (q >= 1) {  // Yb(q-1) done: its (W1^T) buffer takes chunk q+1
-            mbar_wait(&S.g2[(q - 1) & 1], phase(q - 1));
-            if (q + 1 < total && q >= 1) load_wy(q + 1);
-          }
+      __syncwarp();
+    };
+    load_wa(0);
+    load_wy(0);
+    if (total > 1) {
+      load_wa(1);
+      load_wy(1);
+    }
+    for (int kl = 0; kl < my_tiles; kl++) {
+      mbar_wait(&S.full, kl & 1);  // tiles produced; the previous tile's Yb read out
+      if (lane == 0) { ADJ_STAMP(1, 10) }
+      const int q0 = kl * nchunk;
+      issue_zv(q0);
+      for (int c = 0; c < nchunk; c++) {
+        const int q = q0 + c;
+        if (c + 1 < nchunk) issue_zv(q + 1);
+        if (lane == 0) { ADJ_STAMP(1, 20) }
+        // weights of chunk q+2 into buffer q & 1 once ZV(q) has read it
+        mbar_wait(&S.g1[q & 1], phase(q));
+        if (q + 2 < total) load_wa(q + 2);
+        issue_yb(q, c);
+        if (lane == 0) { ADJ_STAMP(1, 21) }
+        if (q >= 1) {  // Yb(q-1) done: its (W1^T) buffer takes chunk q+1
+          mbar_wait(&S.g2[(q - 1) & 1], phase(q - 1));
+          if (q + 1 < total) load_wy(q + 1);
         }
       }
     }
-    __syncwarp();
   } else {
     // ============ row owners: production + epilogues (column half h) ============
     const int h = warp >> 2, r = tid & 127;
@@ -729,25 +744,39 @@ __global__ void __launch_bounds__(256, 1) wg_kernel(const WgArgs A) {
     fence_async_smem();
     fence_before();
     __syncthreads();
-    if (tid == 0) {
-      fence_after();
+    if (warp == 0) {  // warp-uniform operands, one elected lane issues
       const WgStage& g = S.st[b];
-      const int ta[3] = {0, 0, 1}, tb[3] = {0, 1, 0};
+      uint64_t au[2][2], ba[2][2], ag[2], by[2];
 #pragma unroll
-      for (int ks = 0; ks < kWgK / 8; ks++)
+      for (int t = 0; t < 2; t++) {
 #pragma unroll
-        for (int term = 0; term < 3; term++) {
-          const uint32_t acc = (i | ks | term) ? 1u : 0u;
-          for (int h = 0; h < halves; h++) {
-            mma_tf32(tmem + kN1 * h, smem_desc(smem_u32(g.au[h][ta[term]]) + 256 * ks, 512),
-                     smem_desc(smem_u32(g.by[tb[term]]) + 256 * ks, 512), idesc_mn(128, kN1), acc);
-            mma_tf32(tmem + 2 * kN1 + (h ? (16u << 16) : 0u),
-                     smem_desc(smem_u32(g.ag[ta[term]]) + 256 * ks, 512),
-                     smem_desc(smem_u32(g.ba[h][tb[term]]) + 256 * ks, 512),
-                     idesc_mn(64, h ? 128 : kN2), acc);
-          }
+        for (int h = 0; h < 2; h++) {
+          au[h][t] = smem_desc(smem_u32(g.au[h][t]), 512);
+          ba[h][t] = smem_desc(smem_u32(g.ba[h][t]), 512);
         }
-      mma_commit(&S.done[b]);
+        ag[t] = smem_desc(smem_u32(g.ag[t]), 512);
+        by[t] = smem_desc(smem_u32(g.by[t]), 512);
+      }
+      if (elect_one()) {
+        fence_after();
+        const int ta[3] = {0, 0, 1}, tb[3] = {0, 1, 0};
+#pragma unroll
+        for (int ks = 0; ks < kWgK / 8; ks++)
+#pragma unroll
+          for (int term = 0; term < 3; term++) {
+            const uint32_t acc = (i | ks | term) ? 1u : 0u;
+#pragma unroll
+            for (int h = 0; h < 2; h++) {
+              if (h >= halves) break;
+              mma_tf32(tmem + kN1 * h, au[h][ta[term]] + 16 * ks, by[tb[term]] + 16 * ks,
+                       idesc_mn(128, kN1), acc);
+              mma_tf32(tmem + 2 * kN1 + (h ? (16u << 16) : 0u), ag[ta[term]] + 16 * ks,
+                       ba[h][tb[term]] + 16 * ks, idesc_mn(64, h ? 128 : kN2), acc);
+            }
+          }
+        mma_commit(&S.done[b]);
+      }
+      __syncwarp();
     }
     fetch(i + 2, R);  // (the register set just stored)
   };
