@@ -348,6 +348,31 @@ __device__ __forceinline__ void vjp_produce(const VjpArgs& A, int64_t p, bool lv
   tmem_wait_st();
 }
 
+// L2 prefetch of what vjp_produce will read for row p (this thread's column
+// half) one tile ahead, issued while the current tile's chunks run on the
+// tensor cores: production then waits on L2 instead of HBM latency
+template <int M>
+__device__ __forceinline__ void vjp_prefetch(const VjpArgs& A, int64_t p, int cnt, int h) {
+  using T = Tab<M>;
+  if (p >= cnt) return;
+  auto pf = [](const void* q) { asm volatile("prefetch.global.L2 [%0];" ::"l"(q)); };
+  const int stage = A.stage, c0 = 32 * h;
+  if (stage == 0) {
+    pf(A.y + p * kD + c0);
+    pf(A.y + p * kD + c0 + 16);
+  } else {
+    pf(A.Ystages + (A.rec[p] * T::S + stage) * kD + c0);
+  }
+  const double* kp = A.kb + ((int64_t)stage * A.n + p) * kD + c0;
+  pf(kp);
+  pf(kp + 16);
+#pragma unroll
+  for (int s2 = T::S - 1; s2 > 0; s2--) {
+    if (s2 <= stage || T::za(s2, stage) == 0.0) continue;
+    pf(A.Ybar + ((int64_t)s2 * A.n + p) * kD + c0);
+  }
+}
+
 // One CTA per SM, tiles of 128 rows; warps 0-3 and 4-7 own the rows (thread
 // = row = TMEM lane) and split the columns of every production and
 // epilogue; warp 8 issues every MMA and weight copy.  Per hidden chunk c:
@@ -505,6 +530,7 @@ __global__ void __launch_bounds__(kVjpThreads, 1) vjp_kernel(const VjpArgs A) {
       rows_sync();
       if (tid == 0) mbar_arrive(&S.full);
       if (tid == 0) { ADJ_STAMP(0, 2) }
+      vjp_prefetch<M>(A, (int64_t)(tile + (int)gridDim.x) * kRows + r, cnt, h);
       const int q0 = kl * nchunk;
       for (int c = 0; c < nchunk; c++) {
         const int q = q0 + c, b = q & 1;

@@ -16,7 +16,7 @@
 // with cp.async.bulk (TMA engine) into separate W1/W2 buffers, each
 // prefetched as soon as the MMA that read it has completed; the producer
 // fills the next tile's A buffer while the consumer works on this one.
-// One elected thread issues every MMA; completions are tcgen05.commit ->
+// One elected lane of warp 0 issues every MMA; completions are tcgen05.commit ->
 // mbarrier.  3xTF32 keeps ~fp32 accuracy: plain TF32 inflates step counts
 // by +613% at rtol = 1e-6 (SURVEY.md finding 6).
 #include <cuda_runtime.h>
@@ -217,17 +217,20 @@ __global__ void __launch_bounds__(256, 1) mlp_tc_kernel(MlpTcArgs A) {
         // ---- GEMM1: acc1 = Y W1_c^T  (3xTF32, K = 64 in 8 steps)
         mbar_wait(&S.mb_w1, ph_w1);
         ph_w1 ^= 1;
-        if (tid == 0) {
-          fence_after();
-          const uint32_t aa[3] = {a_hi, a_hi, a_lo}, bb[3] = {w1h, w1l, w1h};
+        if (warp == 0) {  // warp-uniform descriptors, one elected lane issues
+          const uint64_t da[3] = {smem_desc(a_hi, 2048), smem_desc(a_hi, 2048), smem_desc(a_lo, 2048)};
+          const uint64_t db[3] = {smem_desc(w1h, 2048), smem_desc(w1l, 2048), smem_desc(w1h, 2048)};
+          if (elect_one()) {
+            fence_after();
 #pragma unroll
-          for (int s = 0; s < kD / 8; s++)
+            for (int s = 0; s < kD / 8; s++)
 #pragma unroll
-            for (int term = 0; term < 3; term++)
-              mma_tf32(acc1, smem_desc(aa[term] + 256 * s, 2048), smem_desc(bb[term] + 256 * s, 2048),
-                       idesc(kHc), (term | s) ? 1u : 0u);
-          mma_commit(&S.mb_g1);
-          if (last) mma_commit(&S.empty[b]);  // A[b] free once this GEMM1 is done
+              for (int term = 0; term < 3; term++)
+                mma_tf32(acc1, da[term] + 16 * s, db[term] + 16 * s, idesc(kHc), (term | s) ? 1u : 0u);
+            mma_commit(&S.mb_g1);
+            if (last) mma_commit(&S.empty[b]);  // A[b] free once this GEMM1 is done
+          }
+          __syncwarp();
         }
         mbar_wait(&S.mb_g1, ph_g1);
         ph_g1 ^= 1;
@@ -254,16 +257,19 @@ __global__ void __launch_bounds__(256, 1) mlp_tc_kernel(MlpTcArgs A) {
         // ---- GEMM2: acc2 += H_c W2_c^T  (3xTF32, K = 32 in 4 steps)
         mbar_wait(&S.mb_w2, ph_w2);
         ph_w2 ^= 1;
-        if (tid == 0) {
-          fence_after();
-          const uint32_t aa[3] = {h_hi, h_hi, h_lo}, bb[3] = {w2h, w2l, w2h};
+        if (warp == 0) {
+          const uint64_t da[3] = {smem_desc(h_hi, 1024), smem_desc(h_hi, 1024), smem_desc(h_lo, 1024)};
+          const uint64_t db[3] = {smem_desc(w2h, 1024), smem_desc(w2l, 1024), smem_desc(w2h, 1024)};
+          if (elect_one()) {
+            fence_after();
 #pragma unroll
-          for (int s = 0; s < kHc / 8; s++)
+            for (int s = 0; s < kHc / 8; s++)
 #pragma unroll
-            for (int term = 0; term < 3; term++)
-              mma_tf32(acc2, smem_desc(aa[term] + 256 * s, 1024), smem_desc(bb[term] + 256 * s, 1024),
-                       idesc(kD), (c | term | s) ? 1u : 0u);
-          mma_commit(&S.mb_g2);
+              for (int term = 0; term < 3; term++)
+                mma_tf32(acc2, da[term] + 16 * s, db[term] + 16 * s, idesc(kD), (c | term | s) ? 1u : 0u);
+            mma_commit(&S.mb_g2);
+          }
+          __syncwarp();
         }
         mbar_wait(&S.mb_g2, ph_g2);
         ph_g2 ^= 1;
