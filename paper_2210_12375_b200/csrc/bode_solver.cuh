@@ -386,11 +386,24 @@ struct Lane {
 
   // _emit, solver.py:284-322: every point with theta in (.., 1] is
   // interpolated from the pre-commit state (y is still y_old here)
+  // Fast mode: one reciprocal per call (not an IEEE division per point --
+  // the hottest stall of C3's kernel) and theta = diff / h as the product
+  // refined by one residual step, i.e. the rounded quotient except at rare
+  // near-ties; diff == h still gives theta == 1 exactly (a point at the end
+  // of the step is emitted by this step).
   __device__ __forceinline__ void emit(const EmitBase& eb, double t_old, double h) {
     const double* te = eb.te;
     double* ys = eb.ys;
+    const double rh = O::kFast ? fast_rcp(h) : 0.0;
     while (cursor < m) {
-      double theta = ddiv(O::sub(te_next, t_old), h);
+      const double diff = O::sub(te_next, t_old);
+      double theta;
+      if constexpr (O::kFast) {
+        const double q = diff * rh;
+        theta = fma(fma(-q, h, diff), rh, q);
+      } else {
+        theta = ddiv(diff, h);
+      }
       if (!(theta <= 1.0)) break;
       theta = np_max(theta, 0.0);
       double out[D];
