@@ -156,6 +156,24 @@ __global__ void mlp_init_a_kernel(MlpWs W, InitArgs I, int64_t n, int D) {
   }
 }
 
+// NumPy's pairwise sum (pairwise_sum_rt) of sq[0..D) across a warp: for
+// 8 <= D <= 128, D % 8 == 0 (the MLP tile, D = 64) lanes 0-7 run the eight
+// strided accumulators and three shuffle levels form the fixed tree
+// ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) -- bitwise the serial result, in
+// lane 0; other widths sum serially in lane 0
+__device__ __forceinline__ double warp_pairwise_sum(const double* sq, int D, int lane) {
+  if (D < 8 || D > 128 || D % 8 != 0)
+    return lane == 0 ? pairwise_sum_rt<ExactOps>(sq, D) : 0.0;
+  double r = 0.0;
+  if (lane < 8) {
+    r = sq[lane];
+    for (int i = 8; i < D; i += 8) r = ExactOps::add(r, sq[i + lane]);
+  }
+  r = ExactOps::add(r, __shfl_down_sync(0xffffffffu, r, 1));
+  r = ExactOps::add(r, __shfl_down_sync(0xffffffffu, r, 2));
+  return ExactOps::add(r, __shfl_down_sync(0xffffffffu, r, 4));
+}
+
 // after f0 = MLP(y0) (in k[0]): d0, d1, h0 and the Euler probe input
 // (controller.py:167-185), one warp per instance
 __global__ void __launch_bounds__(128) mlp_init_b_kernel(MlpWs W, InitArgs I, int64_t n, int D) {
@@ -177,8 +195,9 @@ __global__ void __launch_bounds__(128) mlp_init_b_kernel(MlpWs W, InitArgs I, in
       sq[wib][c] = ExactOps::mul(q, q);
     }
     __syncwarp();
+    const double ssum = warp_pairwise_sum(sq[wib], D, lane);
     if (lane == 0) {
-      const double dd = dsqrt(ddiv(pairwise_sum_rt<ExactOps>(sq[wib], D), (double)D));
+      const double dd = dsqrt(ddiv(ssum, (double)D));
       if (pass == 0) d0 = dd; else d1 = dd;
     }
     __syncwarp();
@@ -224,11 +243,12 @@ __global__ void __launch_bounds__(128) mlp_init_c_kernel(MlpWs W, InitArgs I, Ct
   }
   bad = __any_sync(0xffffffffu, bad);
   __syncwarp();
+  const double ssum = have_f1 ? warp_pairwise_sum(sq[wib], D, lane) : 0.0;
   if (lane != 0) return;
   double dt;
   if (have_f1) {
     const double d1 = W.scr[i], h0 = W.scr[n + i], dir = W.scr[2 * n + i];
-    const double d2 = ddiv(dsqrt(ddiv(pairwise_sum_rt<ExactOps>(sq[wib], D), (double)D)), h0);
+    const double d2 = ddiv(dsqrt(ddiv(ssum, (double)D)), h0);
     const double dmax = np_max(d1, d2);
     const bool small = (dmax <= 1e-15) || !isfinite(dmax);
     const double h1 = small ? np_max(1e-6, __dmul_rn(h0, 1e-3))
