@@ -209,10 +209,10 @@ typedef struct bode_solve_args {
    * OR over shards of map[j]} (FSAL), 1 + S * max_j otherwise. */
   int64_t* max_iterations_out;
   uint8_t* refresh_map_out;
-  /* reserved, must be 0.  (MLP dynamics run one path per shape: d == 64
-   * with hidden a multiple of 32 up to 256 -> the fused persistent tcgen05
-   * integrator; d == 64 with a wider hidden layer -> the per-stage tcgen05
-   * kernels; other d -> fp32 FMA kernels.  There is no backend switch.) */
+  /* reserved, must be 0.  (MLP dynamics run one path: d == 64 with hidden
+   * a multiple of 32 up to 256 -> the fused persistent tcgen05 integrator;
+   * other shapes return BODE_EUNSUPPORTED -- the Python facade zero-pads
+   * narrower networks to the 64-wide tile.  There is no backend switch.) */
   int32_t reserved_mlp;
   int32_t _pad3;
   /* optional cudaEvent_t pair recorded on `stream` immediately before and
@@ -421,6 +421,21 @@ int bode_program_initial_step(const bode_program* prog, const bode_dynamics* dyn
                               const double* atol_v, const double* rtol_v, double atol,
                               double rtol, const double* direction, double* dt, double* f0,
                               void* stream);
+
+/* One batch sharded across the GPUs of one process:
+ * per_dev[k] is a complete bode_solve_args for shard k -- its buffers,
+ * workspace and stream on one device (found from y0), a built-in method,
+ * the same method and max_steps on every shard, max_iterations_out and
+ * refresh_map_out set.  The shard solves run concurrently; then the
+ * batch-global n_f_evals (solver.py:184,224,239) is combined across the
+ * shards -- a MAX all-reduce over NCCL when comms != NULL (comms[k] = the
+ * ncclComm_t of shard k in a communicator of exactly these ndev devices;
+ * NCCL is loaded at run time), else one kernel on shard 0's device reading
+ * the other shards by peer access -- and written to every shard's
+ * n_f_evals (max_iterations_out / refresh_map_out then hold the global
+ * values too).  Asynchronous on the shards' streams; per-instance outputs
+ * stay on their shard's device.  At most 16 shards. */
+int bode_solve_multi(const bode_solve_args* per_dev, int32_t ndev, void* const* comms);
 
 /* Multi-GPU shard plan (the reference has one process and
  * no partition -- a shard is bitwise equal to its rows of the full batch,

@@ -151,6 +151,7 @@ SIGNATURES = {
                                    _P, _P], C.c_int),
     "bode_partition": ([_P, _I64, _I32, _P, _P, _P, _SZ, _P], C.c_int),
     "bode_probe_tf32": ([_I32, _I32, _P], C.c_int),
+    "bode_solve_multi": ([C.POINTER(SolveArgs), _I32, _P], C.c_int),
 }
 
 _lib = None

@@ -373,3 +373,83 @@ def solve_sharded_device(y0, t_start, t_end, f, *, t_eval=None, cost_hint=None, 
     res["ys"] = (torch.empty_like(ys).index_copy_(0, perm, ys).reshape(n * mpts, d) if mpts
                  else out["ys"][:0])
     return res
+
+
+def solve_multi(y0, t_start, t_end, f, *, devices, t_eval=None, cost_hint=None,
+                method="dopri5", atol=1e-6, rtol=1e-6, dt0=None, comms=None, gather: bool = True,
+                **solve_kw):
+    """One batch across several GPUs of THIS process through the C ABI's
+    ``bode_solve_multi`` (no torch.distributed, no extra processes): the
+    device shard plan (``shard_plan``, cost-aware with ``cost_hint``), each
+    shard's rows copied to its device, the shard solves launched
+    concurrently and the batch-global ``n_f_evals`` combined by the library
+    (peer access, or NCCL when ``comms`` holds one ncclComm_t per shard, as
+    integers, of a communicator over exactly these devices).  ``devices``
+    lists CUDA device indices, one per shard (repeats allowed: several
+    shards on one GPU).  Returns the solve_device-style dict in batch order
+    on ``devices[0]`` (``gather=True``) or the list of shard dicts (each
+    with ``idx``, its rows of the batch)."""
+    import torch
+
+    from . import _abi
+    from .solver import solve_device
+    from .tableau import method_of
+
+    lib = _abi.load()
+    ndev = len(devices)
+    n, d = y0.shape
+    if ndev < 1 or n < ndev:
+        raise ValueError("solve_multi needs 1 <= len(devices) <= n")
+    home = y0.device
+    perm, sizes = shard_plan(n, ndev, cost_hint, home)
+    m = method_of(method)
+    shards, off = [], 0
+    for k, dv in enumerate(devices):
+        idx = perm[off:off + sizes[k]]
+        off += sizes[k]
+        dev = torch.device("cuda", int(dv))
+
+        def rows(x, idx=idx, dev=dev):
+            if isinstance(x, torch.Tensor) and x.dim() > 0 and x.shape[0] == n:
+                return x.index_select(0, idx.to(x.device)).to(dev)
+            if isinstance(x, torch.Tensor):
+                return x.to(dev)
+            return x
+
+        ts = torch.as_tensor(t_start, dtype=torch.float64, device=home).expand(n)
+        tn = torch.as_tensor(t_end, dtype=torch.float64, device=home).expand(n)
+        te = None if t_eval is None else (t_eval.to(dev) if t_eval.dim() == 1 else rows(t_eval))
+        sub_f = f.subset(idx.cpu().numpy()) if hasattr(f, "subset") else f
+        with torch.cuda.device(dev):
+            o = solve_device(rows(y0), rows(ts), rows(tn), sub_f, t_eval=te, method=m,
+                             atol=rows(atol), rtol=rows(rtol), dt0=rows(dt0),
+                             with_refresh_map=True, _launch=False, **solve_kw)
+        o["idx"] = idx
+        shards.append(o)
+    arr = (_abi.SolveArgs * ndev)(*[o["_args"] for o in shards])
+    cm = None if comms is None else (_abi.C.c_void_p * ndev)(*comms)
+    _abi.check(lib.bode_solve_multi(arr, ndev, cm))
+    for o in shards:
+        o["launches"] = 3  # init pass, persistent integrator, finalize (+ the combine below)
+    shards[0]["launches"] += 1
+    if not gather:
+        return shards
+    # results back in batch order on the first device
+    dev0 = torch.device("cuda", int(devices[0]))
+    for dv in set(int(x) for x in devices):
+        torch.cuda.synchronize(dv)  # (every shard's stream has seen the combine)
+    keys = ("n_steps", "n_accepted", "final_dt", "status", "n_emitted")
+    rec = torch.cat([torch.stack([o[k].view(torch.int64) if o[k].dtype == torch.float64 else o[k]
+                                  for k in keys], dim=1).to(dev0) for o in shards])
+    full = torch.empty_like(rec).index_copy_(0, perm.to(dev0), rec)
+    res = {k: full[:, j] for j, k in enumerate(keys)}
+    res["final_dt"] = res["final_dt"].contiguous().view(torch.float64)
+    res["n_f_evals"] = shards[0]["n_f_evals"].to(dev0)
+    mpts = 0 if t_eval is None else (t_eval.numel() if t_eval.dim() == 1 else t_eval.shape[1])
+    if mpts:
+        ys = torch.cat([o["ys"].reshape(-1, mpts * d).to(dev0) for o in shards])
+        res["ys"] = torch.empty_like(ys).index_copy_(0, perm.to(dev0), ys).reshape(n * mpts, d)
+    else:
+        res["ys"] = shards[0]["ys"][:0].to(dev0)
+    res["launches"] = sum(o["launches"] for o in shards)
+    return res

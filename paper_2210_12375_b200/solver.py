@@ -494,7 +494,7 @@ def solve_device(y0, t_start, t_end, f, *, t_eval=None, t_eval_offsets=None, met
                  mode: str = "exact", record_trace: bool = False, stream=None,
                  threads_per_block: int = 0, blocks: int = 0,
                  prof_events=None, with_refresh_map: bool = False,
-                 record_trajectory: bool = False):
+                 record_trajectory: bool = False, _launch: bool = True):
     """Device-resident solve on torch CUDA tensors; asynchronous (no host
     sync).  ``t_eval``: None, a 1-D tensor shared by all instances, a 2-D
     (n, m) tensor, or CSR values with ``t_eval_offsets`` (n+1).  ``atol`` /
@@ -503,10 +503,15 @@ def solve_device(y0, t_start, t_end, f, *, t_eval=None, t_eval_offsets=None, met
     n_f_evals (+ trace_* when ``record_trace``).  ``record_trajectory``:
     also record every accepted step for :func:`adjoint_device` (a second,
     recording pass of the same deterministic solve, sized from the first
-    pass's n_accepted -- one host sync)."""
+    pass's n_accepted -- one host sync).  ``_launch=False`` (internal,
+    ``distributed.solve_multi``): build the arguments and outputs without
+    launching; the returned dict's ``_args`` is then launched by the
+    caller."""
     import torch
 
     lib = _abi.load()
+    if not _launch and record_trajectory:
+        raise ValueError("record_trajectory needs the launch (its sizing pass)")
     if max_steps < 1:
         raise ValueError("max_steps must be at least 1")
     method = method_of(method)
@@ -529,7 +534,7 @@ def solve_device(y0, t_start, t_end, f, *, t_eval=None, t_eval_offsets=None, met
                            cost_hint=cost_hint, mode=mode, record_trace=record_trace,
                            stream=stream, threads_per_block=threads_per_block, blocks=blocks,
                            prof_events=prof_events, with_refresh_map=with_refresh_map,
-                           record_trajectory=record_trajectory)
+                           record_trajectory=record_trajectory, _launch=_launch)
         out["ys"] = out["ys"][:, :D].contiguous()
         out["_mlp_pad"] = (D, H)
         return out
@@ -626,7 +631,8 @@ def solve_device(y0, t_start, t_end, f, *, t_eval=None, t_eval_offsets=None, met
     nlaunch = _abi.C.c_int64(0)
     keep.append(nlaunch)  # a.launch_count_out must stay valid while `a` is reused
     a.launch_count_out = _abi.C.addressof(nlaunch)
-    _abi.check(lib.bode_solve(_abi.C.byref(a)))
+    if _launch:
+        _abi.check(lib.bode_solve(_abi.C.byref(a)))
     if record_trajectory:
         # the sizing reads (cumsum, row count, divergence check) run on the
         # solve's own stream, so they see the sizing solve's n_accepted even
@@ -656,6 +662,8 @@ def solve_device(y0, t_start, t_end, f, *, t_eval=None, t_eval_offsets=None, met
         if isinstance(t, torch.Tensor):
             t.record_stream(st)
     out["ys"] = out["ys"][:n_rows]
+    out.setdefault("_args", a)
+    out.setdefault("_keep", keep)
     out["launches"] = int(nlaunch.value)
     out["offsets"] = offsets
     out["shared_len"] = shared_len

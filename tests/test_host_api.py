@@ -209,3 +209,12 @@ def test_adjoint_oracle_tableau_matches_product_tableau():
         assert np.array_equal(T["a"], np.asarray(tab.a)[:S, :S])
         assert np.array_equal(T["b"], np.asarray(tab.b)[:S])
         assert np.array_equal(T["c"], np.asarray(tab.c)[:S])
+
+
+def test_solve_multi_validates_before_touching_the_gpu():
+    """bode_solve_multi rejects an empty shard list with
+    BODE_EINVAL and a message, without a device."""
+    from paper_2210_12375_b200 import _abi
+    lib = _abi.load()
+    assert lib.bode_solve_multi(None, 0, None) == _abi.EINVAL
+    assert b"at least one shard" in lib.bode_last_error()
