@@ -444,6 +444,10 @@ static __device__ unsigned g_exit_count;
 #ifndef BODE_BLOCKS_2D
 #define BODE_BLOCKS_2D 5
 #endif
+template <bool B>
+struct BoolTag {  // (no <type_traits> under NVRTC)
+  static constexpr bool value = B;
+};
 template <int M, class F, class O, bool REC, bool PI>
 __global__ void __launch_bounds__(128, ((F::D <= 2 && (!REC || PI)) ? BODE_BLOCKS_2D : 4)) bode_persistent_kernel(const SolveParams P) {
   extern __shared__ uint32_t s_refresh[];
@@ -458,7 +462,6 @@ __global__ void __launch_bounds__(128, ((F::D <= 2 && (!REC || PI)) ? BODE_BLOCK
   __syncthreads();
 
   Lane<M, F, O> L;
-  const bool tracing = P.trace_cap > 0;  // uniform: hoisted out of the step loop
   __shared__ TrajRows s_trec[REC ? 128 : 1];  // per-lane trajectory rows
   const TrajRows* trec = REC ? &s_trec[threadIdx.x] : nullptr;
   __shared__ EmitBase s_eb[128];
@@ -466,6 +469,10 @@ __global__ void __launch_bounds__(128, ((F::D <= 2 && (!REC || PI)) ? BODE_BLOCK
   unsigned long long my_max = 0;
   const unsigned lt_mask = (1u << lane) - 1u;
 
+  // the step loop, compiled twice: with the debug trace (record_trace) and
+  // without it, so the solve loop carries no trace test or trace stores
+  auto loop = [&](auto trace_tag) {
+  constexpr bool tracing = decltype(trace_tag)::value;
   while (true) {
     const unsigned need = __ballot_sync(0xffffffffu, !have && !done);
     if (need) {
@@ -523,6 +530,11 @@ __global__ void __launch_bounds__(128, ((F::D <= 2 && (!REC || PI)) ? BODE_BLOCK
       }
     }
   }
+  };
+  if (P.trace_cap > 0)
+    loop(BoolTag<true>{});
+  else
+    loop(BoolTag<false>{});
 #ifdef BODE_EXIT_PROF
   if (lane == 0) {  // debug builds: when did each warp run out of work
     unsigned long long ts;
