@@ -299,7 +299,10 @@ struct Lane {
   // the arithmetic of one attempt: t_end truncation, the RK trial step, the
   // error norm and the controller (no memory traffic, no branches on the
   // fast I / PI path); commit() applies the decision
-  template <bool PI>
+  // VT: the launch may carry per-instance tolerance vectors; false = the
+  // caller passed scalars (atol_v == rtol_v == NULL), so the step loop keeps
+  // no pointer tests or predicated loads for them
+  template <bool PI, bool VT = true>
   __device__ __forceinline__ bool attempt(const SolveParams& P, const PowTables& PT, double* yn,
                                           double* err, double& dtn, double& h, bool& trunc) {
     const double remaining = O::sub(t_end, t);
@@ -307,10 +310,11 @@ struct Lane {
     h = trunc ? remaining : dt;
     rk_step<T, F, O>(f, t, h, y, k, yn, err);
     dtn = h;
+    const double at = VT ? atol_of(P) : P.atol, rt = VT ? rtol_of(P) : P.rtol;
     if constexpr (O::kFast && PI) {
-      return adapt_pi_ms(P.ctrl, error_ms<D, O>(err, y, yn, atol_of(P), rtol_of(P)), L1, dtn, PT);
+      return adapt_pi_ms(P.ctrl, error_ms<D, O>(err, y, yn, at, rt), L1, dtn, PT);
     } else {
-      const double norm = error_norm<D, O>(err, y, yn, atol_of(P), rtol_of(P));
+      const double norm = error_norm<D, O>(err, y, yn, at, rt);
       return adapt_cached<O>(P.ctrl, norm, n1, n2, L1, dtn, PT);
     }
   }
@@ -375,12 +379,12 @@ struct Lane {
   // PI (fast mode only): the launch was specialised for an I / PI
   // controller (CtrlParams::plain_pi), so the general controller is not
   // compiled into the loop
-  template <bool PI>
+  template <bool PI, bool VT = true>
   __device__ __forceinline__ bool step(const SolveParams& P, const PowTables& PT, bool tracing,
                                        const TrajRows* trec, const EmitBase& eb) {
     double yn[D], err[D], dtn, h;
     bool trunc;
-    const bool accept = attempt<PI>(P, PT, yn, err, dtn, h, trunc);
+    const bool accept = attempt<PI, VT>(P, PT, yn, err, dtn, h, trunc);
     return commit(P, tracing, trec, eb, yn, accept, dtn, h, trunc);
   }
 
@@ -469,10 +473,14 @@ __global__ void __launch_bounds__(128, ((F::D <= 2 && (!REC || PI)) ? BODE_BLOCK
   unsigned long long my_max = 0;
   const unsigned lt_mask = (1u << lane) - 1u;
 
-  // the step loop, compiled twice: with the debug trace (record_trace) and
-  // without it, so the solve loop carries no trace test or trace stores
-  auto loop = [&](auto trace_tag) {
+  // the step loop, compiled with and without the debug trace (record_trace)
+  // and with and without per-instance tolerance vectors, so the solve loop
+  // carries no trace test or trace stores and, for scalar tolerances, no
+  // tolerance pointer tests
+  auto loop = [&](auto trace_tag, auto vtol_tag) {
   constexpr bool tracing = decltype(trace_tag)::value;
+  constexpr bool vtol = decltype(vtol_tag)::value;
+  unsigned done_mask = 0u;  // lanes out of work for good (changes only at a refill)
   while (true) {
     const unsigned need = __ballot_sync(0xffffffffu, !have && !done);
     if (need) {
@@ -507,14 +515,13 @@ __global__ void __launch_bounds__(128, ((F::D <= 2 && (!REC || PI)) ? BODE_BLOCK
           }
         }
       }
+      done_mask = __ballot_sync(0xffffffffu, done);
     }
-    if (!__any_sync(0xffffffffu, have)) {
-      if (__all_sync(0xffffffffu, done)) break;
-      continue;
-    }
+    // every lane has a row or is done (need == 0): one vote per iteration
+    if (done_mask == 0xffffffffu) break;
     if (have) {
       const int64_t j = L.nsteps;
-      if (L.template step<PI>(P, s_pow, tracing, trec, s_eb[threadIdx.x])) {
+      if (L.template step<PI, vtol>(P, s_pow, tracing, trec, s_eb[threadIdx.x])) {
         const uint64_t bit = (uint64_t)j + 1;
         const uint32_t w = (uint32_t)(bit >> 5), msk = 1u << (bit & 31);
         if (P.smem_words > 0) {
@@ -532,9 +539,11 @@ __global__ void __launch_bounds__(128, ((F::D <= 2 && (!REC || PI)) ? BODE_BLOCK
   }
   };
   if (P.trace_cap > 0)
-    loop(BoolTag<true>{});
+    loop(BoolTag<true>{}, BoolTag<true>{});
+  else if (P.atol_v || P.rtol_v)
+    loop(BoolTag<false>{}, BoolTag<true>{});
   else
-    loop(BoolTag<false>{});
+    loop(BoolTag<false>{}, BoolTag<false>{});
 #ifdef BODE_EXIT_PROF
   if (lane == 0) {  // debug builds: when did each warp run out of work
     unsigned long long ts;
