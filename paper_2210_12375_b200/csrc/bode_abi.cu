@@ -120,6 +120,8 @@ int validate(const bode_solve_args* a) {
   if (a->mode != BODE_MODE_EXACT && a->mode != BODE_MODE_FAST) return fail(BODE_EINVAL, "unknown mode");
   if (!valid_kind(a->dyn.kind)) return fail(BODE_EINVAL, "unknown dynamics");
   if (a->max_steps < 1) return fail(BODE_EINVAL, "max_steps must be at least 1");
+  if (a->max_steps > 2147483645)  // (per-instance step counters are 32-bit)
+    return fail(BODE_EINVAL, "max_steps must be below 2^31 - 2");
   if (!a->y0 || !a->t_start || !a->t_end) return fail(BODE_EINVAL, "y0/t_start/t_end required");
   if (!a->n_emitted || !a->n_steps || !a->n_accepted || !a->final_dt || !a->status || !a->n_f_evals)
     return fail(BODE_EINVAL, "output statistics buffers required");

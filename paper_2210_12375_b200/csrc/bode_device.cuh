@@ -482,9 +482,11 @@ __device__ __forceinline__ double error_ms(const double* e, const double* y0, co
   double sq[D], rr[D];
 #pragma unroll
   for (int j = 0; j < D; j++) {
-    // fmax instead of NumPy's NaN-propagating maximum: a NaN |y1| implies a
-    // NaN error estimate here, so the ratio is NaN (-> rejection) either way
-    const double scale = O::mad(rtol, fmax(fabs(y0[j]), fabs(y1[j])), atol);
+    // a plain compare-select instead of NumPy's NaN-propagating maximum: a
+    // NaN |y0| or |y1| implies a NaN error estimate here, so the ratio is NaN
+    // (-> +inf, rejection) whichever operand the select keeps
+    const double a0 = fabs(y0[j]), a1 = fabs(y1[j]);
+    const double scale = O::mad(rtol, a0 > a1 ? a0 : a1, atol);
     rr[j] = __dmul_rn(e[j], fast_rcp1(scale));
     sq[j] = O::mul(rr[j], rr[j]);
   }
@@ -635,8 +637,13 @@ __device__ __forceinline__ bool adapt_pi_ms(const CtrlParams& C, double ms, LogC
     if (C.e2 == 0.0 || L1.ok) {
       double y = C.e1 * La.h;
       if (C.e2 != 0.0) y = fma(C.e2, L1.h, y);
-      if (y < 700.0 && y > -700.0)
-        factor = fmin(fmax(C.safety * fast_exp3(y, T), C.fmin), C.fmax);  // finite, > 0
+      if (y < 700.0 && y > -700.0) {
+        // finite and > 0: plain compare-selects (fmax/fmin would add NaN
+        // handling that cannot trigger here)
+        const double x = C.safety * fast_exp3(y, T);
+        factor = x > C.fmin ? x : C.fmin;
+        factor = factor < C.fmax ? factor : C.fmax;
+      }
       else
         factor = (y > 0.0 && y < 709.78) ? C.fmax : C.fmin;
     }

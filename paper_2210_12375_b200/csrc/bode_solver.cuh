@@ -520,10 +520,10 @@ __global__ void __launch_bounds__(128, ((F::D <= 2 && (!REC || PI)) ? BODE_BLOCK
     // every lane has a row or is done (need == 0): one vote per iteration
     if (done_mask == 0xffffffffu) break;
     if (have) {
-      const int64_t j = L.nsteps;
+      const uint32_t j = (uint32_t)L.nsteps;  // (n_steps is 32-bit: 32-bit bit index)
       if (L.template step<PI, vtol>(P, s_pow, tracing, trec, s_eb[threadIdx.x])) {
-        const uint64_t bit = (uint64_t)j + 1;
-        const uint32_t w = (uint32_t)(bit >> 5), msk = 1u << (bit & 31);
+        const uint32_t bit = j + 1u;
+        const uint32_t w = bit >> 5, msk = 1u << (bit & 31);
         if (P.smem_words > 0) {
           if (!(s_refresh[w] & msk)) atomicOr(&s_refresh[w], msk);
         } else {
