@@ -367,7 +367,8 @@ struct Lane {
     }
     dt = dtn;
     if (status == BODE_RUNNING && O::add(t, dt) == t) status = BODE_STEP_UNDERFLOW;
-    if (status == BODE_RUNNING && nsteps >= P.max_steps) status = BODE_MAX_STEPS_EXCEEDED;
+    if (status == BODE_RUNNING && nsteps >= (int32_t)P.max_steps)  // (max_steps < 2^31, bode_abi.cu)
+      status = BODE_MAX_STEPS_EXCEEDED;
     return !accept && status == BODE_RUNNING;
   }
 
@@ -481,6 +482,11 @@ __global__ void __launch_bounds__(128, ((F::D <= 2 && (!REC || PI)) ? BODE_BLOCK
   constexpr bool tracing = decltype(trace_tag)::value;
   constexpr bool vtol = decltype(vtol_tag)::value;
   unsigned done_mask = 0u;  // lanes out of work for good (changes only at a refill)
+  // the shared bitmap's 32-bit shared-window address, kept in a register
+  // (not re-derived from the CTA id on every rejection)
+  uint32_t s_ref;
+  asm("{ .reg .u64 t; cvta.to.shared.u64 t, %1; cvt.u32.u64 %0, t; }" : "=r"(s_ref) : "l"(s_refresh));
+  const bool smem_bm = P.smem_words > 0;
   while (true) {
     const unsigned need = __ballot_sync(0xffffffffu, !have && !done);
     if (need) {
@@ -524,8 +530,11 @@ __global__ void __launch_bounds__(128, ((F::D <= 2 && (!REC || PI)) ? BODE_BLOCK
       if (L.template step<PI, vtol>(P, s_pow, tracing, trec, s_eb[threadIdx.x])) {
         const uint32_t bit = j + 1u;
         const uint32_t w = bit >> 5, msk = 1u << (bit & 31);
-        if (P.smem_words > 0) {
-          if (!(s_refresh[w] & msk)) atomicOr(&s_refresh[w], msk);
+        if (smem_bm) {
+          const uint32_t a = s_ref + 4u * w;
+          uint32_t v;
+          asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+          if (!(v & msk)) asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(a), "r"(msk) : "memory");
         } else {
           if (!(__ldcg(&P.refresh[w]) & msk)) atomicOr(&P.refresh[w], msk);
         }
