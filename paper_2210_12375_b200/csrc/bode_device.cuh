@@ -635,8 +635,8 @@ __device__ __forceinline__ bool adapt_pi_ms(const CtrlParams& C, double ms, LogC
     const bool tiny = !(ms >= 1e-20);  // norm below the floor: a = 1e-10 exactly
     La.h = fast_log1(tiny ? 1e-10 : ms, T) * (tiny ? 1.0 : 0.5);
     if (C.e2 == 0.0 || L1.ok) {
-      double y = C.e1 * La.h;
-      if (C.e2 != 0.0) y = fma(C.e2, L1.h, y);
+      // (e2 == 0: fma(0, 0, y) == y -- no second uniform test of e2)
+      const double y = fma(C.e2, L1.ok ? L1.h : 0.0, C.e1 * La.h);
       if (y < 700.0 && y > -700.0) {
         // finite and > 0: plain compare-selects (fmax/fmin would add NaN
         // handling that cannot trigger here)

@@ -326,16 +326,29 @@ BODE_HD double fast_log1(double x, const PowTables& T) {
 BODE_HD double fast_exp3(double y, const PowTables& T) {
   using namespace powimpl;
   const double kd = rint(mul(y, BODE_PK(18)));
+#if defined(__CUDA_ARCH__)
+  // |y| < 700 (the caller's range): 32-bit k, and the 2^ke scaling as an
+  // add to the high word (the result is normal, no carry from the low word)
+  const int kf = __double2int_rn(kd);
+  const int j = kf & 127;
+  const int ke = (kf - j) / 128;
+#else
   const int64_t kf = (int64_t)kd;
   const int j = (int)(kf & 127);
   const int64_t ke = (kf - j) / 128;
+#endif
   const double r = fma_(-kd, BODE_PK(17), fma_(-kd, BODE_PK(16), y));
   double c = fma_(BODE_PK(10), r, BODE_PK(11));
   c = fma_(c, r, BODE_PK(12));
   c = fma_(c, r, BODE_PK(13));
   const double p = fma_(mul(r, r), c, r);
   const double th = T.exp_tab[j][0], tl = T.exp_tab[j][1];
-  return from_bits(bits(add(th, fma_(th, p, tl))) + (ke << 52));
+  const double res = add(th, fma_(th, p, tl));
+#if defined(__CUDA_ARCH__)
+  return __hiloint2double(__double2hiint(res) + ke * (1 << 20), __double2loint(res));
+#else
+  return from_bits(bits(res) + (ke << 52));
+#endif
 }
 
 // Correctly rounded (w.h.p.) x**e for x > 0 finite, e finite; everything
