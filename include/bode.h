@@ -160,7 +160,8 @@ typedef struct bode_solve_args {
   const double* atol_v;
   const double* rtol_v;
   double atol, rtol;
-  int64_t max_steps;   /* solver.py:42,155 */
+  int64_t max_steps;   /* solver.py:42,155; 1 <= max_steps < 2^31 - 2 (32-bit per-instance
+                        * step counters), BODE_EINVAL otherwise */
   double dt0;          /* BODE_DT0_SCALAR */
   const double* dt0_v; /* BODE_DT0_ARRAY, (n,) */
   /* processing order (cost-sorted LPT queue); NULL = natural order */

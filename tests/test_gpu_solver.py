@@ -154,6 +154,17 @@ def test_constant_solution():
     assert np.array_equal(sol.ys[0], np.tile([3.0, -1.0], (3, 1)))
 
 
+def test_max_steps_bound():
+    """Per-instance step counters are 32-bit: max_steps >= 2^31 - 2 is
+    rejected (ValueError, BODE_EINVAL) instead of wrapping; the largest
+    accepted value solves normally."""
+    prob = _prob(np.array([[3.0, -1.0]]), t_eval=[np.array([0.0, 1.0])])
+    with pytest.raises(ValueError):
+        bode.solve(prob, bode.zero_dynamics(), max_steps=2 ** 31)
+    sol = bode.solve(prob, bode.zero_dynamics(), max_steps=16)
+    assert sol.status[0] == bode.SolveStatus.SUCCESS
+
+
 def test_exponential_accuracy_and_backward():
     sol = bode.solve(_prob(np.ones((1, 1)), t_eval=[np.array([1.0])]), bode.linear_dynamics(1.0),
                      tol=bode.Tolerances(1e-8, 1e-8))
