@@ -449,12 +449,15 @@ static __device__ unsigned g_exit_count;
 #ifndef BODE_BLOCKS_2D
 #define BODE_BLOCKS_2D 5
 #endif
+#ifndef BODE_BLOCKS_WIDE
+#define BODE_BLOCKS_WIDE 4
+#endif
 template <bool B>
 struct BoolTag {  // (no <type_traits> under NVRTC)
   static constexpr bool value = B;
 };
 template <int M, class F, class O, bool REC, bool PI>
-__global__ void __launch_bounds__(128, ((F::D <= 2 && (!REC || PI)) ? BODE_BLOCKS_2D : 4)) bode_persistent_kernel(const SolveParams P) {
+__global__ void __launch_bounds__(128, ((F::D <= 2 && (!REC || PI)) ? BODE_BLOCKS_2D : BODE_BLOCKS_WIDE)) bode_persistent_kernel(const SolveParams P) {
   extern __shared__ uint32_t s_refresh[];
   __shared__ PowTables s_pow;  // pow tables: divergent lookups, so shared not constant
   const int lane = threadIdx.x & 31;
