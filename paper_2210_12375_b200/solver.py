@@ -350,7 +350,8 @@ def solve(problem: IvpBatch, f, tableau=None, tol: Tolerances | None = None,
         pipeline_chunks = 3 if n >= 65536 else 1
         if cost_hint is not None and pipeline_chunks > 1:
             c = np.asarray(cost_hint, dtype=np.float64).reshape(-1)
-            smp = c[::max(1, c.size // 4096)]
+            # one strided gather, then max and mean on the contiguous copy
+            smp = np.ascontiguousarray(c[::max(1, c.size // 4096)])
             if smp.max() > smp.mean() * n / (_LANES * pipeline_chunks):
                 pipeline_chunks = 1
     a.pipeline_chunks = int(pipeline_chunks) if n >= 65536 else 1

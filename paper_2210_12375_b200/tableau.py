@@ -12,6 +12,7 @@ bit.  Any other (validated) tableau runs through a run-time specialisation
 of the same kernels with its coefficients compiled in (program.py).
 """
 
+import functools
 from dataclasses import dataclass
 
 import numpy as np
@@ -147,6 +148,13 @@ def heun() -> ButcherTableau:
     return _make("heun", _heun_data())
 
 
+@functools.lru_cache(maxsize=1)
+def _builtin_refs():
+    """The built-in pairs, constructed (and validated) once per process, not
+    on every solve() call."""
+    return (("dopri5", dopri5()), ("tsit5", tsit5()), ("heun", heun()))
+
+
 def method_of(tableau):
     """Device method for a tableau: the name of a built-in pair (compiled
     into libbode) when the coefficients equal one -- whatever object carries
@@ -161,8 +169,7 @@ def method_of(tableau):
     for k in ("stages", "a", "b", "b_err", "c", "order", "error_order", "interp_coeffs", "fsal"):
         if not hasattr(tableau, k):
             raise TypeError(f"tableau has no {k!r}: expected a ButcherTableau")
-    for name, make in (("dopri5", dopri5), ("tsit5", tsit5), ("heun", heun)):
-        ref = make()
+    for name, ref in _builtin_refs():
         if int(tableau.stages) == ref.stages and bool(tableau.fsal) == ref.fsal and \
                 int(tableau.order) == ref.order and int(tableau.error_order) == ref.error_order and \
                 all(np.array_equal(np.asarray(getattr(tableau, k), dtype=np.float64),
