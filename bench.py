@@ -471,7 +471,9 @@ def run_bode(args, rank, world, local_rank):
                 return bdist.solve_sharded(prob, dyn_h, **kw)
             return bode.solve(prob, dyn_h, **kw)
 
-        e2e_solve()
+        for _ in range(max(3, args.warmup)):  # untimed warm-up calls, as for `value`
+            del_sol = e2e_solve()
+            del del_sol
         if dist:
             dist.barrier()
         e2e_t, e2e_acc = [], 0
